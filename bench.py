@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: synchronous Downpour training samples/s on B200 (BASELINE.json).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A *step* is one synchronous Downpour round of the SPEC benchmark net
+`lstm(5,20,10),softmax(20,3)`: every worker gathers its batch of
+B=1000 samples from its HBM-resident shard, runs forward+loss+backward, the
+gradients are combined (sample-weighted mean), the master
+applies momentum SGD with whole-update non-finite rejection and every worker
+continues from the new weights.  One process per GPU; at N=1 the master and
+the single worker share GPU 0 and a round is one fused sm_100a kernel.
+
+Prints ONE JSON line (rank 0).  `value` is device-timed (CUDA events on the
+launching stream, inputs resident in HBM); `e2e` is the same metric through
+the C ABI with HOST batches (H2D of each round's batch and D2H of its loss
+inside the timed region).  The reference arm (`--impl reference`) runs the
+reference's own CPU code (oracle/_ref: nn.cpp/optim.cpp/transport.cpp + the
+SPEC roles over InprocHub) on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ARCH = "lstm(5,20,10),softmax(20,3)"
+FLOP_PER_SAMPLE = 102_760   # fwd 36,920 + bwd 65,840
+SGD_BYTES_PER_PARAM = 20    # read w, v, g; write w, v (fp32)
+WIDE_P = 16_881_699         # SURVEY §8 wide variant parameter count
+METRIC = "train samples/sec at 1/2/4/8 B200 (sync Downpour); % of roofline"
+UNIT = "samples/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 7:
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------------
+# reference arm: the reference's own CPU code (oracle/_ref)
+# --------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    ncores = os.cpu_count() or 1
+    W = max(1, min(ncores - 1, 96))
+    spec = O.data_spec(96, 9500)
+    cfg = O.train_cfg(n_workers=W, batch_size=args.batch, epochs=1000)
+    # each step = one sync round of W workers × B samples; bounded sample
+    steps = max(1, min(args.steps, args.ref_rounds))
+    sec, n = O.ref_bench_sync(ARCH, spec, cfg, max(1, args.warmup // 10), steps)
+    value = n / sec
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": steps, "warmup": max(1, args.warmup // 10),
+        "ms_per_step": 1e3 * sec / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "sync Downpour, lstm(5,20,10)+softmax(20,3), B=1000/worker",
+                   "workers": W, "batch_per_worker": args.batch, "dataset_files": 96,
+                   "samples_per_file": 9500},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": W + 1, "kind": "reference",
+                         "sample": f"{steps} timed sync rounds × {W} worker threads × "
+                                   f"B={args.batch} (reference nn/optim over InprocHub, "
+                                   f"1 master thread + {W} worker threads on {ncores} cores)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(args):
+    """oracle/_ref sync Downpour at the bench's own config (W=1, B=1000)."""
+    try:
+        from oracle import oracle as O
+        spec = O.data_spec(96, 9500)
+        cfg = O.train_cfg(n_workers=1, batch_size=args.batch, epochs=1000)
+        sec, n = O.ref_bench_sync(ARCH, spec, cfg, 2, args.cpu_rounds)
+        return {"value": n / sec, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"{args.cpu_rounds} sync rounds, 1 worker × B={args.batch} "
+                          "(reference nn.cpp/optim.cpp over InprocHub; 1 busy core + idle "
+                          "master thread)"}
+    except Exception as e:  # reported, never fatal
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import paper_1712_05878_b200 as g
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("multi-GPU sync rounds need the NCCL exchange (ghc_comm_*); "
+                         "run with --gpus 1")
+    ctx = g.Context(local)
+    arch = g.Architecture(ctx, ARCH)
+    B = args.batch
+    P = arch.n_params
+
+    # dataset: DatasetSpec{96 files × 9500, T=10, D=5, K=3, δ=5, seed 1234}
+    # (SURVEY §8(d)); the single worker's shard = all 96 files = 182 MB f32,
+    # larger than the 126 MB L2, and every round gathers a fresh shuffled batch.
+    t0 = time.time()
+    spec = g.data_spec(96, 9500)
+    x, y = g.generate(spec)
+    total_rounds = args.warmup + args.steps
+    per_epoch = x.shape[0] // B
+    epochs = (total_rounds + per_epoch - 1) // per_epoch
+    stream = []
+    for e in range(epochs):
+        idx = g.epoch_indices(spec, 1, 0, e, 99)
+        stream.extend(idx[i:i + B] for i in range(0, per_epoch * B, B))
+    idx = np.concatenate(stream[:total_rounds]).astype(np.int32)
+    dx, dy, di = ctx.upload(x), ctx.upload(y), ctx.upload(idx)
+    setup_s = time.time() - t0
+
+    w0 = g.init_weights(arch, 7)
+    m = g.Master(arch, w0, 0.01, 0.9)
+    loss = ctx.array(total_rounds)
+
+    # warm-up rounds (untimed)
+    m.sync_rounds(dx, dy, di, B, B, args.warmup, loss_out=loss)
+    ctx.sync()
+
+    # ---- timed: K rounds, device-resident roles loop (one persistent launch
+    # per `chunk` rounds) ----
+    chunk = args.chunk if args.chunk > 0 else args.steps
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        ctx.sync()
+        ctx.timer_start()
+        done = 0
+        while done < args.steps:
+            r = min(chunk, args.steps - done)
+            m.sync_rounds(dx, dy, di, B, B, r, loss_out=loss, idx_offset=(args.warmup + done) * B,
+                          loss_offset=args.warmup + done)
+            done += r
+        ms = ctx.timer_stop()
+        ctx.sync()
+    launches = ctx.launches - launches0
+    _, _, version, rejected = m.read()
+    losses = loss.numpy() / B
+
+    # ---- kernel-level: one round per launch, CUDA events per launch ----
+    per_launch_ms = []
+    for k in range(min(args.steps, 200)):
+        ctx.timer_start()
+        m.sync_rounds(dx, dy, di, B, B, 1, idx_offset=(k % total_rounds) * B)
+        per_launch_ms.append(ctx.timer_stop())
+    per_launch_ms.sort()
+    one_round_ms = statistics.median(per_launch_ms)
+
+    # ---- e2e: host batches through the C ABI, H2D + round + D2H per step ----
+    e2e = run_e2e(args, g, ctx, arch, x, y, idx)
+
+    # ---- update path on the wide-variant parameter count (HBM roofline) ----
+    upd = update_roofline(args, g, ctx)
+
+    pk, pk_kind = peaks()
+    steps_s = ms / 1e3
+    value = world * B * args.steps / steps_s
+    flops_per_round = B * FLOP_PER_SAMPLE
+    achieved_tflops = flops_per_round * args.steps / steps_s / 1e12
+    tensor_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) / 2.0  # TF32 ≈ ½ bf16
+    fp32_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SPEC generator, 96 files x 9500 samples, delta=5)",
+        "config": {"workload": "c2 sync Downpour, 1 master + 1 worker per GPU, "
+                               "lstm(5,20,10)+softmax(20,3), B=1000/worker",
+                   "global_batch": B * world, "seq_len": 10, "parallelism": f"dp{world}",
+                   "rounds_per_launch": chunk,
+                   "l2": "inputs larger than L2: 182 MB shard/GPU > 126 MB L2, fresh "
+                         "shuffled batch gathered every round"},
+        "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tensor_peak,
+                     "unit": "TFLOP/s", "frac": achieved_tflops / tensor_peak,
+                     "traffic": args.traffic,
+                     "kernel": "lstm_softmax_step<D5,H20,T10,K3> (fused fwd+bwd+reduce+SGD)",
+                     "peak_kind": f"{pk_kind} bf16 sustained / 2 (TF32)",
+                     "fp32_core": {"peak": fp32_peak,
+                                   "frac": achieved_tflops / fp32_peak,
+                                   "note": "the kernel is FFMA/MUFU/latency-bound by design "
+                                           "(DESIGN.md §Kernels)"},
+                     "one_round_launch_ms": one_round_ms},
+        "cpu_baseline": cpu_baseline(args) if (rank == 0 and not args.no_cpu) else None,
+        "e2e": e2e,
+        "update_kernel": upd,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "training": {"version": version, "rejected": rejected,
+                     "loss_first": float(losses[0]), "loss_last": float(losses[-1])},
+        "setup_s": setup_s,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_e2e(args, g, ctx, arch, x, y, idx):
+    """Same metric through the C ABI with HOST batches: per step the batch is
+    copied from pinned host memory, one sync round runs, and the round's loss
+    is copied back; no host sync between steps."""
+    import ctypes as C
+    from paper_1712_05878_b200 import _lib
+    lib = _lib.load()
+    B = args.batch
+    K = min(args.steps, args.e2e_steps)
+    width = x.shape[1]
+    xb_bytes = B * width * 4
+    yb_bytes = B * 4
+    hp = C.c_void_p()
+    _lib.check(lib.ghc_host_alloc(K * (xb_bytes + yb_bytes) + K * 4, C.byref(hp)))
+    base = hp.value
+    hx = np.ctypeslib.as_array((C.c_float * (K * B * width)).from_address(base)).reshape(K, B, width)
+    hy = np.ctypeslib.as_array((C.c_int32 * (K * B)).from_address(base + K * xb_bytes)).reshape(K, B)
+    hl = np.ctypeslib.as_array((C.c_float * K).from_address(base + K * (xb_bytes + yb_bytes)))
+    for k in range(K):
+        sel = idx[k * B:(k + 1) * B]
+        hx[k] = x[sel]
+        hy[k] = y[sel]
+    w0 = g.init_weights(arch, 7)
+    m = g.Master(arch, w0, 0.01, 0.9)
+    dxb = ctx.array((B, width))
+    dyb = ctx.array(B, np.int32)
+    dl = ctx.array(1)
+    for k in range(3):  # warm-up
+        m.sync_rounds(dxb, dyb, None, 0, B, 1, loss_out=dl)
+    ctx.sync()
+    ctx.timer_start()
+    for k in range(K):
+        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dxb.ptr, C.c_void_p(base + k * xb_bytes), xb_bytes))
+        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dyb.ptr, C.c_void_p(base + K * xb_bytes + k * yb_bytes),
+                                      yb_bytes))
+        m.sync_rounds(dxb, dyb, None, 0, B, 1, loss_out=dl)
+        _lib.check(lib.ghc_memcpy_d2h(ctx.h, C.c_void_p(base + K * (xb_bytes + yb_bytes) + 4 * k),
+                                      dl.ptr, 4))
+    ms = ctx.timer_stop()
+    ctx.sync()
+    ok = bool(np.isfinite(hl).all())
+    lib.ghc_host_free(hp)
+    return {"value": B * K / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": xb_bytes + yb_bytes,
+            "d2h_bytes_per_step": 4, "steps": K, "ms_per_step": ms / K, "losses_finite": ok,
+            "path": "ghc_memcpy_h2d(batch) + ghc_master_sync_rounds(1 round) + "
+                    "ghc_memcpy_d2h(loss) per step, pinned host buffers, one stream"}
+
+
+def update_roofline(args, g, ctx):
+    """ghc_sgd_apply (optim.cpp:39-65) at the wide variant's P: HBM roofline."""
+    import ctypes as C
+    P = WIDE_P
+    rng = np.random.default_rng(0)
+    w = ctx.upload(rng.normal(size=P).astype(np.float32))
+    v = ctx.upload(np.zeros(P, np.float32))
+    gr = ctx.upload((rng.normal(size=P) * 1e-3).astype(np.float32))
+    st = ctx.array(1, np.int32)
+    flush = ctx.array(64 << 20)  # 256 MB > L2: evict between launches
+    times = []
+    for it in range(23):
+        flush.zero()
+        ctx.timer_start()
+        g.gradhub.check(ctx.lib.ghc_sgd_apply(ctx.h, w.ptr, v.ptr, gr.ptr, P, 0.01, 0.9, st.ptr,
+                                              None))
+        t = ctx.timer_stop()
+        if it >= 3:
+            times.append(t)
+    t = statistics.median(times)
+    gbs = SGD_BYTES_PER_PARAM * P / (t / 1e3) / 1e9
+    pk, kind = peaks()
+    return {"kernel": "sgd_apply_kernel", "P": P, "ms": t, "achieved_gbs": gbs,
+            "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"], "bytes_per_param": 20,
+            "peak_kind": kind, "l2": "256 MB flush before every launch"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1000)
+    ap.add_argument("--chunk", type=int, default=0, help="rounds per persistent launch (0=all)")
+    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--cpu-rounds", type=int, default=120)
+    ap.add_argument("--ref-rounds", type=int, default=40)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes/launch from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

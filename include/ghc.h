@@ -1,0 +1,209 @@
+/*
+ * ghc.h — C ABI of the B200-native Downpour/EASGD hot path ("gradhub-cuda").
+ *
+ * The drop-in boundary for arXiv 1712.05878's reference (`gradhub`,
+ * /root/reference/proj): the reference's C++ Model / Algo / Data interfaces
+ * and master/worker loop stay the caller-facing API (see INTEGRATION.md for
+ * the C++ shim a maintainer adds); underneath them every compute step runs
+ * as a hand-written sm_100a kernel behind these extern "C" entry points.
+ *
+ *  - plain pointers and sizes only; no C++ or torch types cross the ABI;
+ *  - device pointers are `d_*`, host pointers `h_*`; sizes in elements;
+ *  - every call is stream-ordered on the context's CUDA stream and
+ *    asynchronous unless it says otherwise; ghc_ctx_sync() is the explicit
+ *    sync point;
+ *  - errors never throw: each call returns a ghc_status that maps 1:1 onto
+ *    the reference exception classes (errors.hpp:10-45); ghc_last_error()
+ *    returns the thread's last message.  There is no CPU fallback: on a host
+ *    without a usable sm_100 device ghc_ctx_create fails with GHC_ERR_CUDA.
+ *
+ * Reference interface each entry point replaces is cited per function.
+ */
+#ifndef GHC_H
+#define GHC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ghc_status {
+  GHC_OK = 0,
+  GHC_ERR_SHAPE = 1,          /* ShapeError              errors.hpp:10-14 */
+  GHC_ERR_NONFINITE = 2,      /* NonFiniteGradientError  errors.hpp:16-21 */
+  GHC_ERR_CACHE_MISMATCH = 3, /* CacheMismatchError      errors.hpp:23-27 */
+  GHC_ERR_CONFIG = 4,         /* ConfigError             errors.hpp:29-32 */
+  GHC_ERR_TRANSPORT = 5,      /* TransportError          errors.hpp:34-38 */
+  GHC_ERR_PROTOCOL = 6,       /* ProtocolError           errors.hpp:40-45 */
+  GHC_ERR_CUDA = 7,           /* CUDA runtime / launch failure (new)       */
+  GHC_ERR_NCCL = 8            /* NCCL failure (new)                         */
+} ghc_status;
+
+typedef struct ghc_ctx ghc_ctx;       /* one per (GPU, host thread): stream + scratch */
+typedef struct ghc_plan ghc_plan;     /* Architecture compiled to a kernel plan      */
+typedef struct ghc_master ghc_master; /* device-resident master state (w, v, version) */
+
+const char* ghc_version(void);
+const char* ghc_last_error(void);
+const char* ghc_status_name(ghc_status s);
+
+/* ------------------------------------------------------------------ */
+/* Context, memory, timing                                            */
+/* ------------------------------------------------------------------ */
+ghc_status ghc_device_count(int* n);
+ghc_status ghc_ctx_create(int device, ghc_ctx** out);
+void ghc_ctx_destroy(ghc_ctx* ctx);
+ghc_status ghc_ctx_sync(ghc_ctx* ctx);
+int ghc_ctx_num_sms(const ghc_ctx* ctx);
+/* Kernel launches this context issued so far (evidence for the bench). */
+uint64_t ghc_ctx_launch_count(const ghc_ctx* ctx);
+ghc_status ghc_malloc(ghc_ctx* ctx, size_t bytes, void** d_ptr);
+ghc_status ghc_free(ghc_ctx* ctx, void* d_ptr);
+ghc_status ghc_host_alloc(size_t bytes, void** h_ptr); /* pinned */
+ghc_status ghc_host_free(void* h_ptr);
+ghc_status ghc_memcpy_h2d(ghc_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);
+ghc_status ghc_memcpy_d2h(ghc_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
+ghc_status ghc_memcpy_d2d(ghc_ctx* ctx, void* d_dst, const void* d_src, size_t bytes);
+ghc_status ghc_memset(ghc_ctx* ctx, void* d_dst, int value, size_t bytes);
+/* CUDA-event timer on the context stream: start, then stop returns ms. */
+ghc_status ghc_timer_start(ghc_ctx* ctx);
+ghc_status ghc_timer_stop(ghc_ctx* ctx, float* ms);
+
+/* ------------------------------------------------------------------ */
+/* Model: Architecture (arch.hpp:36-57) → kernel plan                 */
+/* ------------------------------------------------------------------ */
+/* Grammar of parse_architecture (arch.hpp:54-57, arch.cpp:173-214):
+ * "lstm(D,H,T),dense(i,o,act)*,softmax(i,K)"; validated as arch.cpp:26-73. */
+ghc_status ghc_plan_create(ghc_ctx* ctx, const char* arch_text, ghc_plan** out);
+void ghc_plan_destroy(ghc_plan* plan);
+int64_t ghc_plan_n_params(const ghc_plan* plan);   /* Architecture::n_params  arch.cpp:114 */
+int64_t ghc_plan_input_width(const ghc_plan* plan); /* Architecture::input_width arch.cpp:75 */
+int32_t ghc_plan_n_classes(const ghc_plan* plan);   /* Architecture::n_classes arch.cpp:83 */
+/* Parameter tensors in weight-set order (arch.cpp:95-112). */
+ghc_status ghc_plan_tensors(const ghc_plan* plan, int64_t* offset, int64_t* dim0,
+                            int64_t* dim1, int cap, int* n_tensors);
+/* Name of the fused kernel the plan dispatches to (diagnostics). */
+const char* ghc_plan_kernel_name(const ghc_plan* plan);
+
+/* Host-only architecture check (no device needed): parse + validate and
+ * report the sizes; GHC_ERR_CONFIG with the reference's message on error. */
+ghc_status ghc_arch_info(const char* arch_text, int64_t* n_params, int64_t* input_width,
+                         int32_t* n_classes);
+/* init_weights from the architecture text (host only). */
+ghc_status ghc_init_weights_text(const char* arch_text, uint64_t seed, double* h_w);
+
+/* init_weights (nn.cpp:83-98), host-side and bit-identical to the reference
+ * (mt19937_64 + Glorot-uniform bounds).  h_w: n_params doubles. */
+ghc_status ghc_init_weights(const ghc_plan* plan, uint64_t seed, double* h_w);
+
+/* ------------------------------------------------------------------ */
+/* Worker minibatch step: forward (nn.cpp:100-232) + loss (nn.cpp:     */
+/* 234-248) + backward (nn.cpp:250-399) fused in one launch.          */
+/* ------------------------------------------------------------------ */
+/* d_grad[P] = grad_scale * Σ_s ∂ℓ_s/∂w   (grad_scale = 1/n reproduces the
+ *                                        reference's batch mean, nn.cpp:283-297)
+ * d_loss_sum[0] = Σ_s ℓ_s                 (loss() = d_loss_sum / n)
+ * Samples: rows d_x[s] / d_y[s] for s < n when d_idx == NULL, otherwise the
+ * rows d_idx[s] of a device-resident dataset (d_x, d_y).  Labels outside
+ * [0,K) → GHC_ERR_SHAPE (nn.cpp:241-244, checked on the host copy only when
+ * validate_labels != 0, since that costs a device→host read).
+ * Deterministic: fixed reduction order, bit-identical across repeats. */
+ghc_status ghc_worker_grad(ghc_plan* plan, const float* d_w, const float* d_x,
+                           const int32_t* d_y, const int32_t* d_idx, int64_t n,
+                           float grad_scale, float* d_grad, float* d_loss_sum);
+
+/* Forward only: class probabilities d_probs[n×K] (nullable) and loss sum. */
+ghc_status ghc_forward(ghc_plan* plan, const float* d_w, const float* d_x,
+                       const int32_t* d_y, const int32_t* d_idx, int64_t n,
+                       float* d_probs, float* d_loss_sum);
+
+/* ------------------------------------------------------------------ */
+/* Algo (optim.cpp) on device buffers                                  */
+/* ------------------------------------------------------------------ */
+/* sgd_step (optim.cpp:39-65): v = mu*v - lr*g; w += v, in place.  If any
+ * g is non-finite the WHOLE update is rejected (optim.cpp:49-51): w, v stay
+ * untouched, *d_status = GHC_ERR_NONFINITE (else GHC_OK) and *d_version is
+ * not incremented.  Hyper-parameters validated as optim.cpp:20-29.  One
+ * launch, no host sync (the status lands in device memory). */
+ghc_status ghc_sgd_apply(ghc_ctx* ctx, float* d_w, float* d_v, const float* d_g,
+                         int64_t p, float lr, float mu, int32_t* d_status,
+                         uint64_t* d_version);
+/* elastic_pull (optim.cpp:67-80): w -= alpha*(w - c). */
+ghc_status ghc_elastic_pull(ghc_ctx* ctx, float* d_w, const float* d_c, int64_t p,
+                            float alpha);
+/* easgd_worker_step (optim.cpp:82-105): w -= lr*g; pull toward c when
+ * batch_index % tau == 0.  Non-finite g → *d_status = GHC_ERR_NONFINITE and
+ * w untouched. */
+ghc_status ghc_easgd_worker_step(ghc_ctx* ctx, float* d_w, const float* d_c,
+                                 const float* d_g, int64_t p, float lr, float alpha,
+                                 uint64_t tau, uint64_t batch_index, int32_t* d_status);
+/* easgd_center_step (optim.cpp:107-123): c += alpha*(w - c); version += 1.
+ * alpha validated in (0,1) (optim.cpp:31-37). */
+ghc_status ghc_easgd_center_step(ghc_ctx* ctx, float* d_c, const float* d_w, int64_t p,
+                                 float alpha, uint64_t* d_version);
+/* Sync-round combine: out = Σ_i c_i * slot_i / Σ_i c_i in
+ * slot (rank) order; slots are contiguous [W][P]. */
+ghc_status ghc_weighted_mean(ghc_ctx* ctx, float* d_out, const float* d_slots,
+                             const double* h_counts, int32_t n_slots, int64_t p);
+
+/* ------------------------------------------------------------------ */
+/* Master: device-resident Downpour master state + fused sync rounds   */
+/* ------------------------------------------------------------------ */
+/* Holds w and v double-buffered in HBM, the version counter and the
+ * commit/reject flag; the update of round r is committed on device only if
+ * its combined gradient is finite, with no host sync. */
+ghc_status ghc_master_create(ghc_plan* plan, const double* h_w0, float lr, float mu,
+                             ghc_master** out);
+void ghc_master_destroy(ghc_master* m);
+/* Current weights / velocity (device pointers valid until the next round). */
+ghc_status ghc_master_weights(ghc_master* m, float** d_w, float** d_v);
+ghc_status ghc_master_read(ghc_master* m, float* h_w, float* h_v, uint64_t* version,
+                           uint64_t* rejected);
+/* n_rounds synchronous Downpour rounds of ONE worker colocated with the
+ * master (1 master + 1 worker per GPU) in ONE persistent
+ * launch: per round gather the batch d_idx[r*stride ..] from the resident
+ * dataset, forward+loss+backward, deterministic cross-CTA gradient reduce,
+ * finite check, sgd_step, commit.  d_counts[r] = samples in round r
+ * (nullable → n each).  d_loss_out[r] = loss sum of round r (nullable). */
+ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t* d_y,
+                                  const int32_t* d_idx, int64_t stride,
+                                  const int32_t* d_counts, int64_t n, int32_t n_rounds,
+                                  float* d_loss_out);
+/* Apply a combined gradient produced elsewhere (NCCL reduce, virtual workers):
+ * d_g[P] is the already-combined gradient. */
+ghc_status ghc_master_apply(ghc_master* m, const float* d_g);
+
+/* ------------------------------------------------------------------ */
+/* Data layer, host side, bit-identical to the oracle */
+/* ------------------------------------------------------------------ */
+typedef struct ghc_data_spec {
+  int32_t n_files;
+  int32_t samples_per_file;
+  int32_t seq_len;
+  int32_t input_dim;
+  int32_t n_classes;
+  int32_t pad_;
+  double delta;
+  uint64_t seed;
+} ghc_data_spec;
+
+/* generate_synthetic for files [f0, f0+nf): rows of seq_len*input_dim f32
+ * (the on-disk/wire precision) + labels. */
+ghc_status ghc_data_generate(const ghc_data_spec* spec, int32_t f0, int32_t nf,
+                             float* h_x, int32_t* h_y);
+/* shard_files. */
+ghc_status ghc_data_shard(int32_t n_files, int32_t n_workers, int32_t worker,
+                          int32_t* first_file, int32_t* n_files_out);
+/* batches: the epoch permutation of worker's shard as
+ * GLOBAL sample indices; returns the count in *count. */
+ghc_status ghc_data_epoch_indices(const ghc_data_spec* spec, int32_t n_workers,
+                                  int32_t worker, int32_t epoch, uint64_t shuffle_seed,
+                                  int32_t shuffle, int64_t* h_out, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GHC_H */

@@ -1,0 +1,135 @@
+"""ctypes binding of libghc.so (include/ghc.h).
+
+Fails loudly: importing the product on a host where the in-tree library was
+not built raises; every non-OK status raises the matching reference error
+class (errors.hpp:10-45).  There is no CPU fallback anywhere in the package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libghc.so")
+
+
+class GradhubError(RuntimeError):
+    """Base of the reference exception taxonomy."""
+
+
+class ShapeError(GradhubError):            # errors.hpp:10-14
+    pass
+
+
+class NonFiniteGradientError(GradhubError):  # errors.hpp:16-21
+    pass
+
+
+class CacheMismatchError(GradhubError):    # errors.hpp:23-27
+    pass
+
+
+class ConfigError(GradhubError):           # errors.hpp:29-32
+    pass
+
+
+class TransportError(GradhubError):        # errors.hpp:34-38
+    pass
+
+
+class ProtocolError(GradhubError):         # errors.hpp:40-45
+    pass
+
+
+class CudaError(GradhubError):
+    pass
+
+
+class NcclError(GradhubError):
+    pass
+
+
+_STATUS = {1: ShapeError, 2: NonFiniteGradientError, 3: CacheMismatchError, 4: ConfigError,
+           5: TransportError, 6: ProtocolError, 7: CudaError, 8: NcclError}
+
+# Every symbol include/ghc.h declares: (name, restype, argtypes)
+_vp, _i32, _i64, _u64, _f32, _sz, _cp = (C.c_void_p, C.c_int32, C.c_int64, C.c_uint64,
+                                         C.c_float, C.c_size_t, C.c_char_p)
+SIGNATURES = [
+    ("ghc_version", _cp, []),
+    ("ghc_last_error", _cp, []),
+    ("ghc_status_name", _cp, [C.c_int]),
+    ("ghc_device_count", C.c_int, [_vp]),
+    ("ghc_ctx_create", C.c_int, [C.c_int, _vp]),
+    ("ghc_ctx_destroy", None, [_vp]),
+    ("ghc_ctx_sync", C.c_int, [_vp]),
+    ("ghc_ctx_num_sms", C.c_int, [_vp]),
+    ("ghc_ctx_launch_count", _u64, [_vp]),
+    ("ghc_malloc", C.c_int, [_vp, _sz, _vp]),
+    ("ghc_free", C.c_int, [_vp, _vp]),
+    ("ghc_host_alloc", C.c_int, [_sz, _vp]),
+    ("ghc_host_free", C.c_int, [_vp]),
+    ("ghc_memcpy_h2d", C.c_int, [_vp, _vp, _vp, _sz]),
+    ("ghc_memcpy_d2h", C.c_int, [_vp, _vp, _vp, _sz]),
+    ("ghc_memcpy_d2d", C.c_int, [_vp, _vp, _vp, _sz]),
+    ("ghc_memset", C.c_int, [_vp, _vp, C.c_int, _sz]),
+    ("ghc_timer_start", C.c_int, [_vp]),
+    ("ghc_timer_stop", C.c_int, [_vp, _vp]),
+    ("ghc_plan_create", C.c_int, [_vp, _cp, _vp]),
+    ("ghc_plan_destroy", None, [_vp]),
+    ("ghc_plan_n_params", _i64, [_vp]),
+    ("ghc_plan_input_width", _i64, [_vp]),
+    ("ghc_plan_n_classes", _i32, [_vp]),
+    ("ghc_plan_tensors", C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
+    ("ghc_plan_kernel_name", _cp, [_vp]),
+    ("ghc_arch_info", C.c_int, [_cp, _vp, _vp, _vp]),
+    ("ghc_init_weights_text", C.c_int, [_cp, _u64, _vp]),
+    ("ghc_init_weights", C.c_int, [_vp, _u64, _vp]),
+    ("ghc_worker_grad", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _vp, _vp]),
+    ("ghc_forward", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    ("ghc_sgd_apply", C.c_int, [_vp, _vp, _vp, _vp, _i64, _f32, _f32, _vp, _vp]),
+    ("ghc_elastic_pull", C.c_int, [_vp, _vp, _vp, _i64, _f32]),
+    ("ghc_easgd_worker_step", C.c_int, [_vp, _vp, _vp, _vp, _i64, _f32, _f32, _u64, _u64, _vp]),
+    ("ghc_easgd_center_step", C.c_int, [_vp, _vp, _vp, _i64, _f32, _vp]),
+    ("ghc_weighted_mean", C.c_int, [_vp, _vp, _vp, _vp, _i32, _i64]),
+    ("ghc_master_create", C.c_int, [_vp, _vp, _f32, _f32, _vp]),
+    ("ghc_master_destroy", None, [_vp]),
+    ("ghc_master_weights", C.c_int, [_vp, _vp, _vp]),
+    ("ghc_master_read", C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    ("ghc_master_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp]),
+    ("ghc_master_apply", C.c_int, [_vp, _vp]),
+    ("ghc_data_generate", C.c_int, [_vp, _i32, _i32, _vp, _vp]),
+    ("ghc_data_shard", C.c_int, [_i32, _i32, _i32, _vp, _vp]),
+    ("ghc_data_epoch_indices", C.c_int, [_vp, _i32, _i32, _i32, _u64, _i32, _vp, _vp]),
+]
+
+_lib = None
+
+
+def load():
+    """Load the in-tree libghc.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1712_05878_b200.build` "
+                              "(no CPU fallback exists)")
+        lib = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status != 0:
+        msg = load().ghc_last_error().decode(errors="replace")
+        raise _STATUS.get(status, GradhubError)(f"{what}: {msg}" if what else msg)
+
+
+class DataSpec(C.Structure):
+    """ghc_data_spec (SPEC.md:421-423 DatasetSpec)."""
+    _fields_ = [("n_files", C.c_int32), ("samples_per_file", C.c_int32),
+                ("seq_len", C.c_int32), ("input_dim", C.c_int32), ("n_classes", C.c_int32),
+                ("pad_", C.c_int32), ("delta", C.c_double), ("seed", C.c_uint64)]

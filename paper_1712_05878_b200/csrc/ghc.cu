@@ -1,0 +1,639 @@
+// ghc.cu — C ABI (include/ghc.h) of the B200-native Downpour/EASGD hot path.
+//
+// Host glue only: argument checking with the reference's error taxonomy,
+// kernel selection per Architecture, launch geometry sized to the SM count,
+// cooperative launches for the kernels that carry a grid barrier.  All math
+// runs in the sm_100a kernels of lstm_step.cuh / update_kernels.cuh; there is
+// no CPU compute path.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ghc.h"
+#include "host_model.hpp"
+#include "lstm_step.cuh"
+#include "update_kernels.cuh"
+
+using namespace ghc;
+
+namespace {
+
+thread_local std::string g_err;
+
+ghc_status fail(ghc_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CU(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(GHC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+// ---- fused LSTM→softmax kernel table (one instantiation per shape) ----
+struct LstmEntry {
+  int D, H, T, K;
+  void (*fn)(StepArgs);
+  int P, ppad;
+  size_t (*smem)(int);
+  const char* name;
+};
+
+template <int D, int H, int T, int K>
+LstmEntry make_entry(const char* name) {
+  using N = LstmNet<D, H, T, K>;
+  return LstmEntry{D, H, T, K, &lstm_softmax_step_kernel<D, H, T, K>, N::P, N::PPAD,
+                   &N::smem_bytes, name};
+}
+
+const std::vector<LstmEntry>& lstm_table() {
+  static const std::vector<LstmEntry> t = {
+      make_entry<5, 20, 10, 3>("lstm_softmax_step<D5,H20,T10,K3>"),  // SPEC.md:109 bench net
+      make_entry<5, 8, 10, 3>("lstm_softmax_step<D5,H8,T10,K3>"),
+      make_entry<3, 4, 5, 3>("lstm_softmax_step<D3,H4,T5,K3>"),
+      make_entry<2, 16, 3, 4>("lstm_softmax_step<D2,H16,T3,K4>"),
+      make_entry<5, 32, 10, 3>("lstm_softmax_step<D5,H32,T10,K3>"),
+      make_entry<4, 12, 6, 5>("lstm_softmax_step<D4,H12,T6,K5>"),
+  };
+  return t;
+}
+
+}  // namespace
+
+struct ghc_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::atomic<uint64_t> launches{0};
+};
+
+struct ghc_plan {
+  ghc_ctx* ctx = nullptr;
+  Model model;
+  const LstmEntry* lstm = nullptr;
+  int max_ctas = 0;       // co-resident CTAs of the fused kernel
+  float* part = nullptr;  // [max_ctas][ppad]
+  MasterDev* ms = nullptr;  // scratch barrier state for grad/fwd launches
+  int* err = nullptr;
+  std::string kname;
+};
+
+struct ghc_master {
+  ghc_plan* plan = nullptr;
+  float* w[2] = {nullptr, nullptr};
+  float* v[2] = {nullptr, nullptr};
+  MasterDev* ms = nullptr;
+  MasterDev* ms_apply = nullptr;  // barrier state for ghc_master_apply
+  float lr = 0.01f, mu = 0.0f;
+  int64_t P = 0;
+};
+
+namespace {
+
+// Launch geometry of the fused step: ≈ one CTA per SM, one warp per sample.
+void step_geometry(const ghc_plan* p, int64_t n, int& ctas, int& warps) {
+  const int sms = p->ctx->num_sms;
+  warps = static_cast<int>((n + sms - 1) / sms);
+  if (warps < 1) warps = 1;
+  if (warps > 8) warps = 8;
+  int64_t c = (n + warps - 1) / warps;
+  if (c < 1) c = 1;
+  if (c > p->max_ctas) c = p->max_ctas;
+  ctas = static_cast<int>(c);
+}
+
+ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
+  if (!p->lstm) return fail(GHC_ERR_CONFIG, "plan has no fused worker kernel");
+  int ctas, warps;
+  step_geometry(p, n_max, ctas, warps);
+  a.part = p->part;
+  a.pstride = p->lstm->ppad;
+  a.err = p->err;
+  const size_t smem = p->lstm->smem(warps);
+  void* args[] = {&a};
+  CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(p->lstm->fn), dim3(ctas),
+                                 dim3(warps * 32), args, smem, p->ctx->stream));
+  p->ctx->launches++;
+  return GHC_OK;
+}
+
+int occupancy_grid(ghc_ctx* c, const void* fn, int threads) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * c->num_sms;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ghc_version(void) { return "gradhub-cuda 0.1 (sm_100a)"; }
+const char* ghc_last_error(void) { return g_err.c_str(); }
+const char* ghc_status_name(ghc_status s) {
+  switch (s) {
+    case GHC_OK: return "OK";
+    case GHC_ERR_SHAPE: return "ShapeError";
+    case GHC_ERR_NONFINITE: return "NonFiniteGradientError";
+    case GHC_ERR_CACHE_MISMATCH: return "CacheMismatchError";
+    case GHC_ERR_CONFIG: return "ConfigError";
+    case GHC_ERR_TRANSPORT: return "TransportError";
+    case GHC_ERR_PROTOCOL: return "ProtocolError";
+    case GHC_ERR_CUDA: return "CudaError";
+    case GHC_ERR_NCCL: return "NcclError";
+  }
+  return "?";
+}
+
+ghc_status ghc_device_count(int* n) {
+  CU(cudaGetDeviceCount(n));
+  return GHC_OK;
+}
+
+ghc_status ghc_ctx_create(int device, ghc_ctx** out) {
+  int n = 0;
+  CU(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(GHC_ERR_CUDA, "no such CUDA device");
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(GHC_ERR_CUDA, std::string("libghc is built for sm_100a; device is ") + prop.name);
+  CU(cudaSetDevice(device));
+  auto* c = new ghc_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CU(cudaEventCreate(&c->ev0));
+  CU(cudaEventCreate(&c->ev1));
+  *out = c;
+  return GHC_OK;
+}
+
+void ghc_ctx_destroy(ghc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaEventDestroy(c->ev0);
+  cudaEventDestroy(c->ev1);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+ghc_status ghc_ctx_sync(ghc_ctx* c) {
+  CU(cudaStreamSynchronize(c->stream));
+  return GHC_OK;
+}
+int ghc_ctx_num_sms(const ghc_ctx* c) { return c->num_sms; }
+uint64_t ghc_ctx_launch_count(const ghc_ctx* c) { return c->launches.load(); }
+
+ghc_status ghc_malloc(ghc_ctx* c, size_t bytes, void** d) {
+  CU(cudaSetDevice(c->device));
+  CU(cudaMalloc(d, bytes ? bytes : 16));
+  return GHC_OK;
+}
+ghc_status ghc_free(ghc_ctx* c, void* d) {
+  CU(cudaSetDevice(c->device));
+  CU(cudaFree(d));
+  return GHC_OK;
+}
+ghc_status ghc_host_alloc(size_t bytes, void** h) {
+  CU(cudaMallocHost(h, bytes ? bytes : 16));
+  return GHC_OK;
+}
+ghc_status ghc_host_free(void* h) {
+  CU(cudaFreeHost(h));
+  return GHC_OK;
+}
+ghc_status ghc_memcpy_h2d(ghc_ctx* c, void* d, const void* h, size_t bytes) {
+  CU(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream));
+  return GHC_OK;
+}
+ghc_status ghc_memcpy_d2h(ghc_ctx* c, void* h, const void* d, size_t bytes) {
+  CU(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+  return GHC_OK;
+}
+ghc_status ghc_memcpy_d2d(ghc_ctx* c, void* d, const void* s, size_t bytes) {
+  CU(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  return GHC_OK;
+}
+ghc_status ghc_memset(ghc_ctx* c, void* d, int v, size_t bytes) {
+  CU(cudaMemsetAsync(d, v, bytes, c->stream));
+  return GHC_OK;
+}
+ghc_status ghc_timer_start(ghc_ctx* c) {
+  CU(cudaEventRecord(c->ev0, c->stream));
+  return GHC_OK;
+}
+ghc_status ghc_timer_stop(ghc_ctx* c, float* ms) {
+  CU(cudaEventRecord(c->ev1, c->stream));
+  CU(cudaEventSynchronize(c->ev1));
+  CU(cudaEventElapsedTime(ms, c->ev0, c->ev1));
+  return GHC_OK;
+}
+
+// ---------------------------------------------------------------- plan
+ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
+  if (!c || !arch_text || !out) return fail(GHC_ERR_CONFIG, "null argument");
+  auto* p = new ghc_plan();
+  p->ctx = c;
+  try {
+    p->model = parse_model(arch_text);
+  } catch (const std::exception& e) {
+    delete p;
+    return fail(GHC_ERR_CONFIG, e.what());
+  }
+  const auto& L = p->model.layers;
+  if (L.size() == 2 && L[0].kind == LayerKind::lstm && L[1].kind == LayerKind::softmax) {
+    for (const LstmEntry& e : lstm_table())
+      if (e.D == L[0].a && e.H == L[0].b && e.T == L[0].c && e.K == L[1].b) p->lstm = &e;
+  }
+  if (!p->lstm) {
+    const std::string txt = arch_text;
+    delete p;
+    return fail(GHC_ERR_CONFIG, "no sm_100a kernel instantiated for architecture '" + txt +
+                                    "' (see DESIGN.md §Kernels for the supported shapes)");
+  }
+  p->kname = p->lstm->name;
+  CU(cudaSetDevice(c->device));
+  // co-residency of the cooperative fused kernel at the largest block (8 warps)
+  int per_sm = 0;
+  CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(p->lstm->fn),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(p->lstm->smem(8))));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, reinterpret_cast<const void*>(p->lstm->fn), 256, p->lstm->smem(8)));
+  if (per_sm < 1) {
+    delete p;
+    return fail(GHC_ERR_CUDA, "fused kernel cannot be resident (smem/registers)");
+  }
+  p->max_ctas = per_sm * c->num_sms;
+  CU(cudaMalloc(&p->part, sizeof(float) * static_cast<size_t>(p->max_ctas) * p->lstm->ppad));
+  CU(cudaMalloc(&p->ms, sizeof(MasterDev)));
+  CU(cudaMemset(p->ms, 0, sizeof(MasterDev)));
+  CU(cudaMalloc(&p->err, sizeof(int)));
+  CU(cudaMemset(p->err, 0, sizeof(int)));
+  *out = p;
+  return GHC_OK;
+}
+
+void ghc_plan_destroy(ghc_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  cudaFree(p->part);
+  cudaFree(p->ms);
+  cudaFree(p->err);
+  delete p;
+}
+
+int64_t ghc_plan_n_params(const ghc_plan* p) { return p->model.n_params; }
+int64_t ghc_plan_input_width(const ghc_plan* p) { return p->model.input_width; }
+int32_t ghc_plan_n_classes(const ghc_plan* p) { return p->model.n_classes; }
+const char* ghc_plan_kernel_name(const ghc_plan* p) { return p->kname.c_str(); }
+
+ghc_status ghc_plan_tensors(const ghc_plan* p, int64_t* off, int64_t* d0, int64_t* d1, int cap,
+                            int* nt) {
+  *nt = static_cast<int>(p->model.tensors.size());
+  for (int i = 0; i < *nt && i < cap; ++i) {
+    off[i] = p->model.tensors[i].offset;
+    d0[i] = p->model.tensors[i].dim0;
+    d1[i] = p->model.tensors[i].dim1;
+  }
+  return GHC_OK;
+}
+
+ghc_status ghc_arch_info(const char* text, int64_t* n_params, int64_t* input_width,
+                         int32_t* n_classes) {
+  try {
+    const Model m = parse_model(text ? text : "");
+    if (n_params) *n_params = m.n_params;
+    if (input_width) *input_width = m.input_width;
+    if (n_classes) *n_classes = m.n_classes;
+  } catch (const std::exception& e) {
+    return fail(GHC_ERR_CONFIG, e.what());
+  }
+  return GHC_OK;
+}
+
+ghc_status ghc_init_weights_text(const char* text, uint64_t seed, double* h_w) {
+  try {
+    init_weights(parse_model(text ? text : ""), seed, h_w);
+  } catch (const std::exception& e) {
+    return fail(GHC_ERR_CONFIG, e.what());
+  }
+  return GHC_OK;
+}
+
+ghc_status ghc_init_weights(const ghc_plan* p, uint64_t seed, double* h_w) {
+  init_weights(p->model, seed, h_w);
+  return GHC_OK;
+}
+
+// ---------------------------------------------------------------- worker step
+ghc_status ghc_worker_grad(ghc_plan* p, const float* d_w, const float* d_x, const int32_t* d_y,
+                           const int32_t* d_idx, int64_t n, float grad_scale, float* d_grad,
+                           float* d_loss_sum) {
+  if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");  // nn.cpp:104
+  if (!d_w || !d_x || !d_y || !d_grad) return fail(GHC_ERR_CONFIG, "null device pointer");
+  StepArgs a{};
+  a.x = d_x;
+  a.y = d_y;
+  a.idx = d_idx;
+  a.n = static_cast<int>(n);
+  a.rounds = 1;
+  a.grad_scale = grad_scale;
+  a.w_in = d_w;
+  a.ms = p->ms;
+  a.g_out = d_grad;
+  a.loss_out = d_loss_sum;
+  a.mode = MODE_GRAD;
+  return launch_step(p, a, n);
+}
+
+ghc_status ghc_forward(ghc_plan* p, const float* d_w, const float* d_x, const int32_t* d_y,
+                       const int32_t* d_idx, int64_t n, float* d_probs, float* d_loss_sum) {
+  if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");
+  StepArgs a{};
+  a.x = d_x;
+  a.y = d_y;
+  a.idx = d_idx;
+  a.n = static_cast<int>(n);
+  a.rounds = 1;
+  a.w_in = d_w;
+  a.ms = p->ms;
+  a.loss_out = d_loss_sum;
+  a.probs_out = d_probs;
+  a.mode = MODE_FWD;
+  return launch_step(p, a, n);
+}
+
+// ---------------------------------------------------------------- algo
+static ghc_status validate_sgd(float lr, float mu) {  // optim.cpp:20-29
+  if (!(lr > 0.0f)) return fail(GHC_ERR_CONFIG, "learning_rate must be > 0");
+  if (!(mu >= 0.0f && mu < 1.0f)) return fail(GHC_ERR_CONFIG, "momentum must be in [0,1)");
+  return GHC_OK;
+}
+static ghc_status validate_alpha(float alpha) {  // optim.cpp:31-37
+  if (!(alpha > 0.0f && alpha < 1.0f)) return fail(GHC_ERR_CONFIG, "elastic_alpha must be in (0,1)");
+  return GHC_OK;
+}
+
+namespace {
+struct ScratchMs {
+  std::mutex mu;
+  std::vector<std::pair<ghc_ctx*, MasterDev*>> v;
+};
+ScratchMs g_scratch;
+MasterDev* ctx_scratch_ms(ghc_ctx* c) {
+  std::lock_guard<std::mutex> lk(g_scratch.mu);
+  for (auto& e : g_scratch.v)
+    if (e.first == c) return e.second;
+  MasterDev* m = nullptr;
+  cudaSetDevice(c->device);
+  if (cudaMalloc(&m, sizeof(MasterDev)) != cudaSuccess) return nullptr;
+  cudaMemset(m, 0, sizeof(MasterDev));
+  g_scratch.v.push_back({c, m});
+  return m;
+}
+}  // namespace
+
+ghc_status ghc_sgd_apply(ghc_ctx* c, float* d_w, float* d_v, const float* d_g, int64_t P, float lr,
+                         float mu, int32_t* d_status, uint64_t* d_version) {
+  if (ghc_status s = validate_sgd(lr, mu)) return s;
+  if (P < 1) return fail(GHC_ERR_SHAPE, "sgd_step: empty weight set");
+  MasterDev* ms = ctx_scratch_ms(c);
+  if (!ms) return fail(GHC_ERR_CUDA, "scratch allocation failed");
+  int vec = aligned16(d_w) && aligned16(d_v) && aligned16(d_g);
+  long long PP = P;
+  unsigned long long* ver = reinterpret_cast<unsigned long long*>(d_version);
+  int* st = d_status;
+  void* args[] = {&d_w, &d_v, &d_g, &PP, &vec, &lr, &mu, &ms, &st, &ver};
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
+  CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid), dim3(256),
+                                 args, 0, c->stream));
+  c->launches++;
+  return GHC_OK;
+}
+
+ghc_status ghc_elastic_pull(ghc_ctx* c, float* d_w, const float* d_c, int64_t P, float alpha) {
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(elastic_kernel), 256);
+  elastic_kernel<<<grid, 256, 0, c->stream>>>(d_w, d_c, P, aligned16(d_w) && aligned16(d_c), alpha,
+                                              1, nullptr);
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
+ghc_status ghc_easgd_worker_step(ghc_ctx* c, float* d_w, const float* d_c, const float* d_g,
+                                 int64_t P, float lr, float alpha, uint64_t tau,
+                                 uint64_t batch_index, int32_t* d_status) {
+  if (!(lr > 0.0f)) return fail(GHC_ERR_CONFIG, "learning_rate must be > 0");
+  if (ghc_status s = validate_alpha(alpha)) return s;
+  if (tau < 1) return fail(GHC_ERR_CONFIG, "elastic_tau must be >= 1");
+  MasterDev* ms = ctx_scratch_ms(c);
+  if (!ms) return fail(GHC_ERR_CUDA, "scratch allocation failed");
+  int vec = aligned16(d_w) && aligned16(d_c) && aligned16(d_g);
+  int pull = (batch_index % tau) == 0;
+  long long PP = P;
+  int* st = d_status;
+  void* args[] = {&d_w, &d_c, &d_g, &PP, &vec, &lr, &alpha, &pull, &ms, &st};
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(easgd_worker_kernel), 256);
+  CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(easgd_worker_kernel), dim3(grid),
+                                 dim3(256), args, 0, c->stream));
+  c->launches++;
+  return GHC_OK;
+}
+
+ghc_status ghc_easgd_center_step(ghc_ctx* c, float* d_c, const float* d_w, int64_t P, float alpha,
+                                 uint64_t* d_version) {
+  if (ghc_status s = validate_alpha(alpha)) return s;
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(elastic_kernel), 256);
+  elastic_kernel<<<grid, 256, 0, c->stream>>>(d_c, d_w, P, aligned16(d_c) && aligned16(d_w), alpha,
+                                              0, reinterpret_cast<unsigned long long*>(d_version));
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
+ghc_status ghc_weighted_mean(ghc_ctx* c, float* d_out, const float* d_slots, const double* h_counts,
+                             int32_t W, int64_t P) {
+  if (W < 1 || W > kMaxSlots) return fail(GHC_ERR_CONFIG, "weighted_mean: 1..64 slots");
+  SlotWeights cw{};
+  double total = 0.0;
+  for (int i = 0; i < W; ++i) {
+    if (!(h_counts[i] >= 1.0)) return fail(GHC_ERR_PROTOCOL, "GRADIENT sample_count must be >= 1");
+    cw.c[i] = static_cast<float>(h_counts[i]);
+    total += h_counts[i];
+  }
+  const int vec = aligned16(d_out) && aligned16(d_slots) && (P % 4 == 0);
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(weighted_mean_kernel), 256);
+  weighted_mean_kernel<<<grid, 256, 0, c->stream>>>(d_out, d_slots, W, P, P, vec, cw,
+                                                    static_cast<float>(1.0 / total));
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
+// ---------------------------------------------------------------- master
+ghc_status ghc_master_create(ghc_plan* p, const double* h_w0, float lr, float mu, ghc_master** out) {
+  if (ghc_status s = validate_sgd(lr, mu)) return s;
+  auto* m = new ghc_master();
+  m->plan = p;
+  m->lr = lr;
+  m->mu = mu;
+  m->P = p->model.n_params;
+  CU(cudaSetDevice(p->ctx->device));
+  const size_t bytes = sizeof(float) * static_cast<size_t>((m->P + 3) & ~3LL);
+  std::vector<float> w32(static_cast<size_t>(m->P));
+  for (int64_t i = 0; i < m->P; ++i) w32[static_cast<size_t>(i)] = static_cast<float>(h_w0[i]);
+  for (int b = 0; b < 2; ++b) {
+    CU(cudaMalloc(&m->w[b], bytes));
+    CU(cudaMalloc(&m->v[b], bytes));
+    CU(cudaMemset(m->v[b], 0, bytes));
+    CU(cudaMemcpy(m->w[b], w32.data(), sizeof(float) * m->P, cudaMemcpyHostToDevice));
+  }
+  CU(cudaMalloc(&m->ms, sizeof(MasterDev)));
+  CU(cudaMemset(m->ms, 0, sizeof(MasterDev)));
+  CU(cudaMalloc(&m->ms_apply, sizeof(MasterDev)));
+  CU(cudaMemset(m->ms_apply, 0, sizeof(MasterDev)));
+  *out = m;
+  return GHC_OK;
+}
+
+void ghc_master_destroy(ghc_master* m) {
+  if (!m) return;
+  cudaSetDevice(m->plan->ctx->device);
+  cudaStreamSynchronize(m->plan->ctx->stream);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(m->w[b]);
+    cudaFree(m->v[b]);
+  }
+  cudaFree(m->ms);
+  cudaFree(m->ms_apply);
+  delete m;
+}
+
+static ghc_status master_cur(ghc_master* m, int& cur) {
+  MasterDev h;
+  CU(cudaMemcpyAsync(&h, m->ms, sizeof(h), cudaMemcpyDeviceToHost, m->plan->ctx->stream));
+  CU(cudaStreamSynchronize(m->plan->ctx->stream));
+  cur = h.cur;
+  return GHC_OK;
+}
+
+ghc_status ghc_master_weights(ghc_master* m, float** d_w, float** d_v) {
+  int cur = 0;
+  if (ghc_status s = master_cur(m, cur)) return s;
+  if (d_w) *d_w = m->w[cur];
+  if (d_v) *d_v = m->v[cur];
+  return GHC_OK;
+}
+
+ghc_status ghc_master_read(ghc_master* m, float* h_w, float* h_v, uint64_t* version,
+                           uint64_t* rejected) {
+  MasterDev h;
+  cudaStream_t s = m->plan->ctx->stream;
+  CU(cudaMemcpyAsync(&h, m->ms, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h_w) CU(cudaMemcpyAsync(h_w, m->w[h.cur], sizeof(float) * m->P, cudaMemcpyDeviceToHost, s));
+  if (h_v) CU(cudaMemcpyAsync(h_v, m->v[h.cur], sizeof(float) * m->P, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (version) *version = h.version;
+  if (rejected) *rejected = h.rejected;
+  return GHC_OK;
+}
+
+ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t* d_y,
+                                  const int32_t* d_idx, int64_t stride, const int32_t* d_counts,
+                                  int64_t n, int32_t n_rounds, float* d_loss_out) {
+  if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");
+  if (n_rounds < 1) return GHC_OK;
+  StepArgs a{};
+  a.x = d_x;
+  a.y = d_y;
+  a.idx = d_idx;
+  a.stride = stride;
+  a.counts = d_counts;
+  a.n = static_cast<int>(n);
+  a.rounds = n_rounds;
+  a.w0 = m->w[0];
+  a.w1 = m->w[1];
+  a.v0 = m->v[0];
+  a.v1 = m->v[1];
+  a.lr = m->lr;
+  a.mu = m->mu;
+  a.ms = m->ms;
+  a.loss_out = d_loss_out;
+  a.mode = MODE_SGD;
+  return launch_step(m->plan, a, n);
+}
+
+ghc_status ghc_master_apply(ghc_master* m, const float* d_g) {
+  // Single-buffer apply on the current buffer (host knows cur after sync).
+  int cur = 0;
+  if (ghc_status s = master_cur(m, cur)) return s;
+  ghc_ctx* c = m->plan->ctx;
+  float* w = m->w[cur];
+  float* v = m->v[cur];
+  MasterDev* ms = m->ms_apply;
+  int vec = 1;
+  long long PP = m->P;
+  float lr = m->lr, mu = m->mu;
+  int* st = &m->ms->status;
+  unsigned long long* ver = &m->ms->version;
+  void* args[] = {&w, &v, &d_g, &PP, &vec, &lr, &mu, &ms, &st, &ver};
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
+  CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid), dim3(256),
+                                 args, 0, c->stream));
+  c->launches++;
+  return GHC_OK;
+}
+
+// ---------------------------------------------------------------- data
+ghc_status ghc_data_generate(const ghc_data_spec* s, int32_t f0, int32_t nf, float* h_x,
+                             int32_t* h_y) {
+  DataSpec d{s->n_files, s->samples_per_file, s->seq_len, s->input_dim, s->n_classes, 0, s->delta,
+             s->seed};
+  if (f0 < 0 || nf < 0 || f0 + nf > s->n_files) return fail(GHC_ERR_CONFIG, "file range");
+  generate_files(d, f0, nf, h_x, h_y);
+  return GHC_OK;
+}
+
+ghc_status ghc_data_shard(int32_t n_files, int32_t W, int32_t k, int32_t* f0, int32_t* nf) {
+  try {
+    int a = 0, b = 0;
+    shard_files(n_files, W, k, a, b);
+    *f0 = a;
+    *nf = b;
+  } catch (const std::exception& e) {
+    return fail(GHC_ERR_CONFIG, e.what());
+  }
+  return GHC_OK;
+}
+
+ghc_status ghc_data_epoch_indices(const ghc_data_spec* s, int32_t W, int32_t k, int32_t epoch,
+                                  uint64_t seed, int32_t shuffle, int64_t* out, int64_t* count) {
+  DataSpec d{s->n_files, s->samples_per_file, s->seq_len, s->input_dim, s->n_classes, 0, s->delta,
+             s->seed};
+  try {
+    const auto idx = epoch_indices(d, W, k, epoch, seed, shuffle != 0);
+    std::memcpy(out, idx.data(), idx.size() * sizeof(int64_t));
+    *count = static_cast<int64_t>(idx.size());
+  } catch (const std::exception& e) {
+    return fail(GHC_ERR_CONFIG, e.what());
+  }
+  return GHC_OK;
+}
+
+}  // extern "C"

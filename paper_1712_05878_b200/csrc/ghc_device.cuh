@@ -1,0 +1,68 @@
+// ghc_device.cuh — device-side building blocks shared by the sm_100a kernels:
+// device-resident master state, a grid barrier for persistent (cooperatively
+// launched) kernels, fast activations and warp reductions.
+#pragma once
+
+#include <cuda/atomic>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ghc {
+
+// Device-resident master state (one per ghc_master / per fused launch).
+// Lives in HBM so that commit/reject decisions never need a host sync.
+struct MasterDev {
+  unsigned bar_count;          // grid-barrier arrivals
+  unsigned bar_gen;            // grid-barrier generation
+  int cur;                     // which of the double-buffered w/v is current
+  int status;                  // last round: 0 = accepted, GHC_ERR_NONFINITE = rejected
+  unsigned long long version;  // accepted master updates (optim.cpp:63)
+  unsigned long long rejected; // rejected (non-finite) updates
+  unsigned long long round;    // rounds run so far (flag parity)
+  int flag[2];                 // per-round non-finite flags (parity round & 1)
+  unsigned arrive;             // last-CTA-done counter (single-barrier kernels)
+  int pad_;
+};
+
+// Sense-free generation barrier across all CTAs of a cooperative launch.
+// Thread 0 of each CTA arrives on a device-scope counter (release), the last
+// arriver bumps the generation, the others spin (acquire).  Loads of data
+// written by other CTAs after the barrier use ld.global.cg (__ldcg) so no
+// stale L1 line can be observed.
+__device__ __forceinline__ void grid_barrier(MasterDev* ms) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> gen(ms->bar_gen);
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> cnt(ms->bar_count);
+    const unsigned g = gen.load(cuda::memory_order_relaxed);
+    __threadfence();
+    const unsigned arrived = cnt.fetch_add(1u, cuda::memory_order_acq_rel);
+    if (arrived == gridDim.x - 1) {
+      cnt.store(0u, cuda::memory_order_relaxed);
+      gen.store(g + 1u, cuda::memory_order_release);
+    } else {
+      while (gen.load(cuda::memory_order_acquire) == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// sigmoid / tanh via MUFU.EX2 + IEEE reciprocal (abs error ~3e-7, well inside
+// the fp32 parity budget; the reference uses libm exp/tanh, nn.cpp:15-19).
+__device__ __forceinline__ float sigmoid_f(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_f(float x) {
+  const float e = __expf(2.0f * x);
+  return 1.0f - 2.0f * __frcp_rn(e + 1.0f);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool is_finite_f(float v) { return isfinite(v); }
+
+}  // namespace ghc

@@ -1,0 +1,375 @@
+"""Python mirror of the reference's Model / Algo / Data interface over libghc.
+
+Names and argument meaning follow /root/reference/proj/include/gradhub/*.hpp so
+tests read like the reference's own: `Architecture`, `init_weights`,
+`forward`, `backward`-as-`forward_backward`, `loss`, `sgd_step`,
+`elastic_pull`, `easgd_worker_step`, `easgd_center_step`, `shard_files`,
+`batches`; errors are the reference exception classes.  Host-array calls are
+copy-in/copy-out through the C ABI (the drop-in path); `DeviceArray`-based
+calls keep everything resident in HBM (the fast path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import (CacheMismatchError, ConfigError, CudaError, DataSpec, GradhubError,  # noqa: F401
+                   NcclError, NonFiniteGradientError, ProtocolError, ShapeError,
+                   TransportError, check)
+
+_NP2C = {np.dtype(np.float32): 4, np.dtype(np.int32): 4, np.dtype(np.float64): 8,
+         np.dtype(np.int64): 8, np.dtype(np.uint64): 8}
+
+
+def _vp(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+class Context:
+    """ghc_ctx: one CUDA device + stream (one per GPU per host thread)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.ghc_ctx_create(device, C.byref(h)), "ghc_ctx_create")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.ghc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def num_sms(self) -> int:
+        return self.lib.ghc_ctx_num_sms(self.h)
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.ghc_ctx_launch_count(self.h))
+
+    def sync(self):
+        check(self.lib.ghc_ctx_sync(self.h), "ghc_ctx_sync")
+
+    def timer_start(self):
+        check(self.lib.ghc_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        check(self.lib.ghc_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
+    def array(self, shape, dtype=np.float32) -> "DeviceArray":
+        return DeviceArray(self, shape, dtype)
+
+    def upload(self, a: np.ndarray) -> "DeviceArray":
+        a = np.ascontiguousarray(a)
+        d = DeviceArray(self, a.shape, a.dtype)
+        d.copy_from(a)
+        return d
+
+
+class DeviceArray:
+    """A device buffer owned through the C ABI (ghc_malloc / ghc_free)."""
+
+    def __init__(self, ctx: Context, shape, dtype=np.float32):
+        self.ctx = ctx
+        self.shape = tuple(shape) if isinstance(shape, (tuple, list)) else (int(shape),)
+        self.dtype = np.dtype(dtype)
+        self.nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+        p = C.c_void_p()
+        check(ctx.lib.ghc_malloc(ctx.h, self.nbytes, C.byref(p)), "ghc_malloc")
+        self.ptr = p
+
+    def free(self):
+        if self.ptr is not None and self.ctx.h:
+            self.ctx.lib.ghc_free(self.ctx.h, self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def offset(self, elements: int) -> C.c_void_p:
+        return C.c_void_p(self.ptr.value + elements * self.dtype.itemsize)
+
+    def copy_from(self, a: np.ndarray):
+        a = np.ascontiguousarray(a, self.dtype)
+        assert a.nbytes <= self.nbytes
+        check(self.ctx.lib.ghc_memcpy_h2d(self.ctx.h, self.ptr, _vp(a), a.nbytes), "h2d")
+        self.ctx.sync()
+
+    def zero(self):
+        check(self.ctx.lib.ghc_memset(self.ctx.h, self.ptr, 0, self.nbytes))
+
+    def numpy(self) -> np.ndarray:
+        out = np.empty(self.shape, self.dtype)
+        check(self.ctx.lib.ghc_memcpy_d2h(self.ctx.h, _vp(out), self.ptr, self.nbytes), "d2h")
+        self.ctx.sync()
+        return out
+
+
+class Architecture:
+    """Architecture (arch.hpp:36-57) compiled to a device plan (ghc_plan)."""
+
+    def __init__(self, ctx: Context, text: str):
+        self.ctx = ctx
+        self.text = text
+        h = C.c_void_p()
+        check(ctx.lib.ghc_plan_create(ctx.h, text.encode(), C.byref(h)), "parse_architecture")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.lib.ghc_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def n_params(self) -> int:
+        return int(self.ctx.lib.ghc_plan_n_params(self.h))
+
+    @property
+    def input_width(self) -> int:
+        return int(self.ctx.lib.ghc_plan_input_width(self.h))
+
+    @property
+    def n_classes(self) -> int:
+        return int(self.ctx.lib.ghc_plan_n_classes(self.h))
+
+    @property
+    def kernel_name(self) -> str:
+        return self.ctx.lib.ghc_plan_kernel_name(self.h).decode()
+
+    def tensors(self):
+        cap = 64
+        off = np.zeros(cap, np.int64); d0 = np.zeros(cap, np.int64); d1 = np.zeros(cap, np.int64)
+        nt = C.c_int()
+        check(self.ctx.lib.ghc_plan_tensors(self.h, _vp(off), _vp(d0), _vp(d1), cap, C.byref(nt)))
+        return [(int(off[i]), int(d0[i]), int(d1[i])) for i in range(nt.value)]
+
+
+def arch_info(text: str):
+    """Host-only parse + validate (arch.cpp:26-73,173-214): (n_params,
+    input_width, n_classes); raises ConfigError like the reference."""
+    n = C.c_int64(); wdt = C.c_int64(); k = C.c_int32()
+    check(_lib.load().ghc_arch_info(text.encode(), C.byref(n), C.byref(wdt), C.byref(k)),
+          "parse_architecture")
+    return n.value, wdt.value, k.value
+
+
+def init_weights(arch, seed: int) -> np.ndarray:
+    """nn.cpp:83-98 (host, f64, bit-identical to the reference).  `arch` is an
+    Architecture or the architecture text."""
+    if isinstance(arch, str):
+        w = np.zeros(arch_info(arch)[0], np.float64)
+        check(_lib.load().ghc_init_weights_text(arch.encode(), seed, _vp(w)), "init_weights")
+        return w
+    w = np.zeros(arch.n_params, np.float64)
+    check(arch.ctx.lib.ghc_init_weights(arch.h, seed, _vp(w)), "init_weights")
+    return w
+
+
+def worker_grad_device(arch: Architecture, w: DeviceArray, x: DeviceArray, y: DeviceArray, n: int,
+                       grad: DeviceArray, loss_sum: DeviceArray, grad_scale: float | None = None,
+                       idx: DeviceArray | None = None):
+    """Fused forward+loss+backward on device buffers (ghc_worker_grad)."""
+    scale = 1.0 / n if grad_scale is None else grad_scale
+    check(arch.ctx.lib.ghc_worker_grad(arch.h, w.ptr, x.ptr, y.ptr,
+                                       idx.ptr if idx is not None else None, n, scale,
+                                       grad.ptr, loss_sum.ptr), "worker_grad")
+
+
+def forward_backward(w: np.ndarray, arch: Architecture, x: np.ndarray, y: np.ndarray):
+    """forward (nn.cpp:100) + loss (nn.cpp:234) + backward (nn.cpp:250) with
+    host arrays: returns (mean gradient f32[P], loss).  Copy-in/copy-out."""
+    ctx = arch.ctx
+    x = np.ascontiguousarray(x, np.float32).reshape(-1, arch.input_width)
+    y = np.ascontiguousarray(y, np.int32)
+    n = y.shape[0]
+    if n < 1:
+        raise ShapeError("batch: n_samples must be >= 1")
+    if x.shape[0] != n:
+        raise ShapeError("batch: inputs size != n_samples*width")
+    if y.min() < 0 or y.max() >= arch.n_classes:
+        raise ShapeError(f"loss: label out of range [0,{arch.n_classes})")
+    dw = ctx.upload(np.asarray(w, np.float32))
+    dx = ctx.upload(x)
+    dy = ctx.upload(y)
+    g = ctx.array(arch.n_params)
+    ls = ctx.array(1)
+    worker_grad_device(arch, dw, dx, dy, n, g, ls)
+    return g.numpy(), float(ls.numpy()[0]) / n
+
+
+def forward(w: np.ndarray, arch: Architecture, x: np.ndarray, y: np.ndarray):
+    """forward + loss: returns (probs[n×K], loss)."""
+    ctx = arch.ctx
+    x = np.ascontiguousarray(x, np.float32).reshape(-1, arch.input_width)
+    y = np.ascontiguousarray(y, np.int32)
+    n = y.shape[0]
+    dw = ctx.upload(np.asarray(w, np.float32))
+    dx = ctx.upload(x)
+    dy = ctx.upload(y)
+    probs = ctx.array((n, arch.n_classes))
+    ls = ctx.array(1)
+    check(ctx.lib.ghc_forward(arch.h, dw.ptr, dx.ptr, dy.ptr, None, n, probs.ptr, ls.ptr),
+          "forward")
+    return probs.numpy(), float(ls.numpy()[0]) / n
+
+
+@dataclass
+class OptimState:
+    """OptimState (optim.hpp:11-19)."""
+    velocity: np.ndarray
+    learning_rate: float = 0.01
+    momentum: float = 0.0
+
+
+def sgd_step(ctx: Context, w: np.ndarray, g: np.ndarray, s: OptimState):
+    """sgd_step (optim.cpp:39-65): returns (w', OptimState'); raises
+    NonFiniteGradientError (caller keeps its weights) on a non-finite g."""
+    w = np.asarray(w, np.float32)
+    if np.shape(g) != w.shape or s.velocity.shape != w.shape:
+        raise ShapeError("sgd_step: gradient/velocity shape does not match weights")
+    dw = ctx.upload(w); dv = ctx.upload(np.asarray(s.velocity, np.float32))
+    dg = ctx.upload(np.asarray(g, np.float32))
+    st = ctx.upload(np.zeros(1, np.int32))
+    check(ctx.lib.ghc_sgd_apply(ctx.h, dw.ptr, dv.ptr, dg.ptr, w.size, s.learning_rate,
+                                s.momentum, st.ptr, None), "sgd_step")
+    if int(st.numpy()[0]) == 2:
+        raise NonFiniteGradientError("sgd_step: gradient has NaN/Inf entries; update rejected")
+    return dw.numpy(), OptimState(dv.numpy(), s.learning_rate, s.momentum)
+
+
+def elastic_pull(ctx: Context, w: np.ndarray, center: np.ndarray, alpha: float) -> np.ndarray:
+    """elastic_pull (optim.cpp:67-80)."""
+    dw = ctx.upload(np.asarray(w, np.float32)); dc = ctx.upload(np.asarray(center, np.float32))
+    check(ctx.lib.ghc_elastic_pull(ctx.h, dw.ptr, dc.ptr, dw.shape[0], alpha), "elastic_pull")
+    return dw.numpy()
+
+
+def easgd_worker_step(ctx: Context, w, center, g, s: OptimState, alpha: float, tau: int,
+                      batch_index: int) -> np.ndarray:
+    """easgd_worker_step (optim.cpp:82-105)."""
+    dw = ctx.upload(np.asarray(w, np.float32)); dc = ctx.upload(np.asarray(center, np.float32))
+    dg = ctx.upload(np.asarray(g, np.float32)); st = ctx.upload(np.zeros(1, np.int32))
+    check(ctx.lib.ghc_easgd_worker_step(ctx.h, dw.ptr, dc.ptr, dg.ptr, dw.shape[0],
+                                        s.learning_rate, alpha, tau, batch_index, st.ptr),
+          "easgd_worker_step")
+    if int(st.numpy()[0]) == 2:
+        raise NonFiniteGradientError("easgd_worker_step: gradient has NaN/Inf entries")
+    return dw.numpy()
+
+
+def easgd_center_step(ctx: Context, center, worker, alpha: float, version: int = 0):
+    """easgd_center_step (optim.cpp:107-123): returns (c', version+1)."""
+    dc = ctx.upload(np.asarray(center, np.float32)); dw = ctx.upload(np.asarray(worker, np.float32))
+    ver = ctx.upload(np.array([version], np.uint64))
+    check(ctx.lib.ghc_easgd_center_step(ctx.h, dc.ptr, dw.ptr, dc.shape[0], alpha, ver.ptr),
+          "easgd_center_step")
+    return dc.numpy(), int(ver.numpy()[0])
+
+
+class Master:
+    """Device-resident Downpour master (ghc_master): w/v in HBM, version,
+    on-device commit/reject.  `sync_rounds` runs whole sync rounds of the
+    colocated worker in one persistent launch."""
+
+    def __init__(self, arch: Architecture, w0: np.ndarray, lr: float, mu: float):
+        self.arch = arch
+        self.ctx = arch.ctx
+        w0 = np.ascontiguousarray(w0, np.float64)
+        h = C.c_void_p()
+        check(self.ctx.lib.ghc_master_create(arch.h, _vp(w0), lr, mu, C.byref(h)), "master_create")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.lib.ghc_master_destroy(self.h)
+        except Exception:
+            pass
+
+    def sync_rounds(self, x: DeviceArray, y: DeviceArray, idx: DeviceArray | None, stride: int,
+                    n: int, rounds: int, counts: DeviceArray | None = None,
+                    loss_out: DeviceArray | None = None, idx_offset: int = 0,
+                    loss_offset: int = 0, counts_offset: int = 0):
+        check(self.ctx.lib.ghc_master_sync_rounds(
+            self.h, x.ptr, y.ptr, idx.offset(idx_offset) if idx is not None else None, stride,
+            counts.offset(counts_offset) if counts is not None else None, n, rounds,
+            loss_out.offset(loss_offset) if loss_out is not None else None), "sync_rounds")
+
+    def apply(self, g: DeviceArray):
+        check(self.ctx.lib.ghc_master_apply(self.h, g.ptr), "master_apply")
+
+    def read(self):
+        P = self.arch.n_params
+        w = np.zeros(P, np.float32); v = np.zeros(P, np.float32)
+        ver = C.c_uint64(); rej = C.c_uint64()
+        check(self.ctx.lib.ghc_master_read(self.h, _vp(w), _vp(v), C.byref(ver), C.byref(rej)))
+        return w, v, ver.value, rej.value
+
+    def weights_ptr(self) -> C.c_void_p:
+        wp = C.c_void_p()
+        check(self.ctx.lib.ghc_master_weights(self.h, C.byref(wp), None))
+        return wp
+
+
+# ---------------------------------------------------------------- data layer
+def data_spec(n_files, samples_per_file, seq_len=10, input_dim=5, n_classes=3, delta=5.0,
+              seed=1234) -> DataSpec:
+    return DataSpec(n_files, samples_per_file, seq_len, input_dim, n_classes, 0, delta, seed)
+
+
+def generate(spec: DataSpec, f0: int = 0, nf: int | None = None):
+    """generate_synthetic for files [f0, f0+nf): f32 rows."""
+    nf = spec.n_files - f0 if nf is None else nf
+    n = nf * spec.samples_per_file
+    x = np.zeros((n, spec.seq_len * spec.input_dim), np.float32)
+    y = np.zeros(n, np.int32)
+    check(_lib.load().ghc_data_generate(C.byref(spec), f0, nf, _vp(x), _vp(y)), "generate")
+    return x, y
+
+
+def shard_files(n_files: int, n_workers: int, worker: int):
+    """shard_files: (first_file, n_files) of `worker`."""
+    f0 = C.c_int32(); nf = C.c_int32()
+    check(_lib.load().ghc_data_shard(n_files, n_workers, worker, C.byref(f0), C.byref(nf)),
+          "shard_files")
+    return f0.value, nf.value
+
+
+def epoch_indices(spec: DataSpec, n_workers: int, worker: int, epoch: int, shuffle_seed: int,
+                  shuffle: bool = True) -> np.ndarray:
+    """The worker's shard permutation for `epoch` (global sample indices)."""
+    f0, nf = shard_files(spec.n_files, n_workers, worker)
+    out = np.zeros(nf * spec.samples_per_file, np.int64)
+    cnt = C.c_int64()
+    check(_lib.load().ghc_data_epoch_indices(C.byref(spec), n_workers, worker, epoch,
+                                             shuffle_seed, int(shuffle), _vp(out), C.byref(cnt)),
+          "epoch_indices")
+    return out[: cnt.value]
+
+
+def batches(spec: DataSpec, n_workers: int, worker: int, batch_size: int, epochs: int,
+            shuffle_seed: int, shuffle: bool = True):
+    """batches over `epochs`: list of global-index arrays
+    (short final batch of each epoch kept with its true size)."""
+    out = []
+    for e in range(epochs):
+        idx = epoch_indices(spec, n_workers, worker, e, shuffle_seed, shuffle)
+        out.extend(idx[i:i + batch_size] for i in range(0, len(idx), batch_size))
+    return out
