@@ -84,6 +84,11 @@ int32_t ghc_plan_n_classes(const ghc_plan* plan);   /* Architecture::n_classes a
 /* Parameter tensors in weight-set order (arch.cpp:95-112). */
 ghc_status ghc_plan_tensors(const ghc_plan* plan, int64_t* offset, int64_t* dim0,
                             int64_t* dim1, int cap, int* n_tensors);
+/* Diagnostics: when d_probe != NULL every fused launch records %globaltimer
+ * at 7 phase boundaries per round and CTA into d_probe[(round*ctas+cta)*8+i]
+ * (weights loaded, samples done, partial stored, barrier 1, reduce, barrier
+ * 2).  NULL disables (the default). */
+ghc_status ghc_plan_set_probe(ghc_plan* plan, uint64_t* d_probe);
 /* Name of the fused kernel the plan dispatches to (diagnostics). */
 const char* ghc_plan_kernel_name(const ghc_plan* plan);
 
@@ -174,6 +179,44 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
 /* Apply a combined gradient produced elsewhere (NCCL reduce, virtual workers):
  * d_g[P] is the already-combined gradient. */
 ghc_status ghc_master_apply(ghc_master* m, const float* d_g);
+
+/* ------------------------------------------------------------------ */
+/* Exchange across GPUs (one process per GPU) over NCCL / NVLink 5:     */
+/* replaces Endpoint send/recv (transport.hpp:22-44) + establish()      */
+/* (transport.cpp:533-586, new backend "nvlink").                       */
+/* ------------------------------------------------------------------ */
+typedef struct ghc_comm ghc_comm;
+#define GHC_UNIQUE_ID_BYTES 128
+enum { GHC_EXCHANGE_REDUCE_BCAST = 0, GHC_EXCHANGE_ALLREDUCE = 1 };
+
+/* Rank 0 creates the id; the caller moves the bytes to every rank. */
+ghc_status ghc_comm_unique_id(uint8_t* out_id);
+ghc_status ghc_comm_init(ghc_ctx* ctx, const uint8_t* id, int32_t rank, int32_t nranks,
+                         ghc_comm** out);
+/* Topology::hierarchical groups (transport.cpp:520-531): ranks with equal
+ * color form a sub-communicator ordered by key; *out = NULL for color < 0. */
+ghc_status ghc_comm_split(ghc_comm* parent, int32_t color, int32_t key, ghc_comm** out);
+void ghc_comm_destroy(ghc_comm* comm);
+int32_t ghc_comm_rank(const ghc_comm* comm);
+int32_t ghc_comm_size(const ghc_comm* comm);
+ghc_status ghc_comm_reduce_sum(ghc_comm* comm, const float* d_send, float* d_recv, int64_t count,
+                               int32_t root);
+ghc_status ghc_comm_broadcast(ghc_comm* comm, float* d_buf, int64_t count, int32_t root);
+ghc_status ghc_comm_allreduce_sum(ghc_comm* comm, const float* d_send, float* d_recv,
+                                  int64_t count);
+
+/* Synchronous Downpour rounds across the communicator:
+ * rank k is worker k and gathers its batch d_idx[r*stride ..] from its
+ * resident shard; h_counts[r*nranks + k] is worker k's sample count in round
+ * r (0 once it has sent DONE; known on every rank from the deterministic
+ * data layer).  exchange = REDUCE_BCAST: gradients reduced to the master on
+ * rank 0, sgd_step there, weights broadcast (the reference protocol);
+ * ALLREDUCE: every rank holds a bit-identical master replica.  The master
+ * object on every rank must be created from the same initial weights. */
+ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
+                                const float* d_x, const int32_t* d_y, const int32_t* d_idx,
+                                int64_t stride, const int32_t* h_counts, int32_t n_rounds,
+                                float* d_loss_out);
 
 /* ------------------------------------------------------------------ */
 /* Data layer, host side, bit-identical to the oracle */

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("ghc_plan_n_classes", _i32, [_vp]),
     ("ghc_plan_tensors", C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
     ("ghc_plan_kernel_name", _cp, [_vp]),
+    ("ghc_plan_set_probe", C.c_int, [_vp, _vp]),
     ("ghc_arch_info", C.c_int, [_cp, _vp, _vp, _vp]),
     ("ghc_init_weights_text", C.c_int, [_cp, _u64, _vp]),
     ("ghc_init_weights", C.c_int, [_vp, _u64, _vp]),
@@ -98,6 +99,16 @@ SIGNATURES = [
     ("ghc_master_read", C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     ("ghc_master_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp]),
     ("ghc_master_apply", C.c_int, [_vp, _vp]),
+    ("ghc_comm_unique_id", C.c_int, [_vp]),
+    ("ghc_comm_init", C.c_int, [_vp, _vp, _i32, _i32, _vp]),
+    ("ghc_comm_split", C.c_int, [_vp, _i32, _i32, _vp]),
+    ("ghc_comm_destroy", None, [_vp]),
+    ("ghc_comm_rank", _i32, [_vp]),
+    ("ghc_comm_size", _i32, [_vp]),
+    ("ghc_comm_reduce_sum", C.c_int, [_vp, _vp, _vp, _i64, _i32]),
+    ("ghc_comm_broadcast", C.c_int, [_vp, _vp, _i64, _i32]),
+    ("ghc_comm_allreduce_sum", C.c_int, [_vp, _vp, _vp, _i64]),
+    ("ghc_dist_sync_rounds", C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _i32, _vp]),
     ("ghc_data_generate", C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     ("ghc_data_shard", C.c_int, [_i32, _i32, _i32, _vp, _vp]),
     ("ghc_data_epoch_indices", C.c_int, [_vp, _i32, _i32, _i32, _u64, _i32, _vp, _vp]),

@@ -14,9 +14,10 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libghc.so")
 
-CU_SOURCES = ["ghc.cu"]
+CU_SOURCES = ["ghc.cu", "dist.cu"]
 CXX_SOURCES = ["host_model.cpp"]
-HEADERS = ["ghc_device.cuh", "lstm_step.cuh", "update_kernels.cuh", "host_model.hpp"]
+HEADERS = ["ghc_device.cuh", "lstm_step.cuh", "update_kernels.cuh", "host_model.hpp",
+           "ghc_internal.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -42,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     srcs = [os.path.join(CSRC, f) for f in CU_SOURCES + CXX_SOURCES]
-    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp", *srcs]
+    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp", *srcs, "-lnccl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -1,0 +1,211 @@
+// dist.cu — the worker exchange across GPUs (one process per GPU) over NCCL /
+// NVLink 5: the B200-native replacement of the reference's Endpoint
+// send/recv pairs (transport.hpp:22-44) for the synchronous Downpour round
+// and the hierarchical groups (Topology::hierarchical,
+// transport.cpp:520-531 → ncclCommSplit).
+//
+// Rendezvous is plumbing: the caller (bench.py / the roles driver) moves the
+// 128-byte NCCL unique id between processes (torch.distributed); everything
+// after that is stream-ordered on the context's stream — no host sync inside
+// a round.
+#include <nccl.h>
+
+#include "ghc_internal.cuh"
+
+using namespace ghc;
+
+#define NC(expr)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return ghc_fail(GHC_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+struct ghc_comm {
+  ghc_ctx* ctx = nullptr;
+  ncclComm_t nccl = nullptr;
+  int rank = 0, size = 1;
+  float* gbuf = nullptr;  // [P+1] this worker's pre-scaled gradient + loss sum
+  float* gsum = nullptr;  // [P+1] reduced
+  int64_t cap = 0;
+};
+
+namespace {
+
+ghc_status ensure_buffers(ghc_comm* c, int64_t n) {
+  if (c->cap >= n) return GHC_OK;
+  cudaSetDevice(c->ctx->device);
+  cudaFree(c->gbuf);
+  cudaFree(c->gsum);
+  const size_t bytes = sizeof(float) * static_cast<size_t>((n + 3) & ~3LL);
+  CU(cudaMalloc(&c->gbuf, bytes));
+  CU(cudaMalloc(&c->gsum, bytes));
+  c->cap = n;
+  return GHC_OK;
+}
+
+__global__ void copy_scalar_kernel(float* dst, const float* src) { *dst = *src; }
+
+}  // namespace
+
+extern "C" {
+
+ghc_status ghc_comm_unique_id(uint8_t* out) {
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return GHC_OK;
+}
+
+ghc_status ghc_comm_init(ghc_ctx* ctx, const uint8_t* id_bytes, int32_t rank, int32_t nranks,
+                         ghc_comm** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return ghc_fail(GHC_ERR_CONFIG, "comm: bad rank");
+  ncclUniqueId id;
+  std::memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);
+  CU(cudaSetDevice(ctx->device));
+  auto* c = new ghc_comm();
+  c->ctx = ctx;
+  c->rank = rank;
+  c->size = nranks;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return ghc_fail(GHC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *out = c;
+  return GHC_OK;
+}
+
+ghc_status ghc_comm_split(ghc_comm* parent, int32_t color, int32_t key, ghc_comm** out) {
+  auto* c = new ghc_comm();
+  c->ctx = parent->ctx;
+  ncclResult_t r = ncclCommSplit(parent->nccl, color, key, &c->nccl, nullptr);
+  if (r != ncclSuccess) {
+    delete c;
+    return ghc_fail(GHC_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+  }
+  if (c->nccl == nullptr) {  // color == NCCL_SPLIT_NOCOLOR
+    delete c;
+    *out = nullptr;
+    return GHC_OK;
+  }
+  NC(ncclCommUserRank(c->nccl, &c->rank));
+  NC(ncclCommCount(c->nccl, &c->size));
+  *out = c;
+  return GHC_OK;
+}
+
+void ghc_comm_destroy(ghc_comm* c) {
+  if (!c) return;
+  cudaSetDevice(c->ctx->device);
+  cudaStreamSynchronize(c->ctx->stream);
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  cudaFree(c->gbuf);
+  cudaFree(c->gsum);
+  delete c;
+}
+
+int32_t ghc_comm_rank(const ghc_comm* c) { return c->rank; }
+int32_t ghc_comm_size(const ghc_comm* c) { return c->size; }
+
+ghc_status ghc_comm_reduce_sum(ghc_comm* c, const float* d_send, float* d_recv, int64_t count,
+                               int32_t root) {
+  NC(ncclReduce(d_send, d_recv, static_cast<size_t>(count), ncclFloat32, ncclSum, root, c->nccl,
+                c->ctx->stream));
+  return GHC_OK;
+}
+
+ghc_status ghc_comm_broadcast(ghc_comm* c, float* d_buf, int64_t count, int32_t root) {
+  NC(ncclBroadcast(d_buf, d_buf, static_cast<size_t>(count), ncclFloat32, root, c->nccl,
+                   c->ctx->stream));
+  return GHC_OK;
+}
+
+ghc_status ghc_comm_allreduce_sum(ghc_comm* c, const float* d_send, float* d_recv, int64_t count) {
+  NC(ncclAllReduce(d_send, d_recv, static_cast<size_t>(count), ncclFloat32, ncclSum, c->nccl,
+                   c->ctx->stream));
+  return GHC_OK;
+}
+
+// Synchronous Downpour rounds across the communicator.  Rank r is worker r;
+// h_counts[round*size + k] = samples of worker k in that round (0 = worker k
+// already sent DONE).  Every rank knows every count (the data layer is
+// deterministic), so the sample-weighted mean Σ c_k g_k / Σ c_k is formed by
+// pre-scaling each worker's summed gradient with 1/Σc and summing — one
+// reduction, no host sync.
+ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange, const float* d_x,
+                                const int32_t* d_y, const int32_t* d_idx, int64_t stride,
+                                const int32_t* h_counts, int32_t n_rounds, float* d_loss_out) {
+  if (exchange != GHC_EXCHANGE_REDUCE_BCAST && exchange != GHC_EXCHANGE_ALLREDUCE)
+    return ghc_fail(GHC_ERR_CONFIG, "unknown exchange");
+  ghc_plan* p = m->plan;
+  ghc_ctx* ctx = p->ctx;
+  const int64_t P = m->P;
+  if (ghc_status s = ensure_buffers(comm, P + 1)) return s;
+  int cur = 0;
+  {
+    MasterDev h;
+    CU(cudaMemcpyAsync(&h, m->ms, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    cur = h.cur;
+  }
+  float* w = m->w[cur];
+  float* v = m->v[cur];
+  const bool master_here = exchange == GHC_EXCHANGE_ALLREDUCE || comm->rank == 0;
+  for (int r = 0; r < n_rounds; ++r) {
+    const int32_t* cnt = h_counts + static_cast<int64_t>(r) * comm->size;
+    int64_t total = 0;
+    for (int k = 0; k < comm->size; ++k) total += cnt[k];
+    if (total == 0) break;  // every worker has sent DONE
+    const int32_t mine = cnt[comm->rank];
+    if (mine > 0) {
+      StepArgs a{};
+      a.x = d_x;
+      a.y = d_y;
+      a.idx = d_idx ? d_idx + static_cast<int64_t>(r) * stride : nullptr;
+      a.n = mine;
+      a.rounds = 1;
+      a.grad_scale = static_cast<float>(1.0 / static_cast<double>(total));
+      a.w_in = w;
+      a.ms = p->ms;
+      a.g_out = comm->gbuf;
+      a.loss_out = comm->gbuf + P;
+      a.mode = MODE_GRAD;
+      if (ghc_status s = launch_step(p, a, mine)) return s;
+    } else {
+      CU(cudaMemsetAsync(comm->gbuf, 0, sizeof(float) * (P + 1), ctx->stream));
+    }
+    if (exchange == GHC_EXCHANGE_REDUCE_BCAST) {
+      NC(ncclReduce(comm->gbuf, comm->gsum, static_cast<size_t>(P + 1), ncclFloat32, ncclSum, 0,
+                    comm->nccl, ctx->stream));
+    } else {
+      NC(ncclAllReduce(comm->gbuf, comm->gsum, static_cast<size_t>(P + 1), ncclFloat32, ncclSum,
+                       comm->nccl, ctx->stream));
+    }
+    if (master_here) {
+      // sgd_step with whole-update rejection (optim.cpp:39-65), in place.
+      MasterDev* ms = m->ms_apply;
+      int vec = 1;
+      long long PP = P;
+      float lr = m->lr, mu = m->mu;
+      int* st = &m->ms->status;
+      unsigned long long* ver = &m->ms->version;
+      const float* g = comm->gsum;
+      unsigned long long* rj = &m->ms->rejected;
+      void* args[] = {&w, &v, &g, &PP, &vec, &lr, &mu, &ms, &st, &ver, &rj};
+      const int grid = occupancy_grid(ctx, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
+      CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid),
+                                     dim3(256), args, 0, ctx->stream));
+      ctx->launches++;
+      if (d_loss_out) {
+        copy_scalar_kernel<<<1, 1, 0, ctx->stream>>>(d_loss_out + r, comm->gsum + P);
+        ctx->launches++;
+      }
+    }
+    if (exchange == GHC_EXCHANGE_REDUCE_BCAST)
+      NC(ncclBroadcast(w, w, static_cast<size_t>(P), ncclFloat32, 0, comm->nccl, ctx->stream));
+  }
+  return GHC_OK;
+}
+
+}  // extern "C"

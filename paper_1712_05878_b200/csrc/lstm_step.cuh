@@ -49,8 +49,15 @@ struct StepArgs {
   float* loss_out;        // per-round loss sum (nullable)
   float* probs_out;       // MODE_FWD: n×K (nullable)
   int* err;               // bit 0: label out of range (nn.cpp:241-244)
+  unsigned long long* probe;  // nullable: [rounds][gridDim][8] %globaltimer per phase
   int mode;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int D, int H, int T, int K>
 struct LstmNet {
@@ -296,8 +303,12 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     const float scale = a.mode == MODE_SGD ? 1.0f / (float)n : a.grad_scale;
     const int parity = (int)((round0 + (unsigned long long)r) & 1ull);
 
+    unsigned long long* pr =
+        a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 8 : nullptr;
+    if (pr && threadIdx.x == 0) pr[0] = globaltimer();
     for (int p = threadIdx.x; p < N::P; p += blockDim.x) wsm[p] = __ldcg(w + p);
     __syncthreads();
+    if (pr && threadIdx.x == 0) pr[1] = globaltimer();
 
     // ---- per-warp samples of this CTA's contiguous chunk ----
     float* wp = wpart + warp * N::PPAD;
@@ -327,6 +338,7 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     }
     if (lane == 0) lossw[warp] = lsum;
     __syncthreads();
+    if (pr && threadIdx.x == 0) pr[2] = globaltimer();
 
     // ---- CTA partial (fixed warp order) → global ----
     float* prow = a.part + (long long)blockIdx.x * a.pstride;
@@ -342,7 +354,9 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
       for (int w2 = 0; w2 < NW; ++w2) t += lossw[w2];
       __stcg(prow + N::P, t);
     }
+    if (pr && threadIdx.x == 0) pr[3] = globaltimer();
     grid_barrier(a.ms);
+    if (pr && threadIdx.x == 0) pr[4] = globaltimer();
     if (a.mode == MODE_SGD && blockIdx.x == 0 && threadIdx.x == 0) a.ms->flag[parity ^ 1] = 0;
 
     // ---- distributed deterministic reduction of slice [p0,p1) over CTAs ----
@@ -386,7 +400,9 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     if (a.mode == MODE_SGD) {
       bad = __syncthreads_or(bad);
       if (bad && threadIdx.x == 0) atomicOr(&a.ms->flag[parity], 1);
+      if (pr && threadIdx.x == 0) pr[5] = globaltimer();
       grid_barrier(a.ms);
+      if (pr && threadIdx.x == 0) pr[6] = globaltimer();
       const int rej = __ldcg(&a.ms->flag[parity]);
       if (rej) {
         ++rejected;

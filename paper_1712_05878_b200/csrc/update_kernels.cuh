@@ -52,7 +52,8 @@ __device__ __forceinline__ int check_finite_all(const float* g, long long P, int
 
 // Last CTA out resets the flag and publishes status / version.
 __device__ __forceinline__ void finish_rejecting(MasterDev* ms, int rej, int* status,
-                                                 unsigned long long* version) {
+                                                 unsigned long long* version,
+                                                 unsigned long long* rejected) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -62,15 +63,17 @@ __device__ __forceinline__ void finish_rejecting(MasterDev* ms, int rej, int* st
       ms->flag[0] = 0;
       if (status) *status = rej ? 2 /*GHC_ERR_NONFINITE*/ : 0;
       if (version && !rej) *version += 1ull;
+      if (rejected && rej) *rejected += 1ull;
       __threadfence();
     }
   }
 }
 
-__global__ void __launch_bounds__(256) sgd_apply_kernel(float* __restrict__ w, float* __restrict__ v,
+static __global__ void __launch_bounds__(256) sgd_apply_kernel(float* __restrict__ w, float* __restrict__ v,
                                                         const float* __restrict__ g, long long P, int vec,
                                                         float lr, float mu, MasterDev* ms,
-                                                        int* status, unsigned long long* version) {
+                                                        int* status, unsigned long long* version,
+                                                        unsigned long long* rejected) {
   const int rej = check_finite_all(g, P, vec, ms);
   if (!rej) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -100,10 +103,10 @@ __global__ void __launch_bounds__(256) sgd_apply_kernel(float* __restrict__ w, f
       w[i] += vn;
     }
   }
-  finish_rejecting(ms, rej, status, version);
+  finish_rejecting(ms, rej, status, version, rejected);
 }
 
-__global__ void __launch_bounds__(256) easgd_worker_kernel(float* __restrict__ w,
+static __global__ void __launch_bounds__(256) easgd_worker_kernel(float* __restrict__ w,
                                                            const float* __restrict__ c,
                                                            const float* __restrict__ g,
                                                            long long P, int vec, float lr,
@@ -139,12 +142,12 @@ __global__ void __launch_bounds__(256) easgd_worker_kernel(float* __restrict__ w
       w[i] = wv;
     }
   }
-  finish_rejecting(ms, rej, status, nullptr);
+  finish_rejecting(ms, rej, status, nullptr, nullptr);
 }
 
 // c += alpha*(w - c)  (optim.cpp:118) — also used for elastic_pull with the
 // roles swapped: w -= alpha*(w - c)  ≡  w += alpha*(c - w).
-__global__ void __launch_bounds__(256) elastic_kernel(float* __restrict__ dst,
+static __global__ void __launch_bounds__(256) elastic_kernel(float* __restrict__ dst,
                                                       const float* __restrict__ src,
                                                       long long P, int vec, float alpha,
                                                       int pull, unsigned long long* version) {
@@ -182,7 +185,7 @@ struct SlotWeights {
 };
 
 // out = Σ_i c_i * slot_i / Σ c_i, slot order fixed (deterministic).
-__global__ void __launch_bounds__(256) weighted_mean_kernel(float* __restrict__ out,
+static __global__ void __launch_bounds__(256) weighted_mean_kernel(float* __restrict__ out,
                                                             const float* __restrict__ slots,
                                                             int W, long long P, long long sstride,
                                                             int vec, SlotWeights cw,
