@@ -85,12 +85,21 @@ int32_t ghc_plan_n_classes(const ghc_plan* plan);   /* Architecture::n_classes a
 ghc_status ghc_plan_tensors(const ghc_plan* plan, int64_t* offset, int64_t* dim0,
                             int64_t* dim1, int cap, int* n_tensors);
 /* Diagnostics: when d_probe != NULL every fused launch records %globaltimer
- * at 7 phase boundaries per round and CTA into d_probe[(round*ctas+cta)*8+i]
+ * at 7 phase boundaries per round and CTA into d_probe[(round*ctas+cta)*16+i]
+ * (+ 5 points inside warp 0's first sample at i = 8..12)
  * (weights loaded, samples done, partial stored, barrier 1, reduce, barrier
  * 2).  NULL disables (the default). */
 ghc_status ghc_plan_set_probe(ghc_plan* plan, uint64_t* d_probe);
+/* Diagnostics: ns per grid-wide barrier for implementation `impl`
+ * (0 atomic counter, 1 gather/broadcast flags, 2 all-poll-all flags,
+ * 3 hardware cluster barrier of 8 CTAs) over `ctas` co-resident CTAs. */
+ghc_status ghc_diag_barrier_bench(ghc_ctx* ctx, int32_t impl, int32_t ctas, int32_t threads,
+                                  int32_t iters, double* ns_per);
 /* Name of the fused kernel the plan dispatches to (diagnostics). */
 const char* ghc_plan_kernel_name(const ghc_plan* plan);
+/* Cluster variant geometry: co-resident clusters and cluster size (0 = flat). */
+int32_t ghc_plan_max_clusters(const ghc_plan* plan);
+int32_t ghc_plan_cluster_size(const ghc_plan* plan);
 
 /* Host-only architecture check (no device needed): parse + validate and
  * report the sizes; GHC_ERR_CONFIG with the reference's message on error. */

@@ -83,6 +83,9 @@ SIGNATURES = [
     ("ghc_plan_tensors", C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
     ("ghc_plan_kernel_name", _cp, [_vp]),
     ("ghc_plan_set_probe", C.c_int, [_vp, _vp]),
+    ("ghc_plan_max_clusters", _i32, [_vp]),
+    ("ghc_plan_cluster_size", _i32, [_vp]),
+    ("ghc_diag_barrier_bench", C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp]),
     ("ghc_arch_info", C.c_int, [_cp, _vp, _vp, _vp]),
     ("ghc_init_weights_text", C.c_int, [_cp, _u64, _vp]),
     ("ghc_init_weights", C.c_int, [_vp, _u64, _vp]),

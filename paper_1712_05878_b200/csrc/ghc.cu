@@ -5,11 +5,48 @@
 // cooperative launches for the kernels that carry a grid barrier.  All math
 // runs in the sm_100a kernels of lstm_step.cuh / update_kernels.cuh; there is
 // no CPU compute path.
+#include <cstdlib>
+
 #include "ghc_internal.cuh"
 
 namespace {
 thread_local std::string g_err;
+
+template <int D, int H, int T, int K>
+LstmEntry make_entry(const char* name) {
+  using N = LstmNet<D, H, T, K>;
+  using R4 = RoundLayout<D, H, T, K, 4>;
+  using R8 = RoundLayout<D, H, T, K, 8>;
+  return LstmEntry{D,
+                   H,
+                   T,
+                   K,
+                   &lstm_softmax_step_kernel<D, H, T, K>,
+                   {&lstm_round_kernel<D, H, T, K, 4>, &lstm_round_kernel<D, H, T, K, 8>},
+                   N::P,
+                   N::PPAD,
+                   {R4::EP, R8::EP},
+                   &N::smem_bytes,
+                   {&R4::smem_bytes, &R8::smem_bytes},
+                   name};
+}
+
 }  // namespace
+
+const std::vector<LstmEntry>& lstm_table() {
+  static const std::vector<LstmEntry> t = {
+      make_entry<5, 20, 10, 3>("lstm_round<D5,H20,T10,K3>"),  // SPEC.md:109 bench net
+      make_entry<5, 8, 10, 3>("lstm_round<D5,H8,T10,K3>"),
+      make_entry<3, 4, 5, 3>("lstm_round<D3,H4,T5,K3>"),
+      make_entry<2, 16, 3, 4>("lstm_round<D2,H16,T3,K4>"),
+      make_entry<5, 32, 10, 3>("lstm_round<D5,H32,T10,K3>"),
+      make_entry<4, 12, 6, 5>("lstm_round<D4,H12,T6,K5>"),
+  };
+  return t;
+}
+
+
+namespace {}  // namespace
 
 ghc_status ghc_fail(ghc_status s, const std::string& msg) {
   g_err = msg;
@@ -143,7 +180,7 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     return fail(GHC_ERR_CONFIG, "no sm_100a kernel instantiated for architecture '" + txt +
                                     "' (see DESIGN.md §Kernels for the supported shapes)");
   }
-  p->kname = p->lstm->name;
+  p->kname = std::string(p->lstm->name) + " [flat]";
   CU(cudaSetDevice(c->device));
   // largest block (≤ 8 warps) whose shared memory fits one SM, and the
   // co-residency of the cooperative fused kernel at that size
@@ -164,11 +201,58 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     return fail(GHC_ERR_CUDA, "fused kernel cannot be resident (smem/registers)");
   }
   p->max_ctas = per_sm * c->num_sms;
+  // cluster variant: for clusters of 8 and of 4, the largest block that fits
+  // and how many clusters can be co-resident (GPC-constrained; queried, not
+  // assumed).  Pick the size that gives every sample its own warp with the
+  // fewest warps per CTA (ties → 8: fewer rows in the cross-cluster reduce).
+  {
+    const char* env = std::getenv("GHC_STEP");
+    p->use_cluster = !(env && std::string(env) == "flat");
+    int best_warps = 1 << 30;
+    for (int ci = 1; ci >= 0; --ci) {
+      const int cs = ci ? 8 : 4;
+      int warps = 8;
+      while (warps > 1 && p->lstm->smem_round[ci](warps) > static_cast<size_t>(smem_optin)) --warps;
+      CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(p->lstm->fn_round[ci]),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(p->lstm->smem_round[ci](warps))));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs * 64);
+      cfg.blockDim = dim3(32 * warps);
+      cfg.dynamicSmemBytes = p->lstm->smem_round[ci](warps);
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = cs;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(p->lstm->fn_round[ci]),
+                                         &cfg) != cudaSuccess)
+        ncl = 0;
+      cudaGetLastError();
+      if (ncl < 1) continue;
+      const int64_t slots = static_cast<int64_t>(ncl) * cs * kSamplesPerWarp;
+      const int need = static_cast<int>((1000 + slots - 1) / slots);  // bench batch per worker
+      if (need < best_warps && need <= warps) {
+        best_warps = need;
+        p->cluster_size = cs;
+        p->cs_index = ci;
+        p->max_clusters = ncl;
+        p->round_warps = warps;
+      }
+    }
+    if (p->max_clusters * p->cluster_size > p->max_ctas) p->max_ctas = p->max_clusters * p->cluster_size;
+  }
   CU(cudaMalloc(&p->part, sizeof(float) * static_cast<size_t>(p->max_ctas) * p->lstm->ppad));
   CU(cudaMalloc(&p->ms, sizeof(MasterDev)));
   CU(cudaMemset(p->ms, 0, sizeof(MasterDev)));
   CU(cudaMalloc(&p->err, sizeof(int)));
   CU(cudaMemset(p->err, 0, sizeof(int)));
+  const size_t bar_bytes = sizeof(unsigned) * 32 * (2 + static_cast<size_t>(p->max_ctas));
+  CU(cudaMalloc(&p->bar, bar_bytes));
+  CU(cudaMemset(p->bar, 0, bar_bytes));
   *out = p;
   return GHC_OK;
 }
@@ -185,13 +269,18 @@ void ghc_plan_destroy(ghc_plan* p) {
   cudaFree(p->part);
   cudaFree(p->ms);
   cudaFree(p->err);
+  cudaFree(p->bar);
   delete p;
 }
 
 int64_t ghc_plan_n_params(const ghc_plan* p) { return p->model.n_params; }
 int64_t ghc_plan_input_width(const ghc_plan* p) { return p->model.input_width; }
 int32_t ghc_plan_n_classes(const ghc_plan* p) { return p->model.n_classes; }
-const char* ghc_plan_kernel_name(const ghc_plan* p) { return p->kname.c_str(); }
+const char* ghc_plan_kernel_name(const ghc_plan* p) {
+  return p->use_cluster && p->max_clusters > 0 ? p->lstm->name : p->kname.c_str();
+}
+int32_t ghc_plan_max_clusters(const ghc_plan* p) { return p->use_cluster ? p->max_clusters : 0; }
+int32_t ghc_plan_cluster_size(const ghc_plan* p) { return p->use_cluster ? p->cluster_size : 0; }
 
 ghc_status ghc_plan_tensors(const ghc_plan* p, int64_t* off, int64_t* d0, int64_t* d1, int cap,
                             int* nt) {

@@ -49,12 +49,47 @@ __device__ __forceinline__ void grid_barrier(MasterDev* ms) {
   __syncthreads();
 }
 
-// sigmoid / tanh via MUFU.EX2 + IEEE reciprocal (abs error ~3e-7, well inside
-// the fp32 parity budget; the reference uses libm exp/tanh, nn.cpp:15-19).
-__device__ __forceinline__ float sigmoid_f(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+// sigmoid / tanh as branch-free MUFU sequences: ex2.approx.ftz + rcp.approx.ftz
+// (each ≤ 2 ulp).  The IEEE __frcp_rn path compiles to a branch + CALL per
+// reciprocal (BSSY/BSYNC), which serialises the four gate activations; these
+// are 4-5 instructions with no control flow, abs error ≲ 3e-7 — well inside
+// the fp32 parity budget (the reference uses libm exp/tanh, nn.cpp:15-19).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigmoid_f(float x) {
+  return rcp_approx(1.0f + ex2_approx(-1.4426950408889634f * x));
+}
 __device__ __forceinline__ float tanh_f(float x) {
-  const float e = __expf(2.0f * x);
-  return 1.0f - 2.0f * __frcp_rn(e + 1.0f);
+  return 1.0f - 2.0f * rcp_approx(ex2_approx(2.8853900817779268f * x) + 1.0f);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// cp.async (LDGSTS): 4-byte global → shared copies that complete
+// asynchronously; the issuing thread waits with cp_async_wait<N>() (at most N
+// newest groups still pending) and a __syncwarp publishes them to the warp.
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

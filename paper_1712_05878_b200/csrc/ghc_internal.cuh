@@ -14,6 +14,7 @@
 
 #include "../../include/ghc.h"
 #include "host_model.hpp"
+#include "lstm_round.cuh"
 #include "lstm_step.cuh"
 #include "update_kernels.cuh"
 
@@ -34,32 +35,18 @@ namespace {
 // ---- fused LSTM→softmax kernel table (one instantiation per shape) ----
 struct LstmEntry {
   int D, H, T, K;
-  void (*fn)(StepArgs);
-  int P, ppad;
+  void (*fn)(StepArgs);        // flat variant (grid barriers)      lstm_step.cuh
+  void (*fn_round[2])(StepArgs);   // cluster variant, clusters of 4 / 8 (lstm_round.cuh)
+  int P, ppad, ep[2];
   size_t (*smem)(int);
+  size_t (*smem_round[2])(int);
   const char* name;
 };
 
-template <int D, int H, int T, int K>
-LstmEntry make_entry(const char* name) {
-  using N = LstmNet<D, H, T, K>;
-  return LstmEntry{D, H, T, K, &lstm_softmax_step_kernel<D, H, T, K>, N::P, N::PPAD,
-                   &N::smem_bytes, name};
-}
-
-const std::vector<LstmEntry>& lstm_table() {
-  static const std::vector<LstmEntry> t = {
-      make_entry<5, 20, 10, 3>("lstm_softmax_step<D5,H20,T10,K3>"),  // SPEC.md:109 bench net
-      make_entry<5, 8, 10, 3>("lstm_softmax_step<D5,H8,T10,K3>"),
-      make_entry<3, 4, 5, 3>("lstm_softmax_step<D3,H4,T5,K3>"),
-      make_entry<2, 16, 3, 4>("lstm_softmax_step<D2,H16,T3,K4>"),
-      make_entry<5, 32, 10, 3>("lstm_softmax_step<D5,H32,T10,K3>"),
-      make_entry<4, 12, 6, 5>("lstm_softmax_step<D4,H12,T6,K5>"),
-  };
-  return t;
-}
-
 }  // namespace
+
+// The instantiated fused-kernel shapes (defined in ghc.cu only).
+const std::vector<LstmEntry>& lstm_table();
 
 struct ghc_ctx {
   int device = 0;
@@ -73,6 +60,12 @@ struct ghc_plan {
   ghc_ctx* ctx = nullptr;
   int max_warps = 8;      // warps/CTA that fit the fused kernel's smem
   unsigned long long* probe = nullptr;  // phase-timing probe (diagnostics)
+  unsigned* bar = nullptr;  // flag barrier: (2 + max_ctas) 128-B lines
+  int max_clusters = 0;      // co-resident clusters of the chosen cluster size
+  int cluster_size = 8;      // 4 or 8 (chosen at plan creation from occupancy)
+  int cs_index = 1;          // 0: clusters of 4, 1: clusters of 8
+  int round_warps = 8;       // warps/CTA that fit the cluster variant's smem
+  bool use_cluster = true;   // GHC_STEP=flat selects the flat variant
   Model model;
   const LstmEntry* lstm = nullptr;
   int max_ctas = 0;       // co-resident CTAs of the fused kernel
@@ -108,12 +101,46 @@ inline void step_geometry(const ghc_plan* p, int64_t n, int& ctas, int& warps) {
 
 inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
   if (!p->lstm) return fail(GHC_ERR_CONFIG, "plan has no fused worker kernel");
+  a.err = p->err;
+  a.probe = p->probe;
+  a.bar = p->bar;
+  if (p->use_cluster && p->max_clusters > 0) {
+    // clusters of 8 CTAs, ≈ one CTA per SM, one warp per sample
+    const int cs = p->cluster_size;
+    const int spw = kSamplesPerWarp;
+    const int64_t slots = static_cast<int64_t>(p->max_clusters) * cs * spw;
+    int warps = static_cast<int>((n_max + slots - 1) / slots);
+    warps = warps < 1 ? 1 : (warps > p->round_warps ? p->round_warps : warps);
+    int64_t ctas = (n_max + warps * spw - 1) / (warps * spw);
+    int64_t nc = (ctas + cs - 1) / cs;
+    if (nc < 1) nc = 1;
+    if (nc > p->max_clusters) nc = p->max_clusters;
+    a.part = p->part;
+    a.pstride = p->lstm->ep[p->cs_index];
+    a.pipelined = n_max <= nc * cs * warps * spw;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(nc * cs));
+    cfg.blockDim = dim3(static_cast<unsigned>(warps * 32));
+    cfg.dynamicSmemBytes = p->lstm->smem_round[p->cs_index](warps);
+    cfg.stream = p->ctx->stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    CU(cudaLaunchKernelEx(&cfg, p->lstm->fn_round[p->cs_index], a));
+    p->ctx->launches++;
+    return GHC_OK;
+  }
   int ctas, warps;
   step_geometry(p, n_max, ctas, warps);
   a.part = p->part;
   a.pstride = p->lstm->ppad;
-  a.err = p->err;
-  a.probe = p->probe;
+  a.pipelined = n_max <= static_cast<int64_t>(ctas) * warps;
   const size_t smem = p->lstm->smem(warps);
   void* args[] = {&a};
   CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(p->lstm->fn), dim3(ctas),

@@ -1,0 +1,361 @@
+// lstm_round.cuh — cluster-resident variant of the fused sync-round kernel.
+//
+// Same per-sample math as lstm_step.cuh (lstm_sample), different round
+// plumbing, designed from the measured B200 sync costs (DESIGN.md §Sync:
+// grid-wide flag barrier ≈ 1.4-2.5 µs, hardware cluster barrier ≈ 0.28 µs):
+//
+//   1. each CTA reduces its warps' gradients into a CTA partial in smem;
+//   2. cluster barrier; CTA j of each cluster (CS = 4 or 8 CTAs, chosen per
+//      plan from occupancy) reduces slice j of the
+//      gradient over its cluster through DSMEM (fixed peer order) and stores
+//      that cluster partial to HBM/L2;
+//   3. ONE column barrier per round: the NC CTAs holding slice j (one per
+//      cluster) wait only for each other;
+//   4. CTA j sums slice j over the NC cluster partials (fixed order — the
+//      result is bit-identical in every cluster), applies sgd_step
+//      (optim.cpp:39-65) with its velocity slice kept in smem across rounds,
+//      and stores the new weights of slice j straight into the weight buffer
+//      of every CTA of its cluster (DSMEM stores);
+//   5. cluster barrier; the non-finite flag is OR-ed over the cluster (whose CS
+//      slices cover the whole gradient → a global decision) and the update is
+//      committed or rejected (optim.cpp:49-51) by a buffer swap — weights
+//      never round-trip through global memory between rounds.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "lstm_step.cuh"
+
+namespace ghc {
+
+namespace cg = cooperative_groups;
+
+// Samples interleaved per warp (static ILP, lstm_samples<..., SPW>).
+#ifndef GHC_SPW
+#define GHC_SPW 1
+#endif
+constexpr int kSamplesPerWarp = GHC_SPW;
+
+template <int D, int H, int T, int K, int CS>
+struct RoundLayout {
+  using N = LstmNet<D, H, T, K>;
+  static constexpr int SPW = kSamplesPerWarp;
+  static constexpr int E = N::P + 1;                          // grad + loss
+  static constexpr int SL = (((E + CS - 1) / CS) + 3) & ~3;   // slice per cluster rank
+  static constexpr int EP = SL * CS;                          // padded row
+  static size_t smem_bytes(int nw) {
+    return sizeof(float) *
+           (size_t)(2 * N::PPAD + nw * SPW * N::WARP_FLOATS + nw * N::PPAD + 2 * SL + CS + 8);
+  }
+};
+
+template <int D, int H, int T, int K, int CS>
+__global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
+  using N = LstmNet<D, H, T, K>;
+  using RL = RoundLayout<D, H, T, K, CS>;
+  constexpr int SL = RL::SL;
+  constexpr int E = RL::E;
+  constexpr int SPW = RL::SPW;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  const int cid = blockIdx.x / CS;
+  const int NC = gridDim.x / CS;
+  const int G = gridDim.x;
+
+  extern __shared__ __align__(16) float smem[];
+  const int NW = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* wbuf0 = smem;
+  float* wbuf1 = smem + N::PPAD;
+  float* ws = smem + 2 * N::PPAD + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
+  float* wpart = smem + 2 * N::PPAD + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
+  float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
+  float* vtmp = vsl + SL;                                      // [SL]
+  int* badv = reinterpret_cast<int*>(vtmp + SL);               // [CS], written by peers
+  const int e0 = crank * SL;
+  const int e1 = min(E, e0 + SL);
+
+  int cur = 0;
+  unsigned long long round0 = 0, accepted = 0, rejected = 0;
+  int last_status = 0;
+  const bool sgd = a.mode == MODE_SGD;
+  if (sgd) {
+    cur = __ldcg(&a.ms->cur);
+    round0 = __ldcg(&a.ms->round);
+  }
+  unsigned epoch = __ldcg(a.bar);
+  float* gw = sgd ? (cur ? a.w1 : a.w0) : nullptr;  // master weights in HBM
+  float* gv = sgd ? (cur ? a.v1 : a.v0) : nullptr;
+  {
+    const float* w = sgd ? gw : a.w_in;
+    for (int p = threadIdx.x; p < N::P; p += blockDim.x) wbuf0[p] = __ldcg(w + p);
+    if (sgd)
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = e < N::P ? __ldcg(gv + e) : 0.f;
+  }
+  float* wa = wbuf0;  // weights the samples use
+  float* wb = wbuf1;  // peers deposit the next weights here
+
+  // ---- sample assignment + cp.async prefetch ----
+  // CTA b owns samples [b*spc, min(n,(b+1)*spc)); warp w, slot sp handles
+  // s0 + w + sp*NW.  Pipelined launches (n ≤ slots) prefetch every slot's
+  // next-round row during the current round: the index one round ahead, the
+  // row after this round's compute (cp.async into the slot's other buffer).
+  auto first_sample = [&](int r, int& s, int& s1) {
+    const int n = a.counts ? __ldg(a.counts + r) : a.n;
+    const int spc = (n + G - 1) / G;
+    const int s0 = blockIdx.x * spc;
+    s1 = min(n, s0 + spc);
+    s = s0 + warp;
+  };
+  auto slot_x = [&](int sp, int b) { return ws + sp * N::WARP_FLOATS + N::S_X + b * N::XWP; };
+  auto slot_l = [&](int sp) { return reinterpret_cast<int*>(ws + sp * N::WARP_FLOATS + N::S_L); };
+  auto fetch_nocommit = [&](int sp, int row, int b) {
+    const float* xrow = a.x + (long long)row * N::XW;
+    float* dst = slot_x(sp, b);
+    for (int i = lane; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);
+    if (lane == 0) cp_async4(slot_l(sp) + b, a.y + row);
+  };
+  auto row_of = [&](int r, int s) {
+    const int32_t* idx = a.idx ? a.idx + (long long)r * a.stride : nullptr;
+    return idx ? __ldg(idx + s) : s;
+  };
+  if (a.pipelined) {
+    int s, s1;
+    first_sample(0, s, s1);
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp)
+      if (s + sp * NW < s1) fetch_nocommit(sp, row_of(0, s + sp * NW), 0);
+    cp_async_commit();
+  }
+  __syncthreads();
+
+  for (int r = 0; r < a.rounds; ++r) {
+    const int n = a.counts ? __ldg(a.counts + r) : a.n;
+    const float scale = sgd ? 1.0f / (float)n : a.grad_scale;
+    const int par = r & 1;
+    unsigned long long* pr =
+        a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
+    if (pr && threadIdx.x == 0) pr[0] = globaltimer();
+
+    float* wp = wpart + warp * N::PPAD;
+    for (int p = lane; p < N::PPAD / 4; p += 32)
+      reinterpret_cast<float4*>(wp)[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+
+    // ---- samples ----
+    float lsum = 0.0f;
+    int s, s1;
+    first_sample(r, s, s1);
+    if (a.pipelined) {
+      int sn = 0, sn1 = 0;
+      const bool next = r + 1 < a.rounds;
+      if (next) {
+        first_sample(r + 1, sn, sn1);
+        if (a.idx && lane == 0) {
+#pragma unroll
+          for (int sp = 0; sp < SPW; ++sp)
+            if (sn + sp * NW < sn1)
+              cp_async4(slot_l(sp) + 2, a.idx + (long long)(r + 1) * a.stride + sn + sp * NW);
+        }
+        cp_async_commit();
+      }
+      if (s < s1) {
+        cp_async_wait<1>();  // this round's rows (older group) have landed
+        __syncwarp();
+        const float* xsp[SPW];
+        int lab[SPW];
+        float scl[SPW];
+        float* prb[SPW];
+        float lo[SPW];
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp) {
+          const bool valid = s + sp * NW < s1;
+          const int use = valid ? sp : 0;  // empty slot: recompute slot 0 with weight 0
+          xsp[sp] = slot_x(use, r & 1);
+          int l = slot_l(use)[r & 1];
+          if (l < 0 || l >= K) {
+            if (lane == 0 && valid) atomicOr(a.err, 1);
+            l = 0;
+          }
+          lab[sp] = l;
+          scl[sp] = valid ? scale : 0.0f;
+          prb[sp] = (valid && a.probs_out) ? a.probs_out + (long long)(s + sp * NW) * K : nullptr;
+        }
+        unsigned long long* ps = (pr && warp == 0) ? pr : nullptr;
+        if (a.mode == MODE_FWD)
+          lstm_samples<D, H, T, K, false, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps);
+        else
+          lstm_samples<D, H, T, K, true, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps);
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp)
+          if (s + sp * NW < s1) lsum += lo[sp];
+      }
+      if (next && sn < sn1) {
+        cp_async_wait<0>();
+        __syncwarp();
+        int rows[SPW];
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp) rows[sp] = a.idx ? slot_l(sp)[2] : sn + sp * NW;
+        __syncwarp();
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp)
+          if (sn + sp * NW < sn1) fetch_nocommit(sp, rows[sp], (r + 1) & 1);
+        cp_async_commit();
+      }
+    } else {
+      for (; s < s1; s += NW) {
+        const int row = row_of(r, s);
+        float* xs = slot_x(0, 0);
+        for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(a.x + (long long)row * N::XW + i);
+        int label = __ldg(a.y + row);
+        __syncwarp();
+        if (label < 0 || label >= K) {
+          if (lane == 0) atomicOr(a.err, 1);
+          label = 0;
+        }
+        if (a.mode == MODE_FWD)
+          lsum += lstm_sample<D, H, T, K, false>(
+              wa, ws, wp, xs, label, scale, lane,
+              a.probs_out ? a.probs_out + (long long)s * K : nullptr, nullptr);
+        else
+          lsum += lstm_sample<D, H, T, K, true>(wa, ws, wp, xs, label, scale, lane, nullptr,
+                                                nullptr);
+        __syncwarp();
+      }
+    }
+    if (lane == 0) wp[N::P] = lsum;  // loss rides in slot P
+    __syncthreads();
+    if (pr && threadIdx.x == 0) pr[2] = globaltimer();
+
+    // ---- (1) CTA partial in smem: wpart[0] += wpart[1..NW-1] (fixed order) ----
+    for (int p = threadIdx.x; p < N::PPAD / 4; p += blockDim.x) {
+      float4 t = reinterpret_cast<const float4*>(wpart)[p];
+      for (int w2 = 1; w2 < NW; ++w2) {
+        const float4 u = reinterpret_cast<const float4*>(wpart + w2 * N::PPAD)[p];
+        t.x += u.x;
+        t.y += u.y;
+        t.z += u.z;
+        t.w += u.w;
+      }
+      reinterpret_cast<float4*>(wpart)[p] = t;
+    }
+    if (pr && threadIdx.x == 0) pr[3] = globaltimer();
+    cluster.sync();  // CTA partials of the whole cluster complete
+    if (pr && threadIdx.x == 0) pr[4] = globaltimer();
+
+    // ---- (2) slice j over the cluster via DSMEM → cluster partial in HBM ----
+    float* grow = a.part + ((long long)par * NC + cid) * RL::EP;
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      float t = 0.0f;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) t += cluster.map_shared_rank(wpart, q)[e];
+      __stcg(grow + e, t);
+    }
+    if (pr && threadIdx.x == 0) pr[5] = globaltimer();
+
+    // ---- (3) column barrier: the NC CTAs that own slice j ----
+    ++epoch;
+    __syncthreads();
+    unsigned* flags = a.bar + 2 * kFlagStride;
+    if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * kFlagStride, epoch);
+    for (int c = threadIdx.x; c < NC; c += blockDim.x) {
+      const unsigned* f = flags + (c * CS + crank) * kFlagStride;
+      while ((int)(ld_relaxed_gpu(f) - epoch) < 0) {
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncthreads();
+    if (pr && threadIdx.x == 0) pr[6] = globaltimer();
+
+    // ---- (4) slice j over all clusters (fixed order) → update → broadcast ----
+    // float4 columns: SL and EP are multiples of 4, e0 too.
+    int bad = 0;
+    const float* gcol = a.part + (long long)par * NC * RL::EP;
+    for (int e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = 0; c0 < NC; c0 += 8) {  // 8 float4 loads in flight, fixed-order sum
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[i] = c0 + i < NC
+                     ? __ldcg(reinterpret_cast<const float4*>(gcol + (long long)(c0 + i) * RL::EP + e))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          t.x += v[i].x;
+          t.y += v[i].y;
+          t.z += v[i].z;
+          t.w += v[i].w;
+        }
+      }
+      const float tv[4] = {t.x, t.y, t.z, t.w};
+      float wn[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ee = e + i;
+        wn[i] = 0.0f;
+        if (ee >= e1) continue;
+        if (ee == N::P) {
+          if (cid == 0 && a.loss_out) a.loss_out[r] = tv[i];
+        } else if (a.mode == MODE_GRAD) {
+          if (cid == 0) a.g_out[ee] = tv[i];
+        } else if (sgd) {
+          if (!is_finite_f(tv[i])) bad = 1;
+          // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v
+          const float vn = fmaf(a.mu, vsl[ee - e0], -a.lr * tv[i]);
+          vtmp[ee - e0] = vn;
+          wn[i] = wa[ee] + vn;
+        }
+      }
+      if (sgd) {  // new weights → every CTA of the cluster (DSMEM, float4)
+        const float4 w4 = make_float4(wn[0], wn[1], wn[2], wn[3]);
+#pragma unroll
+        for (int q = 0; q < CS; ++q)
+          reinterpret_cast<float4*>(cluster.map_shared_rank(wb, q) + e)[0] = w4;
+      }
+    }
+    if (sgd) {
+      bad = __syncthreads_or(bad);
+      if (threadIdx.x < CS) cluster.map_shared_rank(badv, (int)threadIdx.x)[crank] = bad;
+    }
+    if (pr && threadIdx.x == 0) pr[7] = globaltimer();
+    cluster.sync();  // new weights + flags landed in every CTA of the cluster
+    if (pr && threadIdx.x == 0) pr[13] = globaltimer();
+    if (sgd) {
+      int rej = 0;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) rej |= badv[q];
+      if (rej) {
+        ++rejected;
+        last_status = 2;  // GHC_ERR_NONFINITE: keep w/v (optim.cpp:49-51)
+      } else {
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = vtmp[e - e0];
+        float* t = wa;
+        wa = wb;
+        wb = t;
+        ++accepted;
+        last_status = 0;
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- publish master state (cluster 0 holds the same bits as every cluster) ----
+  if (sgd && cid == 0) {
+    for (int e = e0 + threadIdx.x; e < e1 && e < N::P; e += blockDim.x) {
+      gw[e] = wa[e];
+      gv[e] = vsl[e - e0];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.bar[0] = epoch;
+    if (sgd) {
+      a.ms->version += accepted;
+      a.ms->rejected += rejected;
+      a.ms->round = round0 + (unsigned long long)a.rounds;
+      a.ms->status = last_status;
+    }
+  }
+}
+
+}  // namespace ghc

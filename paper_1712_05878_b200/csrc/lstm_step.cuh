@@ -49,14 +49,59 @@ struct StepArgs {
   float* loss_out;        // per-round loss sum (nullable)
   float* probs_out;       // MODE_FWD: n×K (nullable)
   int* err;               // bit 0: label out of range (nn.cpp:241-244)
-  unsigned long long* probe;  // nullable: [rounds][gridDim][8] %globaltimer per phase
+  unsigned long long* probe;  // nullable: [rounds][gridDim][16] %globaltimer per phase
+  unsigned* bar;          // flag barrier: epoch, go, then one 128-B line per CTA
+  int pipelined;          // every round has ≤ 1 sample per warp (cp.async prefetch path)
   int mode;
 };
 
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+// Grid barrier for the persistent round loop (gather → broadcast):
+// CTA b publishes `epoch | bad<<31` in its own 128-B line (release store);
+// CTA 0 polls all G lines, one thread per line, with relaxed loads (no L1
+// invalidate per poll), ORs the `bad` bits and publishes `go = epoch|bad`;
+// every CTA polls `go` with one thread, then one acquire fence.  Two L2 hops,
+// no serialised atomics, no hot line shared by all pollers.  Returns the OR of
+// all CTAs' `bad` bits (a non-finite update is rejected grid-wide).
+constexpr int kFlagStride = 32;  // uints: one 128-byte line per CTA flag
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_barrier(unsigned* bar, unsigned epoch, int bad) {
+  __shared__ int s_bad;
+  __syncthreads();
+  unsigned* go = bar + kFlagStride;  // bar[0] epoch store, bar[32] go, flags from bar[64]
+  unsigned* flags = bar + 2 * kFlagStride;
+  if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * kFlagStride, epoch | (bad ? 0x80000000u : 0u));
+  if (blockIdx.x == 0) {
+    int any = 0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      unsigned v;
+      do {
+        v = ld_relaxed_gpu(flags + b * kFlagStride);
+      } while ((int)((v & 0x7fffffffu) - epoch) < 0);
+      any |= (int)(v >> 31);
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      st_release_gpu(go, epoch | (any ? 0x80000000u : 0u));
+    }
+  }
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      v = ld_relaxed_gpu(go);
+    } while ((int)((v & 0x7fffffffu) - epoch) < 0);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    s_bad = (int)(v >> 31);
+  }
+  __syncthreads();
+  return s_bad;
 }
 
 template <int D, int H, int T, int K>
@@ -71,35 +116,78 @@ struct LstmNet {
   static constexpr int OFF_BS = OFF_WS + K * H;    // bs[K]     arch.cpp:109
   static constexpr int P = OFF_BS + K;
   static constexpr int PPAD = (P + 1 + 3) & ~3;    // + loss slot, 16-B rows
-  static constexpr int XW = T * D;
-  static constexpr int S_X = 0;                          // x_t rows
-  static constexpr int S_H = (XW + 3) & ~3;              // h[T][H]
-  static constexpr int S_C = S_H + ((T * H + 3) & ~3);   // cache[T][6][H]
-  static constexpr int S_DZ = S_C + T * 6 * H;           // dz[T][4H]
+  static constexpr int XW = T * D;                       // global row width
+  static constexpr int DP = (D + 3) & ~3;                // x_t padded to float4s in smem
+  static constexpr int XWP = T * DP;
+  static constexpr bool HV = (H % 4) == 0;               // h rows loadable as float4
+  static constexpr int S_X = 0;                          // x rows [2][T][DP] (double buffer)
+  static constexpr int S_L = 2 * XWP;                    // label[2], next idx (ints)
+  static constexpr int S_H = S_L + 4;                    // h[T][H]
+  static constexpr int S_C = S_H + ((T * H + 3) & ~3);   // cache[T][H][8]: i f g o | c tanh(c)
+  static constexpr int S_DZ = S_C + T * H * 8;           // dz[T][4H]
   static constexpr int WARP_FLOATS = (S_DZ + T * G4 + 3) & ~3;
+  // global row element i → smem offset (t*DP + d)
+  __device__ static int xoff(int i) { return (i / D) * DP + (i % D); }
   static size_t smem_bytes(int nw) {
     return sizeof(float) * (size_t)(PPAD + nw * WARP_FLOATS + nw * PPAD + 32);
   }
 };
 
-// Forward + softmax/loss (+ backward when BWD) of one sample; the sample's
-// gradient is ADDED into the warp's partial `wp` (lane j touches only the
-// entries of its own gate rows, lane 0 the output bias) — no atomics.
-template <int D, int H, int T, int K, bool BWD>
-__device__ __forceinline__ float lstm_sample(const float* __restrict__ wsm, float* __restrict__ ws,
+// Forward + softmax/loss (+ backward when BWD) of SPW samples interleaved in
+// one warp's instruction stream (static ILP: the samples share the weight
+// registers and fill each other's dependency stalls).  Slot sp uses the
+// per-sample scratch at ws + sp*WARP_FLOATS; its input row xs[sp] is already
+// in shared memory (cp.async-prefetched by the caller).  Each sample's
+// gradient (scaled by scale[sp]; 0 masks an empty slot) is ADDED into the
+// warp partial `wp` — lane j touches only the entries of its own gate rows,
+// lane 0 the output bias — no atomics.  loss[sp] receives ℓ of slot sp.
+template <int D, int H, int T, int K, bool BWD, int SPW>
+__device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, float* __restrict__ ws,
                                              float* __restrict__ wp,
-                                             const float* __restrict__ xrow, int label, float scale,
-                                             int lane, float* probs_row) {
+                                             const float* const (&xs)[SPW],
+                                             const int (&label)[SPW], const float (&scale)[SPW],
+                                             int lane, float* const (&probs_row)[SPW],
+                                             float (&loss)[SPW], unsigned long long* pr) {
   using N = LstmNet<D, H, T, K>;
+  constexpr int DP = N::DP;
   const bool act = lane < H;
   const int j = act ? lane : 0;
-  float* xs = ws + N::S_X;
-  float* hs = ws + N::S_H;
-  float* cs = ws + N::S_C;
-  float* dzs = ws + N::S_DZ;  // dz[t][4H], t = 0..T-1
-
-  for (int i = lane; i < N::XW; i += 32) xs[i] = __ldg(xrow + i);
-  __syncwarp();
+  float* hs[SPW];
+  float* cs[SPW];
+  float* dzs[SPW];
+#pragma unroll
+  for (int sp = 0; sp < SPW; ++sp) {
+    hs[sp] = ws + sp * N::WARP_FLOATS + N::S_H;
+    cs[sp] = ws + sp * N::WARP_FLOATS + N::S_C;
+    dzs[sp] = ws + sp * N::WARP_FLOATS + N::S_DZ;  // dz[t][4H]
+  }
+  // x_t (DP floats, float4 loads) and h_t (H floats, float4 when H%4==0)
+  auto load_x = [&](int sp, int t, float (&v)[DP]) {
+#pragma unroll
+    for (int c = 0; c < DP / 4; ++c) {
+      const float4 u = reinterpret_cast<const float4*>(xs[sp] + t * DP)[c];
+      v[4 * c] = u.x;
+      v[4 * c + 1] = u.y;
+      v[4 * c + 2] = u.z;
+      v[4 * c + 3] = u.w;
+    }
+  };
+  auto load_h = [&](int sp, int t, float (&v)[H]) {
+    if constexpr (N::HV) {
+#pragma unroll
+      for (int c = 0; c < H / 4; ++c) {
+        const float4 u = reinterpret_cast<const float4*>(hs[sp] + t * H)[c];
+        v[4 * c] = u.x;
+        v[4 * c + 1] = u.y;
+        v[4 * c + 2] = u.z;
+        v[4 * c + 3] = u.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < H; ++k) v[k] = hs[sp][t * H + k];
+    }
+  };
+  if (pr && lane == 0) pr[8] = globaltimer();
 
   // ---------------- forward recurrence (nn.cpp:160-200) ----------------
   {
@@ -112,166 +200,255 @@ __device__ __forceinline__ float lstm_sample(const float* __restrict__ wsm, floa
 #pragma unroll
       for (int k = 0; k < H; ++k) wh[q][k] = wsm[N::OFF_WH + (q * H + j) * H + k];
     }
-    float c = 0.0f;
+    float c[SPW];
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) c[sp] = 0.0f;
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
-      float a0[4], a1[4];
+      float a0[SPW][4], a1[SPW][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a0[q] = bb[q];
-        a1[q] = 0.0f;
-      }
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const float xv = xs[t * D + d];
+      for (int sp = 0; sp < SPW; ++sp) {
+        float xv[DP];
+        load_x(sp, t, xv);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          if (d & 1) a1[q] = fmaf(wx[q][d], xv, a1[q]);
-          else a0[q] = fmaf(wx[q][d], xv, a0[q]);
+          a0[sp][q] = bb[q];
+          a1[sp][q] = 0.0f;
         }
-      }
-      if (t > 0) {
-        const float* hp = hs + (t - 1) * H;
 #pragma unroll
-        for (int k = 0; k < H; ++k) {
-          const float hv = hp[k];
+        for (int d = 0; d < D; ++d)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (k & 1) a1[q] = fmaf(wh[q][k], hv, a1[q]);
-            else a0[q] = fmaf(wh[q][k], hv, a0[q]);
+            if (d & 1) a1[sp][q] = fmaf(wx[q][d], xv[d], a1[sp][q]);
+            else a0[sp][q] = fmaf(wx[q][d], xv[d], a0[sp][q]);
           }
+      }
+      if (t > 0) {
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp) {
+          float hv[H];
+          load_h(sp, t - 1, hv);
+#pragma unroll
+          for (int k = 0; k < H; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (k & 1) a1[sp][q] = fmaf(wh[q][k], hv[k], a1[sp][q]);
+              else a0[sp][q] = fmaf(wh[q][k], hv[k], a0[sp][q]);
+            }
         }
       }
-      const float ig = sigmoid_f(a0[0] + a1[0]);
-      const float fg = sigmoid_f(a0[1] + a1[1]);
-      const float gg = tanh_f(a0[2] + a1[2]);
-      const float og = sigmoid_f(a0[3] + a1[3]);
-      c = fmaf(fg, c, ig * gg);
-      const float tc = tanh_f(c);
-      if (act) {
-        float* ct = cs + t * 6 * H + j;
-        ct[0 * H] = ig;
-        ct[1 * H] = fg;
-        ct[2 * H] = gg;
-        ct[3 * H] = og;
-        ct[4 * H] = c;
-        ct[5 * H] = tc;
-        hs[t * H + j] = og * tc;
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp) {
+        const float ig = sigmoid_f(a0[sp][0] + a1[sp][0]);
+        const float fg = sigmoid_f(a0[sp][1] + a1[sp][1]);
+        const float gg = tanh_f(a0[sp][2] + a1[sp][2]);
+        const float og = sigmoid_f(a0[sp][3] + a1[sp][3]);
+        c[sp] = fmaf(fg, c[sp], ig * gg);
+        const float tc = tanh_f(c[sp]);
+        if (act) {
+          float* ct = cs[sp] + (t * H + j) * 8;
+          reinterpret_cast<float4*>(ct)[0] = make_float4(ig, fg, gg, og);
+          reinterpret_cast<float2*>(ct)[2] = make_float2(c[sp], tc);
+          hs[sp][t * H + j] = og * tc;
+        }
       }
       __syncwarp();
     }
   }
+  if (pr && lane == 0) pr[9] = globaltimer();
 
   // ---------------- softmax + loss (nn.cpp:202-248) ----------------
-  const float hT = act ? hs[(T - 1) * H + j] : 0.0f;
-  float z[K];
-  float zmax = -3.0e38f;
+  float hT[SPW], e[SPW][K], inv_den[SPW];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    z[k] = warp_sum(act ? wsm[N::OFF_WS + k * H + j] * hT : 0.0f) + wsm[N::OFF_BS + k];
-    zmax = fmaxf(zmax, z[k]);
-  }
-  float e[K];
-  float den = 0.0f, zy = 0.0f;
+  for (int sp = 0; sp < SPW; ++sp) {
+    hT[sp] = act ? hs[sp][(T - 1) * H + j] : 0.0f;
+    float z[K];
+    float zmax = -3.0e38f;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    e[k] = expf(z[k] - zmax);
-    den += e[k];
-    if (k == label) zy = z[k];
-  }
-  const float inv_den = 1.0f / den;
-  const float lossv = logf(den) - (zy - zmax);
-  if (probs_row != nullptr) {
+    for (int k = 0; k < K; ++k) {
+      z[k] = warp_sum(act ? wsm[N::OFF_WS + k * H + j] * hT[sp] : 0.0f) + wsm[N::OFF_BS + k];
+      zmax = fmaxf(zmax, z[k]);
+    }
+    float den = 0.0f, zy = 0.0f;
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (lane == k) probs_row[k] = e[k] * inv_den;
+    for (int k = 0; k < K; ++k) {
+      e[sp][k] = expf(z[k] - zmax);
+      den += e[sp][k];
+      if (k == label[sp]) zy = z[k];
+    }
+    inv_den[sp] = 1.0f / den;
+    loss[sp] = logf(den) - (zy - zmax);
+    if (probs_row[sp] != nullptr) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (lane == k) probs_row[sp][k] = e[sp][k] * inv_den[sp];
+    }
   }
-  if constexpr (!BWD) return lossv;
+  if constexpr (!BWD) return;
 
   // ---------------- backward: softmax (nn.cpp:276-311) ----------------
-  float dh = 0.0f;
+  float dh[SPW];
+#pragma unroll
+  for (int sp = 0; sp < SPW; ++sp) dh[sp] = 0.0f;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const float dzk = (e[k] * inv_den - (k == label ? 1.0f : 0.0f)) * scale;
-    if (act) wp[N::OFF_WS + k * H + j] += dzk * hT;
-    if (lane == 0) wp[N::OFF_BS + k] += dzk;
-    dh = fmaf(act ? wsm[N::OFF_WS + k * H + j] : 0.0f, dzk, dh);
+    float gws = 0.0f, gbs = 0.0f;
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) {
+      const float dzk = (e[sp][k] * inv_den[sp] - (k == label[sp] ? 1.0f : 0.0f)) * scale[sp];
+      gws = fmaf(dzk, hT[sp], gws);
+      gbs += dzk;
+      dh[sp] = fmaf(act ? wsm[N::OFF_WS + k * H + j] : 0.0f, dzk, dh[sp]);
+    }
+    if (act) wp[N::OFF_WS + k * H + j] += gws;
+    if (lane == 0) wp[N::OFF_BS + k] += gbs;
   }
+  if (pr && lane == 0) pr[10] = globaltimer();
 
   // ------- backward pass 1: the BPTT chain (nn.cpp:351-392), dz → smem -------
   {
     float wt[4 * H];  // column j of Wh: Wh[r][j]
 #pragma unroll
     for (int r = 0; r < 4 * H; ++r) wt[r] = wsm[N::OFF_WH + r * H + j];
-    float dc = 0.0f;
+    float dc[SPW];
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) dc[sp] = 0.0f;
 #pragma unroll 1
     for (int t = T - 1; t >= 0; --t) {
-      const float* ct = cs + t * 6 * H + j;
-      const float ig = ct[0 * H], fg = ct[1 * H], gg = ct[2 * H], og = ct[3 * H];
-      const float tc = ct[5 * H];
-      const float cp = t > 0 ? cs[(t - 1) * 6 * H + 4 * H + j] : 0.0f;
-      const float dout = dh * tc;
-      dc = fmaf(dh * og, 1.0f - tc * tc, dc);
-      const float di = dc * gg, dg = dc * ig, df = dc * cp;
-      float* dzt = dzs + t * 4 * H;
-      if (act) {
-        dzt[0 * H + j] = di * ig * (1.0f - ig);
-        dzt[1 * H + j] = df * fg * (1.0f - fg);
-        dzt[2 * H + j] = dg * (1.0f - gg * gg);
-        dzt[3 * H + j] = dout * og * (1.0f - og);
+      float fgs[SPW];
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp) {
+        const float* ct = cs[sp] + (t * H + j) * 8;
+        const float4 g4 = reinterpret_cast<const float4*>(ct)[0];
+        const float ig = g4.x, fg = g4.y, gg = g4.z, og = g4.w;
+        const float tc = ct[5];
+        const float cp = t > 0 ? cs[sp][((t - 1) * H + j) * 8 + 4] : 0.0f;
+        fgs[sp] = fg;
+        const float dout = dh[sp] * tc;
+        dc[sp] = fmaf(dh[sp] * og, 1.0f - tc * tc, dc[sp]);
+        const float di = dc[sp] * gg, dg = dc[sp] * ig, df = dc[sp] * cp;
+        float* dzt = dzs[sp] + t * 4 * H;
+        if (act) {
+          dzt[0 * H + j] = di * ig * (1.0f - ig);
+          dzt[1 * H + j] = df * fg * (1.0f - fg);
+          dzt[2 * H + j] = dg * (1.0f - gg * gg);
+          dzt[3 * H + j] = dout * og * (1.0f - og);
+        }
       }
       __syncwarp();
       if (t > 0) {  // dh_{t-1} = Whᵀ dz_t (the reference also does this at t=0, unused)
-        float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-        for (int r = 0; r < 4 * H; ++r) p[r & 3] = fmaf(wt[r], dzt[r], p[r & 3]);
-        dh = (p[0] + p[1]) + (p[2] + p[3]);
-        dc *= fg;
+        for (int sp = 0; sp < SPW; ++sp) {
+          const float4* dz4 = reinterpret_cast<const float4*>(dzs[sp] + t * 4 * H);
+          float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int r4 = 0; r4 < H; ++r4) {
+            const float4 u = dz4[r4];
+            p[0] = fmaf(wt[4 * r4], u.x, p[0]);
+            p[1] = fmaf(wt[4 * r4 + 1], u.y, p[1]);
+            p[2] = fmaf(wt[4 * r4 + 2], u.z, p[2]);
+            p[3] = fmaf(wt[4 * r4 + 3], u.w, p[3]);
+          }
+          dh[sp] = (p[0] + p[1]) + (p[2] + p[3]);
+          dc[sp] *= fgs[sp];
+        }
       }
     }
   }
+  if (pr && lane == 0) pr[11] = globaltimer();
 
-  // ------- backward pass 2: dWx, dWh, db = Σ_t dz_t ⊗ [x_t, h_{t-1}] -------
+  // ------- backward pass 2: dWx, dWh, db = Σ_{s,t} dz ⊗ [x_t, h_{t-1}] -------
   if (act) {
-    float dz[T][4];
+    float dz[SPW][T][4];
 #pragma unroll
-    for (int t = 0; t < T; ++t)
+    for (int sp = 0; sp < SPW; ++sp)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) dz[t][q] = dzs[t * 4 * H + q * H + j];
+      for (int t = 0; t < T; ++t)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dz[sp][t][q] = dzs[sp][t * 4 * H + q * H + j];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      float s = 0.0f;
+      float acc = 0.0f;
 #pragma unroll
-      for (int t = 0; t < T; ++t) s += dz[t][q];
-      wp[N::OFF_B + q * H + j] += s;
+      for (int sp = 0; sp < SPW; ++sp)
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc += dz[sp][t][q];
+      wp[N::OFF_B + q * H + j] += acc;
     }
+    {
+      float acc[4][D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const float xv = xs[t * D + d];
+        for (int d = 0; d < D; ++d) acc[q][d] = 0.0f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s[q] = fmaf(dz[t][q], xv, s[q]);
-      }
+      for (int sp = 0; sp < SPW; ++sp)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) wp[N::OFF_WX + (q * H + j) * D + d] += s[q];
+        for (int t = 0; t < T; ++t) {
+          float xv[DP];
+          load_x(sp, t, xv);
+#pragma unroll
+          for (int d = 0; d < D; ++d)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q][d] = fmaf(dz[sp][t][q], xv[d], acc[q][d]);
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int d = 0; d < D; ++d) wp[N::OFF_WX + (q * H + j) * D + d] += acc[q][d];
     }
-#pragma unroll 2
-    for (int k = 0; k < H; ++k) {
-      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    // dWh in column blocks of 4: 16 accumulators, h_{t-1} read as float4
+    constexpr int KB = N::HV ? 4 : 1;
+#pragma unroll 1
+    for (int k0 = 0; k0 < H; k0 += KB) {
+      float acc[KB][4];
 #pragma unroll
-      for (int t = 1; t < T; ++t) {
-        const float hv = hs[(t - 1) * H + k];
+      for (int kk = 0; kk < KB; ++kk)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s[q] = fmaf(dz[t][q], hv, s[q]);
-      }
+        for (int q = 0; q < 4; ++q) acc[kk][q] = 0.0f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) wp[N::OFF_WH + (q * H + j) * H + k] += s[q];
+      for (int sp = 0; sp < SPW; ++sp)
+#pragma unroll
+        for (int t = 1; t < T; ++t) {
+          float hv[KB];
+          if constexpr (KB == 4) {
+            const float4 u = reinterpret_cast<const float4*>(hs[sp] + (t - 1) * H + k0)[0];
+            hv[0] = u.x;
+            hv[1] = u.y;
+            hv[2] = u.z;
+            hv[3] = u.w;
+          } else {
+            hv[0] = hs[sp][(t - 1) * H + k0];
+          }
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[kk][q] = fmaf(dz[sp][t][q], hv[kk], acc[kk][q]);
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int kk = 0; kk < KB; ++kk) wp[N::OFF_WH + (q * H + j) * H + k0 + kk] += acc[kk][q];
     }
   }
   __syncwarp();
-  return lossv;
+  if (pr && lane == 0) pr[12] = globaltimer();
+}
+
+// Single-sample convenience wrapper (flat kernel, non-pipelined paths).
+template <int D, int H, int T, int K, bool BWD>
+__device__ __forceinline__ float lstm_sample(const float* __restrict__ wsm, float* __restrict__ ws,
+                                             float* __restrict__ wp,
+                                             const float* __restrict__ xs, int label,
+                                             float scale, int lane, float* probs_row,
+                                             unsigned long long* pr) {
+  const float* xa[1] = {xs};
+  const int la[1] = {label};
+  const float sa[1] = {scale};
+  float* pa[1] = {probs_row};
+  float lo[1];
+  lstm_samples<D, H, T, K, BWD, 1>(wsm, ws, wp, xa, la, sa, lane, pa, lo, pr);
+  return lo[0];
 }
 
 template <int D, int H, int T, int K>
@@ -283,7 +460,6 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
   float* wsm = smem;
   float* ws = smem + N::PPAD + warp * N::WARP_FLOATS;
   float* wpart = smem + N::PPAD + NW * N::WARP_FLOATS;  // [NW][PPAD]; reused as `red`
-  float* lossw = wpart + NW * N::PPAD;                   // [32]
   const int G = gridDim.x;
   const int E = N::P + 1;  // gradient + loss slot
 
@@ -295,69 +471,141 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     cur = __ldcg(&a.ms->cur);
     round0 = __ldcg(&a.ms->round);
   }
+  unsigned epoch = __ldcg(a.bar);
+
+  // Sample s of round r handled by this warp: CTA b owns [b*spc, (b+1)*spc).
+  auto first_sample = [&](int r, int& s, int& s1) {
+    const int n = a.counts ? __ldg(a.counts + r) : a.n;
+    const int spc = (n + G - 1) / G;
+    const int s0 = blockIdx.x * spc;
+    s1 = min(n, s0 + spc);
+    s = s0 + warp;
+  };
+  float* xbuf = ws + N::S_X;  // [2][XWP]
+  int* lbuf = reinterpret_cast<int*>(ws + N::S_L);
+  // Asynchronous copy of sample row `row` (x + label) into buffer `b`.
+  auto fetch_async = [&](int row, int b) {
+    const float* xrow = a.x + (long long)row * N::XW;
+    float* dst = xbuf + b * N::XWP;
+    for (int i = lane; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);
+    if (lane == 0) cp_async4(lbuf + b, a.y + row);
+    cp_async_commit();
+  };
+  auto row_of = [&](int r, int s) {
+    const int32_t* idx = a.idx ? a.idx + (long long)r * a.stride : nullptr;
+    return idx ? __ldg(idx + s) : s;
+  };
+  if (a.pipelined) {
+    int s, s1;
+    first_sample(0, s, s1);
+    if (s < s1) fetch_async(row_of(0, s), 0);
+  }
 
   for (int r = 0; r < a.rounds; ++r) {
     const float* w = a.mode == MODE_SGD ? (cur ? a.w1 : a.w0) : a.w_in;
     const int n = a.counts ? __ldg(a.counts + r) : a.n;
-    const int32_t* idx = a.idx ? a.idx + (long long)r * a.stride : nullptr;
     const float scale = a.mode == MODE_SGD ? 1.0f / (float)n : a.grad_scale;
-    const int parity = (int)((round0 + (unsigned long long)r) & 1ull);
 
     unsigned long long* pr =
-        a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 8 : nullptr;
+        a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
     if (pr && threadIdx.x == 0) pr[0] = globaltimer();
-    for (int p = threadIdx.x; p < N::P; p += blockDim.x) wsm[p] = __ldcg(w + p);
+    if ((reinterpret_cast<uintptr_t>(w) & 15u) == 0) {
+      for (int p = threadIdx.x; p < N::P / 4; p += blockDim.x)
+        reinterpret_cast<float4*>(wsm)[p] = __ldcg(reinterpret_cast<const float4*>(w) + p);
+      for (int p = (N::P & ~3) + threadIdx.x; p < N::P; p += blockDim.x) wsm[p] = __ldcg(w + p);
+    } else {
+      for (int p = threadIdx.x; p < N::P; p += blockDim.x) wsm[p] = __ldcg(w + p);
+    }
+    float* wp = wpart + warp * N::PPAD;
+    if (a.mode != MODE_FWD) {
+      for (int p = lane; p < N::PPAD / 4; p += 32)
+        reinterpret_cast<float4*>(wp)[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     __syncthreads();
     if (pr && threadIdx.x == 0) pr[1] = globaltimer();
 
     // ---- per-warp samples of this CTA's contiguous chunk ----
-    float* wp = wpart + warp * N::PPAD;
-    if (a.mode != MODE_FWD) {
-      for (int p = lane; p < N::PPAD; p += 32) wp[p] = 0.0f;
-      __syncwarp();
-    }
     float lsum = 0.0f;
-    const int spc = (n + G - 1) / G;
-    const int s0 = blockIdx.x * spc;
-    const int s1 = min(n, s0 + spc);
-    for (int s = s0 + warp; s < s1; s += NW) {
-      const int row = idx ? __ldg(idx + s) : s;
-      int label = __ldg(a.y + row);
-      if (label < 0 || label >= K) {
-        if (lane == 0) atomicOr(a.err, 1);
-        label = 0;
+    int s, s1;
+    first_sample(r, s, s1);
+    if (a.pipelined) {
+      // ≤ 1 sample per warp per round; its row is already in flight (or landed)
+      // in buffer r&1.  Ask for next round's index now, the row after compute.
+      int sn = 0, sn1 = 0;
+      const bool next = r + 1 < a.rounds;
+      if (next) {
+        first_sample(r + 1, sn, sn1);
+        if (sn < sn1 && a.idx && lane == 0)
+          cp_async4(lbuf + 2, a.idx + (long long)(r + 1) * a.stride + sn);
+        cp_async_commit();
       }
-      const float* xrow = a.x + (long long)row * N::XW;
-      if (a.mode == MODE_FWD) {
-        lsum += lstm_sample<D, H, T, K, false>(
-            wsm, ws, wp, xrow, label, scale, lane,
-            a.probs_out ? a.probs_out + (long long)s * K : nullptr);
-      } else {
-        lsum += lstm_sample<D, H, T, K, true>(wsm, ws, wp, xrow, label, scale, lane, nullptr);
+      if (s < s1) {
+        cp_async_wait<1>();  // this round's row (older group) has landed
+        __syncwarp();
+        int label = lbuf[r & 1];
+        if (label < 0 || label >= K) {
+          if (lane == 0) atomicOr(a.err, 1);
+          label = 0;
+        }
+        unsigned long long* ps = (pr && warp == 0) ? pr : nullptr;
+        const float* xs = xbuf + (r & 1) * N::XWP;
+        if (a.mode == MODE_FWD) {
+          lsum = lstm_sample<D, H, T, K, false>(
+              wsm, ws, wp, xs, label, scale, lane,
+              a.probs_out ? a.probs_out + (long long)s * K : nullptr, ps);
+        } else {
+          lsum = lstm_sample<D, H, T, K, true>(wsm, ws, wp, xs, label, scale, lane, nullptr, ps);
+        }
+      }
+      if (next && sn < sn1) {
+        cp_async_wait<0>();
+        __syncwarp();
+        const int row = a.idx ? lbuf[2] : sn;
+        __syncwarp();
+        fetch_async(row, (r + 1) & 1);
+      }
+    } else {
+      for (; s < s1; s += NW) {
+        const int row = row_of(r, s);
+        float* xs = xbuf;
+        for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(a.x + (long long)row * N::XW + i);
+        int label = __ldg(a.y + row);
+        __syncwarp();
+        if (label < 0 || label >= K) {
+          if (lane == 0) atomicOr(a.err, 1);
+          label = 0;
+        }
+        if (a.mode == MODE_FWD) {
+          lsum += lstm_sample<D, H, T, K, false>(
+              wsm, ws, wp, xs, label, scale, lane,
+              a.probs_out ? a.probs_out + (long long)s * K : nullptr, nullptr);
+        } else {
+          lsum += lstm_sample<D, H, T, K, true>(wsm, ws, wp, xs, label, scale, lane, nullptr,
+                                                nullptr);
+        }
+        __syncwarp();
       }
     }
-    if (lane == 0) lossw[warp] = lsum;
+    if (lane == 0) wp[N::P] = lsum;  // the loss rides in the padded slot P
     __syncthreads();
     if (pr && threadIdx.x == 0) pr[2] = globaltimer();
 
-    // ---- CTA partial (fixed warp order) → global ----
-    float* prow = a.part + (long long)blockIdx.x * a.pstride;
-    if (a.mode != MODE_FWD) {
-      for (int p = threadIdx.x; p < N::P; p += blockDim.x) {
-        float t = 0.0f;
-        for (int w2 = 0; w2 < NW; ++w2) t += wpart[w2 * N::PPAD + p];
-        __stcg(prow + p, t);
+    // ---- CTA partial (fixed warp order) → global, float4 ----
+    float4* prow = reinterpret_cast<float4*>(a.part + (long long)blockIdx.x * a.pstride);
+    for (int p = threadIdx.x; p < N::PPAD / 4; p += blockDim.x) {
+      float4 t = reinterpret_cast<const float4*>(wpart)[p];
+      for (int w2 = 1; w2 < NW; ++w2) {
+        const float4 u = reinterpret_cast<const float4*>(wpart + w2 * N::PPAD)[p];
+        t.x += u.x;
+        t.y += u.y;
+        t.z += u.z;
+        t.w += u.w;
       }
-    }
-    if (threadIdx.x == 0) {
-      float t = 0.0f;
-      for (int w2 = 0; w2 < NW; ++w2) t += lossw[w2];
-      __stcg(prow + N::P, t);
+      __stcg(prow + p, t);
     }
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
-    grid_barrier(a.ms);
+    flag_barrier(a.bar, ++epoch, 0);
     if (pr && threadIdx.x == 0) pr[4] = globaltimer();
-    if (a.mode == MODE_SGD && blockIdx.x == 0 && threadIdx.x == 0) a.ms->flag[parity ^ 1] = 0;
 
     // ---- distributed deterministic reduction of slice [p0,p1) over CTAs ----
     const int slice = (E + G - 1) / G;
@@ -374,36 +622,50 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     for (int base = p0; base < p1; base += cols) {
       const int nc = min(cols, p1 - base);
       const int c = threadIdx.x % cols, gidx = threadIdx.x / cols;
+      const int p = base + c;
+      // master state for this parameter, loaded while the partials fly
+      float wv = 0.f, vv = 0.f;
+      if (a.mode == MODE_SGD && threadIdx.x < nc && base + threadIdx.x < N::P) {
+        wv = __ldcg(wcur + base + threadIdx.x);
+        vv = __ldcg(vcur + base + threadIdx.x);
+      }
       float sum = 0.0f;
-      if (c < nc && gidx < groups)
-        for (int b = gidx; b < G; b += groups) sum += __ldcg(a.part + (long long)b * a.pstride + base + c);
+      if (c < nc && gidx < groups) {
+        for (int b0 = gidx; b0 < G; b0 += 16 * groups) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int b = b0 + i * groups;
+            v[i] = b < G ? __ldcg(a.part + (long long)b * a.pstride + p) : 0.0f;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sum += v[i];
+        }
+      }
       if (gidx < groups) red[gidx * cols + c] = sum;
       __syncthreads();
       if (threadIdx.x < nc) {
         float tot = 0.0f;
         for (int g2 = 0; g2 < groups; ++g2) tot += red[g2 * cols + threadIdx.x];
-        const int p = base + threadIdx.x;
-        if (p == N::P) {
+        const int pp = base + threadIdx.x;
+        if (pp == N::P) {
           if (a.loss_out) a.loss_out[r] = tot;
         } else if (a.mode == MODE_GRAD) {
-          a.g_out[p] = tot;
+          a.g_out[pp] = tot;
         } else if (a.mode == MODE_SGD) {
           if (!is_finite_f(tot)) bad = 1;
           // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v
-          const float vn = fmaf(a.mu, __ldcg(vcur + p), -a.lr * tot);
-          __stcg(vnext + p, vn);
-          __stcg(wnext + p, __ldcg(wcur + p) + vn);
+          const float vn = fmaf(a.mu, vv, -a.lr * tot);
+          __stcg(vnext + pp, vn);
+          __stcg(wnext + pp, wv + vn);
         }
       }
       __syncthreads();
     }
     if (a.mode == MODE_SGD) {
-      bad = __syncthreads_or(bad);
-      if (bad && threadIdx.x == 0) atomicOr(&a.ms->flag[parity], 1);
       if (pr && threadIdx.x == 0) pr[5] = globaltimer();
-      grid_barrier(a.ms);
+      const int rej = flag_barrier(a.bar, ++epoch, bad);
       if (pr && threadIdx.x == 0) pr[6] = globaltimer();
-      const int rej = __ldcg(&a.ms->flag[parity]);
       if (rej) {
         ++rejected;
         last_status = 2;  // GHC_ERR_NONFINITE: keep w/v (optim.cpp:49-51)
@@ -414,12 +676,15 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
       }
     }
   }
-  if (a.mode == MODE_SGD && blockIdx.x == 0 && threadIdx.x == 0) {
-    a.ms->cur = cur;
-    a.ms->version += accepted;
-    a.ms->rejected += rejected;
-    a.ms->round = round0 + (unsigned long long)a.rounds;
-    a.ms->status = last_status;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.bar[0] = epoch;
+    if (a.mode == MODE_SGD) {
+      a.ms->cur = cur;
+      a.ms->version += accepted;
+      a.ms->rejected += rejected;
+      a.ms->round = round0 + (unsigned long long)a.rounds;
+      a.ms->status = last_status;
+    }
   }
 }
 

@@ -10,6 +10,7 @@ and the gap to the next round.
 from __future__ import annotations
 
 import argparse
+import os
 import json
 
 import numpy as np
@@ -22,8 +23,21 @@ def main():
     ap.add_argument("--rounds", type=int, default=200)
     ap.add_argument("--batch", type=int, default=1000)
     ap.add_argument("--arch", default="lstm(5,20,10),softmax(20,3)")
+    ap.add_argument("--barriers", action="store_true", help="grid-barrier micro-benchmark")
     args = ap.parse_args()
     ctx = g.Context(0)
+    if args.barriers:
+        import ctypes as C
+        res = {}
+        for impl, name in enumerate(["atomic_counter", "flag_gather_bcast", "flag_all_poll",
+                                     "cluster8_hw", "all_poll_nofence", "column16",
+                                     "all_poll_acquire"]):
+            for ctas in (128, 144):
+                ns = C.c_double()
+                rc = ctx.lib.ghc_diag_barrier_bench(ctx.h, impl, ctas, 224, 2000, C.byref(ns))
+                res[f"{name}@{ctas}"] = ns.value if rc == 0 else g._lib.load().ghc_last_error().decode()
+        print(json.dumps(res, indent=1))
+        return
     arch = g.Architecture(ctx, args.arch)
     B, R = args.batch, args.rounds
     spec = g.data_spec(20, 5000)
@@ -32,27 +46,48 @@ def main():
     dx, dy, di = ctx.upload(x), ctx.upload(y), ctx.upload(idx)
     m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
     m.sync_rounds(dx, dy, di, B, B, 5)
-    sms = ctx.num_sms
-    warps = min(8, max(1, -(-B // sms)))
-    ctas = -(-B // warps)  # = step_geometry() in ghc_internal.cuh
-    probe = ctx.array(R * ctas * 8, np.uint64)
+    maxc = int(ctx.lib.ghc_plan_max_clusters(arch.h))
+    cs = int(ctx.lib.ghc_plan_cluster_size(arch.h))
+    if maxc > 0:  # = launch_step() in ghc_internal.cuh (cluster variant)
+        spw = int(os.environ.get("GHC_SPW_DIAG", "1"))
+        warps = min(8, max(1, -(-B // (maxc * cs * spw))))
+        ctas = min(maxc, -(-(-(-B // (warps * spw))) // cs)) * cs
+        bounds = [(0, 2, "samples"), (2, 3, "cta_partial"), (3, 4, "cluster_sync1"),
+                  (4, 5, "dsmem_reduce_store"), (5, 6, "column_barrier"),
+                  (6, 7, "global_reduce_sgd_bcast"), (7, 13, "cluster_sync2")]
+        last = 13
+    else:          # = step_geometry()
+        sms = ctx.num_sms
+        warps = min(8, max(1, -(-B // sms)))
+        ctas = -(-B // warps)
+        bounds = [(0, 1, "weights"), (1, 2, "samples"), (2, 3, "store_partial"),
+                  (3, 4, "barrier1"), (4, 5, "reduce_sgd"), (5, 6, "barrier2")]
+        last = 6
+    probe = ctx.array(R * ctas * 16, np.uint64)
     probe.zero()
     ctx.lib.ghc_plan_set_probe(arch.h, probe.ptr)
     ctx.timer_start()
     m.sync_rounds(dx, dy, di, B, B, R)
     ms = ctx.timer_stop()
     ctx.lib.ghc_plan_set_probe(arch.h, None)
-    pr = probe.numpy().reshape(R, ctas, 8).astype(np.int64)
-    used = (pr[0, :, 0] != 0).sum()
+    pr = probe.numpy().reshape(R, ctas, 16).astype(np.int64)
+    used = int((pr[0, :, 0] != 0).sum())
     pr = pr[:, :used, :]
-    names = ["weights", "samples", "store_partial", "barrier1", "reduce_sgd", "barrier2"]
-    out = {"rounds": R, "ctas": int(used), "us_per_round": 1e3 * ms / R, "phases_ns": {}}
-    for i, nm in enumerate(names):
-        d = pr[:, :, i + 1] - pr[:, :, i]
-        out["phases_ns"][nm] = {"median": float(np.median(d)), "max": float(d.max()),
-                                "mean": float(d.mean())}
-    gap = pr[1:, :, 0] - pr[:-1, :, 6]
+    out = {"kernel": arch.kernel_name, "max_clusters": maxc, "cluster_size": cs, "warps": warps,
+           "rounds": R,
+           "ctas": used, "us_per_round": 1e3 * ms / R, "phases_ns": {}}
+    for a0, a1, nm in bounds:
+        d = pr[:, :, a1] - pr[:, :, a0]
+        out["phases_ns"][nm] = {"median": float(np.median(d)), "max": float(d.max())}
+    gap = pr[1:, :, 0] - pr[:-1, :, last]
     out["phases_ns"]["next_round_gap"] = {"median": float(np.median(gap)), "max": float(gap.max())}
+    inner = ["x_wait", "forward", "softmax", "bptt_chain", "weight_grads"]
+    prev = pr[:, :, 0]
+    for i, nm in enumerate(inner):
+        cur = pr[:, :, 8 + i]
+        d = cur - prev
+        out["phases_ns"]["sample0_" + nm] = {"median": float(np.median(d)), "max": float(d.max())}
+        prev = cur
     # critical path: slowest CTA to finish samples vs fastest
     done = pr[:, :, 3]
     out["samples_done_spread_ns"] = float(np.median(done.max(1) - done.min(1)))
