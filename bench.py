@@ -164,12 +164,10 @@ def run_ours(args):
     import paper_1712_05878_b200 as g
     rank, world, local = dist_env()
     if world > 1:
-        raise SystemExit("multi-GPU sync rounds need the NCCL exchange (ghc_comm_*); "
-                         "run with --gpus 1")
+        return run_ours_dist(args, rank, world, local)
     ctx = g.Context(local)
     arch = g.Architecture(ctx, ARCH)
     B = args.batch
-    P = arch.n_params
 
     # dataset: DatasetSpec{96 files × 9500, T=10, D=5, K=3, δ=5, seed 1234}
     # (SURVEY §8(d)); the single worker's shard = all 96 files = 182 MB f32,
@@ -229,46 +227,110 @@ def run_ours(args):
 
     # ---- update path on the wide-variant parameter count (HBM roofline) ----
     upd = update_roofline(args, g, ctx)
+    line = result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clk.summary(),
+                       version, rejected, losses, setup_s, arch.kernel_name,
+                       cpu_baseline(args) if not args.no_cpu else None)
+    print(json.dumps(line), flush=True)
+    return 0
 
+
+def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks, version,
+                rejected, losses, setup_s, kernel, cpu):
     pk, pk_kind = peaks()
+    B = args.batch
     steps_s = ms / 1e3
     value = world * B * args.steps / steps_s
     flops_per_round = B * FLOP_PER_SAMPLE
     achieved_tflops = flops_per_round * args.steps / steps_s / 1e12
     tensor_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) / 2.0  # TF32 ≈ ½ bf16
     fp32_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    line = {
+    return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (SPEC generator, 96 files x 9500 samples, delta=5)",
+        "data": "synthetic (SPEC generator, 96 files x 9500 samples per worker, delta=5)",
         "config": {"workload": "c2 sync Downpour, 1 master + 1 worker per GPU, "
                                "lstm(5,20,10)+softmax(20,3), B=1000/worker",
                    "global_batch": B * world, "seq_len": 10, "parallelism": f"dp{world}",
                    "rounds_per_launch": chunk,
+                   "exchange": "in-kernel (DSMEM + L2)" if world == 1 else
+                               f"NCCL {args.exchange} over NVLink",
                    "l2": "inputs larger than L2: 182 MB shard/GPU > 126 MB L2, fresh "
                          "shuffled batch gathered every round"},
-        "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tensor_peak,
-                     "unit": "TFLOP/s", "frac": achieved_tflops / tensor_peak,
+        "roofline": {"bound": "tensor", "achieved": achieved_tflops / world * world,
+                     "peak": tensor_peak * world, "unit": "TFLOP/s",
+                     "frac": achieved_tflops / (tensor_peak * world),
                      "traffic": args.traffic,
-                     "kernel": "lstm_softmax_step<D5,H20,T10,K3> (fused fwd+bwd+reduce+SGD)",
-                     "peak_kind": f"{pk_kind} bf16 sustained / 2 (TF32)",
-                     "fp32_core": {"peak": fp32_peak,
-                                   "frac": achieved_tflops / fp32_peak,
-                                   "note": "the kernel is FFMA/MUFU/latency-bound by design "
-                                           "(DESIGN.md §Kernels)"},
+                     "kernel": kernel + " (fused fwd+bwd+reduce+SGD)",
+                     "peak_kind": f"{pk_kind} bf16 sustained / 2 (TF32) per GPU",
+                     "fp32_core": {"peak": fp32_peak * world,
+                                   "frac": achieved_tflops / (fp32_peak * world),
+                                   "note": "the kernel is FFMA/MUFU/sync-bound by design "
+                                           "(DESIGN.md §4)"},
                      "one_round_launch_ms": one_round_ms},
-        "cpu_baseline": cpu_baseline(args) if (rank == 0 and not args.no_cpu) else None,
+        "cpu_baseline": cpu,
         "e2e": e2e,
         "update_kernel": upd,
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "training": {"version": version, "rejected": rejected,
                      "loss_first": float(losses[0]), "loss_last": float(losses[-1])},
         "setup_s": setup_s,
     }
+
+
+def run_ours_dist(args, rank, world, local):
+    """N > 1: one worker per GPU; NCCL exchange (ghc_dist_sync_rounds)."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1712_05878_b200 as g
+    from paper_1712_05878_b200 import dist as gd
+    tdist.init_process_group("gloo")
+    ctx = g.Context(local)
+    arch = g.Architecture(ctx, ARCH)
+    B = args.batch
+    uid = gd.rendezvous(tdist, rank, gd.nccl_unique_id)
+    comm = gd.Comm(ctx, uid, rank, world)
+    exchange = gd.ALLREDUCE if args.exchange == "allreduce" else gd.REDUCE_BCAST
+    t0 = time.time()
+    spec = g.data_spec(96 * world, 9500)  # weak scaling: 96 files (182 MB) per worker
+    total_rounds = args.warmup + args.steps
+    per_epoch = 96 * 9500 // B
+    epochs = (total_rounds + per_epoch - 1) // per_epoch
+    plan = gd.plan_worker(spec, world, rank, B, epochs, 99)
+    counts = gd.round_counts(spec, world, B, epochs, 99)[:total_rounds]
+    x, y = g.generate(spec, plan.first_file, plan.n_files)
+    dx, dy = ctx.upload(x), ctx.upload(y)
+    di = ctx.upload(plan.idx_local[: total_rounds * B])
+    setup_s = time.time() - t0
+    m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+    loss = ctx.array(total_rounds)
+    gd.dist_sync_rounds(m, comm, exchange, dx, dy, di, B, counts[: args.warmup], args.warmup, loss)
+    ctx.sync()
+    tdist.barrier()
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        ctx.sync()
+        tdist.barrier()
+        ctx.timer_start()
+        gd.dist_sync_rounds(m, comm, exchange, dx, dy, di, B, counts[args.warmup:], args.steps,
+                            loss, idx_offset=args.warmup * B)
+        ms_local = ctx.timer_stop()
+        ctx.sync()
+        tdist.barrier()
+    t = torch.tensor([ms_local], dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    launches = ctx.launches - launches0
+    _, _, version, rejected = m.read()
+    losses = loss.numpy() / (B * world)
     if rank == 0:
+        line = result_line(args, world, ms, None, 1, None, None, launches, clk.summary(),
+                           version, rejected, losses, setup_s, arch.kernel_name, None)
         print(json.dumps(line), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()
     return 0
 
 
@@ -359,6 +421,7 @@ def main():
     ap.add_argument("--cpu-rounds", type=int, default=120)
     ap.add_argument("--ref-rounds", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", default="reduce_bcast", choices=["reduce_bcast", "allreduce"])
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes/launch from an ncu --set full capture")
     args = ap.parse_args()

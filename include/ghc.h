@@ -254,6 +254,54 @@ ghc_status ghc_data_epoch_indices(const ghc_data_spec* spec, int32_t n_workers,
                                   int32_t worker, int32_t epoch, uint64_t shuffle_seed,
                                   int32_t shuffle, int64_t* h_out, int64_t* count);
 
+/* ------------------------------------------------------------------ */
+/* Roles: a training session of W workers on this     */
+/* device ("virtual workers"), the C++ master/worker loops over the     */
+/* kernels above.  Dataset generated by the data layer and resident.    */
+/* ------------------------------------------------------------------ */
+typedef struct ghc_session ghc_session;
+enum { GHC_ALGO_DOWNPOUR = 0, GHC_ALGO_EASGD = 1 };
+enum { GHC_MODE_SYNC = 0, GHC_MODE_REPLAY = 1 };
+
+/* TrainConfig. */
+typedef struct ghc_train_config {
+  int32_t algo;         /* GHC_ALGO_*                                        */
+  int32_t mode;         /* GHC_MODE_SYNC | GHC_MODE_REPLAY (async, replayed)  */
+  int32_t n_workers;
+  int32_t batch_size;
+  int32_t epochs;
+  int32_t tau;          /* EASGD exchange period                             */
+  float lr;
+  float mu;
+  float alpha;          /* EASGD elastic force                               */
+  int32_t shuffle;
+  uint64_t weight_seed;
+  uint64_t shuffle_seed;
+  int32_t groups;       /* hierarchical sub-masters (0 = flat)               */
+  int32_t flush_k;      /* hierarchical flush period K                       */
+  float parent_lr;      /* top master (pass-through: 1, 0)                   */
+  float parent_mu;
+  int32_t max_updates;  /* sync / hierarchical rounds cap (0 = all epochs)   */
+  int32_t pad_;
+} ghc_train_config;
+
+ghc_status ghc_session_create(ghc_plan* plan, const ghc_train_config* cfg,
+                              const ghc_data_spec* spec, ghc_session** out);
+void ghc_session_destroy(ghc_session* s);
+/* Runs the session.  REPLAY (async Downpour / EASGD): h_order[k] = worker
+ * whose next batch the master processes at step k (EASGD: whose next local
+ * batch runs; it exchanges when its batch_index % tau == 0).  SYNC EASGD
+ * without an order = round-robin.  h_loss (nullable): per-round / per-step
+ * mean loss; h_staleness (nullable): per-step version - basis_version;
+ * at most trace_cap entries of each are written. */
+ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_order,
+                           float* h_loss, int64_t* h_staleness, int64_t trace_cap);
+/* Final master weights (Downpour / top master) or EASGD center, velocity,
+ * every worker's local weights [W][P], sub-master weights [G][P];
+ * stats = {version, rejected, samples absorbed, rounds/steps}. */
+ghc_status ghc_session_read(ghc_session* s, float* h_w, float* h_v, float* h_worker_w,
+                            float* h_group_w, uint64_t* stats);
+
 #ifdef __cplusplus
 }
 #endif

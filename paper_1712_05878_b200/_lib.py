@@ -112,6 +112,10 @@ SIGNATURES = [
     ("ghc_comm_broadcast", C.c_int, [_vp, _vp, _i64, _i32]),
     ("ghc_comm_allreduce_sum", C.c_int, [_vp, _vp, _vp, _i64]),
     ("ghc_dist_sync_rounds", C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _i32, _vp]),
+    ("ghc_session_create", C.c_int, [_vp, _vp, _vp, _vp]),
+    ("ghc_session_destroy", None, [_vp]),
+    ("ghc_session_run", C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64]),
+    ("ghc_session_read", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("ghc_data_generate", C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     ("ghc_data_shard", C.c_int, [_i32, _i32, _i32, _vp, _vp]),
     ("ghc_data_epoch_indices", C.c_int, [_vp, _i32, _i32, _i32, _u64, _i32, _vp, _vp]),
@@ -147,3 +151,14 @@ class DataSpec(C.Structure):
     _fields_ = [("n_files", C.c_int32), ("samples_per_file", C.c_int32),
                 ("seq_len", C.c_int32), ("input_dim", C.c_int32), ("n_classes", C.c_int32),
                 ("pad_", C.c_int32), ("delta", C.c_double), ("seed", C.c_uint64)]
+
+
+class TrainConfig(C.Structure):
+    """ghc_train_config (SPEC.md:547-550 TrainConfig)."""
+    _fields_ = [("algo", C.c_int32), ("mode", C.c_int32), ("n_workers", C.c_int32),
+                ("batch_size", C.c_int32), ("epochs", C.c_int32), ("tau", C.c_int32),
+                ("lr", C.c_float), ("mu", C.c_float), ("alpha", C.c_float),
+                ("shuffle", C.c_int32), ("weight_seed", C.c_uint64),
+                ("shuffle_seed", C.c_uint64), ("groups", C.c_int32), ("flush_k", C.c_int32),
+                ("parent_lr", C.c_float), ("parent_mu", C.c_float),
+                ("max_updates", C.c_int32), ("pad_", C.c_int32)]

@@ -619,3 +619,25 @@ ghc_status ghc_data_epoch_indices(const ghc_data_spec* s, int32_t W, int32_t k, 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- diagnostics
+// GHC_SEGV_TRACE=1: print a native backtrace on SIGSEGV (debug aid for
+// crashes that happen outside any Python frame, e.g. in finalizers).
+#include <execinfo.h>
+#include <csignal>
+#include <unistd.h>
+namespace {
+void ghc_segv_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "libghc: fatal signal, native backtrace:\n";
+  (void)!write(2, msg, sizeof(msg) - 1);
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+__attribute__((constructor)) void ghc_install_segv_trace() {
+  const char* e = std::getenv("GHC_SEGV_TRACE");
+  if (e && e[0] == '1') signal(SIGSEGV, ghc_segv_handler);
+}
+}  // namespace

@@ -1,0 +1,124 @@
+"""Multi-GPU host plumbing for the sync Downpour round (one process per GPU).
+
+The reference runs its ranks as threads over `establish(Topology, backend)`
+(transport.cpp:533-586); here each GPU is a worker process launched by
+torchrun and this module does the host-side parts of the new "nvlink" backend:
+
+* `plan_worker` — the worker's shard (shard_files), the local
+  rows it must generate, and its per-round global→local index stream
+  (batches);
+* `round_counts` — every worker's sample count in every round, computed
+  identically on every rank from the deterministic data layer, so the
+  sample-weighted mean needs no extra exchange (ghc_dist_sync_rounds);
+* `rendezvous` — moves the 128-byte NCCL unique id from rank 0 to every rank
+  through torch.distributed (plumbing only; the exchange itself is NCCL over
+  NVLink inside libghc).
+
+Everything here is pure host logic and is covered by world-size-2 gloo tests on
+CPU (tests/test_dist_cpu.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import gradhub as g
+
+
+@dataclass
+class WorkerPlan:
+    rank: int
+    world: int
+    first_file: int
+    n_files: int
+    row0: int            # global row index of the shard's first sample
+    rows: int            # samples in the shard
+    rounds: int          # rounds this worker participates in
+    idx_local: np.ndarray  # [rounds*B] int32 local row indices (padded)
+    counts: np.ndarray     # [rounds] samples per round for this worker
+
+
+def plan_worker(spec, world: int, rank: int, batch: int, epochs: int, shuffle_seed: int,
+                shuffle: bool = True) -> WorkerPlan:
+    f0, nf = g.shard_files(spec.n_files, world, rank)
+    row0 = f0 * spec.samples_per_file
+    rows = nf * spec.samples_per_file
+    stream, counts = [], []
+    for e in range(epochs):
+        idx = g.epoch_indices(spec, world, rank, e, shuffle_seed, shuffle) - row0
+        for i in range(0, len(idx), batch):
+            b = idx[i:i + batch]
+            pad = np.zeros(batch, np.int64)
+            pad[:len(b)] = b
+            stream.append(pad)
+            counts.append(len(b))
+    idx_local = (np.concatenate(stream) if stream else np.zeros(0)).astype(np.int32)
+    return WorkerPlan(rank, world, f0, nf, row0, rows, len(counts), idx_local,
+                      np.asarray(counts, np.int32))
+
+
+def round_counts(spec, world: int, batch: int, epochs: int, shuffle_seed: int) -> np.ndarray:
+    """[rounds][world] samples of each worker per round (0 once it is DONE);
+    identical on every rank without communication."""
+    per = []
+    for k in range(world):
+        f0, nf = g.shard_files(spec.n_files, world, k)
+        rows = nf * spec.samples_per_file
+        c = []
+        for _ in range(epochs):
+            c.extend(min(batch, rows - i) for i in range(0, rows, batch))
+        per.append(c)
+    R = max(len(c) for c in per)
+    out = np.zeros((R, world), np.int32)
+    for k, c in enumerate(per):
+        out[: len(c), k] = c
+    return out
+
+
+def rendezvous(dist, rank: int, make_id) -> bytes:
+    """Broadcast rank 0's unique id (bytes) to every rank via torch.distributed."""
+    obj = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def nccl_unique_id() -> bytes:
+    from . import _lib
+    buf = (C.c_uint8 * 128)()
+    _lib.check(_lib.load().ghc_comm_unique_id(buf), "ncclGetUniqueId")
+    return bytes(buf)
+
+
+class Comm:
+    """ghc_comm: NCCL communicator over the node's GPUs (NVLink/NVSwitch)."""
+
+    def __init__(self, ctx: g.Context, uid: bytes, rank: int, world: int):
+        self.ctx = ctx
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        g.check(ctx.lib.ghc_comm_init(ctx.h, buf, rank, world, C.byref(h)), "ncclCommInitRank")
+        self.h = h
+
+    def split(self, color: int, key: int) -> "Comm | None":
+        h = C.c_void_p()
+        g.check(self.ctx.lib.ghc_comm_split(self.h, color, key, C.byref(h)), "ncclCommSplit")
+        if not h.value:
+            return None
+        c = Comm.__new__(Comm)
+        c.ctx, c.h = self.ctx, h
+        return c
+
+
+REDUCE_BCAST, ALLREDUCE = 0, 1
+
+
+def dist_sync_rounds(master: g.Master, comm: Comm, exchange: int, x, y, idx, stride: int,
+                     counts: np.ndarray, rounds: int, loss_out=None, idx_offset: int = 0):
+    """ghc_dist_sync_rounds: `rounds` sync Downpour rounds across the comm."""
+    counts = np.ascontiguousarray(counts, np.int32)
+    g.check(master.ctx.lib.ghc_dist_sync_rounds(
+        master.h, comm.h, exchange, x.ptr, y.ptr, idx.offset(idx_offset), stride,
+        C.c_void_p(counts.ctypes.data), rounds,
+        loss_out.ptr if loss_out is not None else None), "dist_sync_rounds")

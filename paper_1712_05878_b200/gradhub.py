@@ -20,8 +20,18 @@ from ._lib import (CacheMismatchError, ConfigError, CudaError, DataSpec, Gradhub
                    NcclError, NonFiniteGradientError, ProtocolError, ShapeError,
                    TransportError, check)
 
-_NP2C = {np.dtype(np.float32): 4, np.dtype(np.int32): 4, np.dtype(np.float64): 8,
-         np.dtype(np.int64): 8, np.dtype(np.uint64): 8}
+_SHUTDOWN = [False]
+
+
+def _at_exit():
+    # the process is going away: the driver reclaims device memory; finalizers
+    # must not touch library objects whose owners may already be gone
+    _SHUTDOWN[0] = True
+
+
+import atexit  # noqa: E402
+
+atexit.register(_at_exit)
 
 
 def _vp(a: np.ndarray):
@@ -39,15 +49,11 @@ class Context:
         self.device = device
 
     def close(self):
+        """Explicit teardown (all plans/arrays/sessions of this context must be
+        released first).  Not called from a finalizer: GC order is arbitrary."""
         if self.h:
             self.lib.ghc_ctx_destroy(self.h)
             self.h = None
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
 
     @property
     def num_sms(self) -> int:
@@ -91,7 +97,7 @@ class DeviceArray:
         self.ptr = p
 
     def free(self):
-        if self.ptr is not None and self.ctx.h:
+        if self.ptr is not None and self.ctx.h and not _SHUTDOWN[0]:
             self.ctx.lib.ghc_free(self.ctx.h, self.ptr)
         self.ptr = None
 
@@ -132,8 +138,9 @@ class Architecture:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and self.ctx.h and not _SHUTDOWN[0]:
                 self.ctx.lib.ghc_plan_destroy(self.h)
+            self.h = None
         except Exception:
             pass
 
@@ -298,8 +305,9 @@ class Master:
 
     def __del__(self):
         try:
-            if self.h:
+            if self.h and self.arch.h and self.ctx.h and not _SHUTDOWN[0]:
                 self.ctx.lib.ghc_master_destroy(self.h)
+            self.h = None
         except Exception:
             pass
 
@@ -373,3 +381,65 @@ def batches(spec: DataSpec, n_workers: int, worker: int, batch_size: int, epochs
         idx = epoch_indices(spec, n_workers, worker, e, shuffle_seed, shuffle)
         out.extend(idx[i:i + batch_size] for i in range(0, len(idx), batch_size))
     return out
+
+
+# ---------------------------------------------------------------- roles
+DOWNPOUR, EASGD = 0, 1
+SYNC, REPLAY = 0, 1
+
+
+def train_config(**kw) -> "_lib.TrainConfig":
+    """TrainConfig with the bench/test defaults."""
+    d = dict(algo=DOWNPOUR, mode=SYNC, n_workers=2, batch_size=100, epochs=1, tau=10, lr=0.01,
+             mu=0.9, alpha=0.5, shuffle=1, weight_seed=7, shuffle_seed=99, groups=0, flush_k=1,
+             parent_lr=1.0, parent_mu=0.0, max_updates=0, pad_=0)
+    d.update(kw)
+    c = _lib.TrainConfig()
+    for k, v in d.items():
+        setattr(c, k, v)
+    return c
+
+
+class Session:
+    """A training session (ghc_session): the SPEC master/worker roles with
+    W workers on this GPU — sync / replayed-async Downpour, EASGD,
+    hierarchical masters."""
+
+    def __init__(self, arch: Architecture, cfg, spec: DataSpec):
+        self.arch, self.cfg, self.spec = arch, cfg, spec
+        self.ctx = arch.ctx
+        h = C.c_void_p()
+        check(self.ctx.lib.ghc_session_create(arch.h, C.byref(cfg), C.byref(spec), C.byref(h)),
+              "session_create")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h and self.arch.h and self.ctx.h and not _SHUTDOWN[0]:
+                self.ctx.lib.ghc_session_destroy(self.h)
+            self.h = None
+        except Exception:
+            pass
+
+    def run(self, order=None, max_trace=1 << 16):
+        n = 0 if order is None else len(order)
+        o = None if order is None else np.ascontiguousarray(order, np.int32)
+        cap = max(n, max_trace)
+        loss = np.full(cap, np.nan, np.float32)
+        stale = np.zeros(cap, np.int64)
+        check(self.ctx.lib.ghc_session_run(self.h, None if o is None else _vp(o), n, _vp(loss),
+                                           _vp(stale), cap), "session_run")
+        return loss, stale[:n]
+
+    def read(self):
+        P = self.arch.n_params
+        W = self.cfg.n_workers
+        G = max(self.cfg.groups, 1)
+        w = np.zeros(P, np.float32); v = np.zeros(P, np.float32)
+        ww = np.zeros((W, P), np.float32); gw = np.zeros((G, P), np.float32)
+        st = np.zeros(4, np.uint64)
+        check(self.ctx.lib.ghc_session_read(self.h, _vp(w), _vp(v), _vp(ww), _vp(gw), _vp(st)),
+              "session_read")
+        return {"w": w, "v": v, "worker_w": ww, "group_w": gw[: self.cfg.groups],
+                "version": int(st[0]), "rejected": int(st[1]), "samples": int(st[2]),
+                "rounds": int(st[3])}

@@ -1,0 +1,136 @@
+"""GPU: the SPEC roles on device vs the CPU oracle runners.
+
+Configs from BASELINE.json: c2-shaped sync Downpour with W workers, c3 EASGD
+(8 workers, α=0.5, τ=10, round-robin "sync" and a replayed async order), c4
+async Downpour (8 workers, replayed arrival order), c5 hierarchical 2×4.
+Tolerance: ‖Δw‖₂/‖w‖₂ ≤ 1e-5 and max|Δw| ≤ 1e-5 after the
+whole run (fp32 device vs f64 reference with the f32 wire); integer
+accounting (versions, samples, staleness) exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import BENCH_ARCH
+
+import paper_1712_05878_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def close(w, wo, tol=1e-5):
+    r, m = rel(w, wo), float(np.max(np.abs(np.asarray(w, np.float64) - wo)))
+    assert r <= tol and m <= tol, (r, m)
+
+
+def oracle_data(oracle, nf, spf):
+    spec = oracle.data_spec(nf, spf)
+    x, y = oracle.generate(spec)
+    return spec, x, y
+
+
+@pytest.mark.parametrize("W,B,epochs", [(1, 100, 1), (4, 50, 1), (8, 64, 2), (3, 70, 1)])
+def test_sync_downpour_virtual_workers(ctx, oracle, W, B, epochs):
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    s = g.Session(arch, g.train_config(n_workers=W, batch_size=B, epochs=epochs),
+                  g.data_spec(8, 300))
+    loss, _ = s.run()
+    out = s.read()
+    spec, x, y = oracle_data(oracle, 8, 300)
+    r = oracle.run_sync(oracle.parse_arch(BENCH_ARCH), spec, x, y,
+                        oracle.train_cfg(n_workers=W, batch_size=B, epochs=epochs))
+    assert out["version"] == r.stats.updates and out["samples"] == r.stats.samples
+    close(out["w"], r.w)
+    assert np.max(np.abs(loss[: len(r.loss)] - r.loss) / r.loss) <= 1e-4
+
+
+def test_async_downpour_replay_c4(ctx, oracle):
+    W = 8
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    cfg = g.train_config(n_workers=W, batch_size=40, epochs=1, mode=g.REPLAY)
+    s = g.Session(arch, cfg, g.data_spec(16, 200))
+    rng = np.random.default_rng(3)
+    # a feasible arrival order: each worker has 5 batches
+    order = np.repeat(np.arange(W, dtype=np.int32), 5)
+    rng.shuffle(order)
+    loss, stale = s.run(order)
+    out = s.read()
+    spec, x, y = oracle_data(oracle, 16, 200)
+    r = oracle.run_replay(oracle.parse_arch(BENCH_ARCH), spec, x, y,
+                          oracle.train_cfg(n_workers=W, batch_size=40, epochs=1), order)
+    assert np.array_equal(stale, r.extra["staleness"])
+    assert out["version"] == r.stats.updates == len(order)
+    close(out["w"], r.w)
+    for k in range(W):  # each worker holds the weights of its last reply
+        close(out["worker_w"][k], r.extra["worker_w"][k])
+
+
+@pytest.mark.parametrize("replay", [False, True])
+def test_easgd_c3(ctx, oracle, replay):
+    W = 8
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    kw = dict(algo=g.EASGD, n_workers=W, batch_size=25, epochs=2, alpha=0.5, tau=10, lr=0.05)
+    s = g.Session(arch, g.train_config(mode=g.REPLAY if replay else g.SYNC, **kw),
+                  g.data_spec(16, 200))
+    n_batches = 2 * (400 // 25)
+    if replay:
+        order = np.repeat(np.arange(W, dtype=np.int32), n_batches)
+        np.random.default_rng(11).shuffle(order)
+    else:
+        order = np.tile(np.arange(W, dtype=np.int32), n_batches)
+    loss, _ = s.run(order if replay else None)
+    out = s.read()
+    spec, x, y = oracle_data(oracle, 16, 200)
+    r = oracle.run_replay(oracle.parse_arch(BENCH_ARCH), spec, x, y,
+                          oracle.train_cfg(algo=oracle.EASGD, n_workers=W, batch_size=25,
+                                           epochs=2, alpha=0.5, tau=10, lr=0.05), order)
+    assert out["version"] == r.stats.updates  # center version = exchanges
+    close(out["w"], r.w)
+    for k in range(W):
+        close(out["worker_w"][k], r.extra["worker_w"][k])
+
+
+def test_hierarchical_c5_shape(ctx, oracle):
+    """2 sub-masters × 4 workers → top master (flush K=2, pass-through parent)."""
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    kw = dict(n_workers=8, batch_size=40, epochs=1, groups=2, flush_k=2)
+    s = g.Session(arch, g.train_config(**kw), g.data_spec(16, 200))
+    s.run()
+    out = s.read()
+    spec, x, y = oracle_data(oracle, 16, 200)
+    r = oracle.run_hier(oracle.parse_arch(BENCH_ARCH), spec, x, y, oracle.train_cfg(**kw))
+    assert out["version"] == r.stats.updates and out["samples"] == r.stats.samples
+    close(out["w"], r.w)
+    for q in range(2):
+        close(out["group_w"][q], r.extra["group_w"][q])
+
+
+def test_hierarchical_pass_through_equals_flat(ctx):
+    """AC11 on device: 1 group × 1 worker, K=1, parent (η=1, μ=0) ≡ flat."""
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    flat = g.Session(arch, g.train_config(n_workers=1, batch_size=50, epochs=1),
+                     g.data_spec(2, 200))
+    flat.run()
+    hier = g.Session(arch, g.train_config(n_workers=1, batch_size=50, epochs=1, groups=1,
+                                          flush_k=1), g.data_spec(2, 200))
+    hier.run()
+    assert np.max(np.abs(flat.read()["w"] - hier.read()["w"])) <= 1e-6
+
+
+def test_session_config_errors(ctx):
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    with pytest.raises(g.ConfigError):
+        g.Session(arch, g.train_config(n_workers=5), g.data_spec(4, 10))  # more workers than files
+    with pytest.raises(g.ConfigError):
+        g.Session(arch, g.train_config(algo=g.EASGD, alpha=1.0), g.data_spec(4, 10))
+    with pytest.raises(g.ShapeError):
+        g.Session(arch, g.train_config(), g.data_spec(4, 10, n_classes=4))
+    s = g.Session(arch, g.train_config(n_workers=2, mode=g.REPLAY), g.data_spec(4, 10))
+    with pytest.raises(g.ConfigError):
+        s.run()  # replay needs an order
+    with pytest.raises(g.ProtocolError):
+        g.Session(arch, g.train_config(n_workers=2, mode=g.REPLAY, batch_size=10),
+                  g.data_spec(4, 10)).run(np.zeros(3, np.int32))  # worker 0 has 2 batches
