@@ -71,6 +71,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # nvidia-smi needs ~0.1-1 s before its first row
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.02)
+            self.rows.clear()  # keep only rows sampled during the timed region
         except Exception:
             self.proc = None
         return self
@@ -412,7 +416,7 @@ def update_roofline(args, g, ctx):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--steps", type=int, default=30000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=1000)

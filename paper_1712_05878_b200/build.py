@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     srcs = [os.path.join(CSRC, f) for f in CU_SOURCES + CXX_SOURCES]
-    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp", *srcs, "-lnccl"]
+    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp", *srcs, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

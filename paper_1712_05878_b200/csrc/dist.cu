@@ -8,17 +8,78 @@
 // 128-byte NCCL unique id between processes (torch.distributed); everything
 // after that is stream-ordered on the context's stream — no host sync inside
 // a round.
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include "ghc_internal.cuh"
 
 using namespace ghc;
 
-#define NC(expr)                                                                          \
-  do {                                                                                    \
-    ncclResult_t r_ = (expr);                                                             \
-    if (r_ != ncclSuccess)                                                                \
-      return ghc_fail(GHC_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+// NCCL is resolved lazily with dlopen (not a load-time dependency): a process
+// may already hold torch's bundled libnccl.so.2 (a newer NCCL whose symbols
+// torch needs), and binding the system copy first would break a later
+// `import torch`.  Preference: GHC_NCCL_LIB, an already-loaded libnccl.so.2,
+// the torch-bundled wheel, then the system library.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommSplit) commSplit = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclCommUserRank) commUserRank = nullptr;
+  decltype(&ncclCommCount) commCount = nullptr;
+  decltype(&ncclReduce) reduce = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = nullptr;
+    if (const char* e = std::getenv("GHC_NCCL_LIB")) h = dlopen(e, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h)  // the torch wheel's copy in this image (site-packages/nvidia/nccl/lib)
+      h = dlopen("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
+                 RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+      return a;
+    }
+#define SYM(field, name) a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name))
+    SYM(getUniqueId, "ncclGetUniqueId");
+    SYM(commInitRank, "ncclCommInitRank");
+    SYM(commSplit, "ncclCommSplit");
+    SYM(commDestroy, "ncclCommDestroy");
+    SYM(commUserRank, "ncclCommUserRank");
+    SYM(commCount, "ncclCommCount");
+    SYM(reduce, "ncclReduce");
+    SYM(broadcast, "ncclBroadcast");
+    SYM(allReduce, "ncclAllReduce");
+    SYM(errorString, "ncclGetErrorString");
+#undef SYM
+    a.ok = a.getUniqueId && a.commInitRank && a.commSplit && a.commDestroy && a.commUserRank &&
+           a.commCount && a.reduce && a.broadcast && a.allReduce && a.errorString;
+    if (!a.ok) a.why = "libnccl.so.2 lacks required symbols";
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+#define NCCL_API()                                                 \
+  const NcclApi& N_ = nccl();                                      \
+  if (!N_.ok) return ghc_fail(GHC_ERR_NCCL, N_.why)
+
+#define NC(expr)                                                                           \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return ghc_fail(GHC_ERR_NCCL, std::string(#expr) + ": " + nccl().errorString(r_));   \
   } while (0)
 
 struct ghc_comm {
@@ -52,13 +113,15 @@ extern "C" {
 
 ghc_status ghc_comm_unique_id(uint8_t* out) {
   ncclUniqueId id;
-  NC(ncclGetUniqueId(&id));
+  NCCL_API();
+  NC(N_.getUniqueId(&id));
   std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
   return GHC_OK;
 }
 
 ghc_status ghc_comm_init(ghc_ctx* ctx, const uint8_t* id_bytes, int32_t rank, int32_t nranks,
                          ghc_comm** out) {
+  NCCL_API();
   if (nranks < 1 || rank < 0 || rank >= nranks) return ghc_fail(GHC_ERR_CONFIG, "comm: bad rank");
   ncclUniqueId id;
   std::memcpy(id.internal, id_bytes, NCCL_UNIQUE_ID_BYTES);
@@ -67,10 +130,10 @@ ghc_status ghc_comm_init(ghc_ctx* ctx, const uint8_t* id_bytes, int32_t rank, in
   c->ctx = ctx;
   c->rank = rank;
   c->size = nranks;
-  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+  ncclResult_t r = nccl().commInitRank(&c->nccl, nranks, id, rank);
   if (r != ncclSuccess) {
     delete c;
-    return ghc_fail(GHC_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    return ghc_fail(GHC_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().errorString(r));
   }
   *out = c;
   return GHC_OK;
@@ -79,18 +142,18 @@ ghc_status ghc_comm_init(ghc_ctx* ctx, const uint8_t* id_bytes, int32_t rank, in
 ghc_status ghc_comm_split(ghc_comm* parent, int32_t color, int32_t key, ghc_comm** out) {
   auto* c = new ghc_comm();
   c->ctx = parent->ctx;
-  ncclResult_t r = ncclCommSplit(parent->nccl, color, key, &c->nccl, nullptr);
+  ncclResult_t r = nccl().commSplit(parent->nccl, color, key, &c->nccl, nullptr);
   if (r != ncclSuccess) {
     delete c;
-    return ghc_fail(GHC_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+    return ghc_fail(GHC_ERR_NCCL, std::string("ncclCommSplit: ") + nccl().errorString(r));
   }
   if (c->nccl == nullptr) {  // color == NCCL_SPLIT_NOCOLOR
     delete c;
     *out = nullptr;
     return GHC_OK;
   }
-  NC(ncclCommUserRank(c->nccl, &c->rank));
-  NC(ncclCommCount(c->nccl, &c->size));
+  NC(nccl().commUserRank(c->nccl, &c->rank));
+  NC(nccl().commCount(c->nccl, &c->size));
   *out = c;
   return GHC_OK;
 }
@@ -99,7 +162,7 @@ void ghc_comm_destroy(ghc_comm* c) {
   if (!c) return;
   cudaSetDevice(c->ctx->device);
   cudaStreamSynchronize(c->ctx->stream);
-  if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->nccl) nccl().commDestroy(c->nccl);
   cudaFree(c->gbuf);
   cudaFree(c->gsum);
   delete c;
@@ -110,19 +173,19 @@ int32_t ghc_comm_size(const ghc_comm* c) { return c->size; }
 
 ghc_status ghc_comm_reduce_sum(ghc_comm* c, const float* d_send, float* d_recv, int64_t count,
                                int32_t root) {
-  NC(ncclReduce(d_send, d_recv, static_cast<size_t>(count), ncclFloat32, ncclSum, root, c->nccl,
+  NC(nccl().reduce(d_send, d_recv, static_cast<size_t>(count), ncclFloat32, ncclSum, root, c->nccl,
                 c->ctx->stream));
   return GHC_OK;
 }
 
 ghc_status ghc_comm_broadcast(ghc_comm* c, float* d_buf, int64_t count, int32_t root) {
-  NC(ncclBroadcast(d_buf, d_buf, static_cast<size_t>(count), ncclFloat32, root, c->nccl,
+  NC(nccl().broadcast(d_buf, d_buf, static_cast<size_t>(count), ncclFloat32, root, c->nccl,
                    c->ctx->stream));
   return GHC_OK;
 }
 
 ghc_status ghc_comm_allreduce_sum(ghc_comm* c, const float* d_send, float* d_recv, int64_t count) {
-  NC(ncclAllReduce(d_send, d_recv, static_cast<size_t>(count), ncclFloat32, ncclSum, c->nccl,
+  NC(nccl().allReduce(d_send, d_recv, static_cast<size_t>(count), ncclFloat32, ncclSum, c->nccl,
                    c->ctx->stream));
   return GHC_OK;
 }
@@ -176,10 +239,10 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
       CU(cudaMemsetAsync(comm->gbuf, 0, sizeof(float) * (P + 1), ctx->stream));
     }
     if (exchange == GHC_EXCHANGE_REDUCE_BCAST) {
-      NC(ncclReduce(comm->gbuf, comm->gsum, static_cast<size_t>(P + 1), ncclFloat32, ncclSum, 0,
+      NC(nccl().reduce(comm->gbuf, comm->gsum, static_cast<size_t>(P + 1), ncclFloat32, ncclSum, 0,
                     comm->nccl, ctx->stream));
     } else {
-      NC(ncclAllReduce(comm->gbuf, comm->gsum, static_cast<size_t>(P + 1), ncclFloat32, ncclSum,
+      NC(nccl().allReduce(comm->gbuf, comm->gsum, static_cast<size_t>(P + 1), ncclFloat32, ncclSum,
                        comm->nccl, ctx->stream));
     }
     if (master_here) {
@@ -203,7 +266,7 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
       }
     }
     if (exchange == GHC_EXCHANGE_REDUCE_BCAST)
-      NC(ncclBroadcast(w, w, static_cast<size_t>(P), ncclFloat32, 0, comm->nccl, ctx->stream));
+      NC(nccl().broadcast(w, w, static_cast<size_t>(P), ncclFloat32, 0, comm->nccl, ctx->stream));
   }
   return GHC_OK;
 }

@@ -1,0 +1,29 @@
+"""GPU: the drop-in C++ adapter — the reference's own API (gradhub::, built from
+/root/reference/proj/src) and the GPU backend with identical signatures
+(gradhub::cuda::, paper_1712_05878_b200/adapter) on the same inputs:
+init_weights bit-identical, forward probs ≤ 2e-6, backward ≤ 2e-5 relative,
+20 serial SGD steps ≤ 1e-5, EASGD ops ≤ 1e-6, and the reference's error
+classes (CacheMismatchError, NonFiniteGradientError, ConfigError)."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BIN = os.path.join(ROOT, "paper_1712_05878_b200", "_build", "adapter_selftest")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(BIN), reason="adapter needs oracle/_ref (reference) at build")
+def test_reference_api_through_gpu_adapter():
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ADAPTER OK" in out.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="adapter needs oracle/_ref (reference) at build")
+def test_adapter_links_ghc():
+    out = subprocess.run(["ldd", BIN], capture_output=True, text=True).stdout
+    assert "libghc.so" in out and "libgradhub_cuda.so" in out
