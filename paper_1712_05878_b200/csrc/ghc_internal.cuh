@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -131,7 +132,14 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
     attr[1].id = cudaLaunchAttributeCooperative;
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    // GHC_NO_COOP=1: plain cluster launch (ncu cannot replay cooperative
+    // cluster launches); the grid never exceeds the co-resident clusters
+    // reported by cudaOccupancyMaxActiveClusters, so the spin barriers hold.
+    static const bool no_coop = [] {
+      const char* e = std::getenv("GHC_NO_COOP");
+      return e && e[0] == '1';
+    }();
+    cfg.numAttrs = no_coop ? 1 : 2;
     CU(cudaLaunchKernelEx(&cfg, p->lstm->fn_round[p->cs_index], a));
     p->ctx->launches++;
     return GHC_OK;
