@@ -134,6 +134,23 @@ ghc_status ghc_forward(ghc_plan* plan, const float* d_w, const float* d_x,
                        float* d_probs, float* d_loss_sum);
 
 /* ------------------------------------------------------------------ */
+/* Dense layers (nn.cpp:129-145, 312-334) on tcgen05 tensor cores       */
+/* ------------------------------------------------------------------ */
+enum { GHC_EPI_STORE = 0, GHC_EPI_BIAS_ACT = 1, GHC_EPI_DACT = 2 };
+/* C[M×N] = A[M×K] · B[N×K]ᵀ (both K-major, row-major fp32 in HBM), 3×TF32
+ * on tcgen05 with fp32 TMEM accumulation; fused epilogue:
+ *   GHC_EPI_STORE    C = alpha·acc
+ *   GHC_EPI_BIAS_ACT C = act(acc + bias[n])                 (act: 0 tanh, 1 relu, 2 identity)
+ *   GHC_EPI_DACT     C = acc · act'(Y[m][n]) (act' from the activation output Y) */
+ghc_status ghc_gemm_nt(ghc_ctx* ctx, const float* d_a, const float* d_b, float* d_c, int32_t m,
+                       int32_t n, int32_t k, int32_t lda, int32_t ldb, int32_t ldc, int32_t epi,
+                       int32_t act, const float* d_bias, const float* d_y, int32_t ldy,
+                       float alpha);
+/* out[c][r] = in[r][c]. */
+ghc_status ghc_transpose(ghc_ctx* ctx, float* d_out, const float* d_in, int32_t rows,
+                         int32_t cols, int32_t ldin, int32_t ldout);
+
+/* ------------------------------------------------------------------ */
 /* Algo (optim.cpp) on device buffers                                  */
 /* ------------------------------------------------------------------ */
 /* sgd_step (optim.cpp:39-65): v = mu*v - lr*g; w += v, in place.  If any

@@ -14,10 +14,10 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libghc.so")
 
-CU_SOURCES = ["ghc.cu", "dist.cu", "session.cu", "diag_barrier.cu"]
+CU_SOURCES = ["ghc.cu", "dist.cu", "session.cu", "dense.cu", "layered.cu", "diag_barrier.cu"]
 CXX_SOURCES = ["host_model.cpp"]
 HEADERS = ["ghc_device.cuh", "lstm_step.cuh", "update_kernels.cuh", "host_model.hpp",
-           "ghc_internal.cuh"]
+           "ghc_internal.cuh", "lstm_round.cuh", "dense_gemm.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,295 @@
+// dense_gemm.cuh — tcgen05 (5th-gen tensor core) GEMM for the dense layers of
+// the wide-layer variant (nn.cpp:129-145 forward, nn.cpp:312-334 backward).
+//
+//   C[M×N] = A[M×K] · B[N×K]ᵀ      (both operands K-major, fp32 in HBM)
+//
+// * 3×TF32: every fp32 operand x is split in smem into hi = tf32(x) and
+//   lo = tf32(x − hi); D += A_hi·B_hi + A_hi·B_lo + A_lo·B_hi with fp32
+//   accumulation in TMEM — fp32-level accuracy (the reference is f64; a plain
+//   TF32 product would be ~1e-3 relative and fail parity).
+// * Tile 128 × BN (BN = 128 or 32) × 32 per stage, 2-stage smem pipeline:
+//   all threads load+split the next K-block while the tensor core runs the
+//   current one; one elected thread issues the 12 tcgen05.mma (4 K-steps × 3)
+//   and commits to the stage's mbarrier.
+// * Operands in the canonical K-major SWIZZLE_NONE layout (core matrix = 8
+//   rows × 16 B; LBO = stride between the two 16-B K-chunks of one MMA,
+//   SBO = stride between 8-row groups — CUTLASS mma_sm100_desc.hpp).
+// * Epilogue: tcgen05.ld 32x32b.x32 → registers → fused bias / activation /
+//   activation-derivative / scale → st.global.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ghc {
+
+enum GemmEpi : int {
+  EPI_STORE = 0,     // C = acc * alpha
+  EPI_BIAS_ACT = 1,  // C = act(acc + bias[n])            (forward, act in {tanh, relu, id})
+  EPI_DACT = 2,      // C = acc * act'(Y[m][n])            (backward dX, act' from the layer output)
+};
+
+struct GemmArgs {
+  const float* A;  // [M][lda]
+  const float* B;  // [N][ldb]
+  float* C;        // [M][ldc]
+  const float* bias;  // EPI_BIAS_ACT
+  const float* Y;     // EPI_DACT: [M][ldy]
+  int M, N, K;
+  int lda, ldb, ldc, ldy;
+  int act;      // 0 tanh, 1 relu, 2 identity (arch.hpp:10)
+  float alpha;
+  int epi;
+};
+
+namespace gemm_detail {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per stage along K (= 8 chunks of 16 B)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// K-major, SWIZZLE_NONE smem descriptor (sm_100 "version 1").
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version
+  // base_offset 0, lbo_mode 0, layout_type SWIZZLE_NONE (0)
+  return d;
+}
+
+// kind::tf32, D f32, A/B TF32, both K-major, M = 128.
+__host__ __device__ constexpr uint32_t make_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+// Bounded wait: a descriptor / commit bug traps (kernel error) instead of
+// hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  for (long long spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase));
+    if (done) return;
+    if (spin > (1ll << 26)) __trap();
+  }
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ float act_f(float z, int act) {
+  if (act == 1) return z > 0.f ? z : 0.f;
+  if (act == 0) return tanhf(z);
+  return z;
+}
+// derivative from the activation OUTPUT y (nn.cpp:26-36 rewritten in y):
+// tanh' = 1 − y², relu' = [y > 0] (≡ [z > 0]), identity' = 1
+__device__ __forceinline__ float dact_from_y(float y, int act) {
+  if (act == 1) return y > 0.f ? 1.f : 0.f;
+  if (act == 0) return 1.f - y * y;
+  return 1.f;
+}
+
+}  // namespace gemm_detail
+
+// Block: 128 threads (4 warps).  Warp w owns TMEM lanes 32w..32w+31 = tile
+// rows; one thread of warp 0 issues the MMAs.
+template <int BN>
+__global__ void __launch_bounds__(128, 1) tcgen05_gemm_nt_kernel(GemmArgs g) {
+  using namespace gemm_detail;
+  static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "N tile");
+  constexpr int A_BYTES = BM * BK * 4;                 // one operand copy per stage
+  constexpr int B_BYTES = BN * BK * 4;
+  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;     // hi + lo of A and B
+  extern __shared__ __align__(1024) uint8_t gsm[];
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tmem_base_s;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+  // NACC accumulators in TMEM, K-blocks rotate over them: the tensor core's
+  // fp32 accumulation truncates, so fewer adds into each (smaller) partial
+  // sum + round-to-nearest FADDs of the partials in the epilogue cut the
+  // K-proportional bias (measured: DESIGN.md §4, dense layers).
+  constexpr int NACC = 4;
+  constexpr int TCOLS = NACC * BN < 32 ? 32 : NACC * BN;
+  static_assert(TCOLS <= 512, "TMEM columns");
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  // Canonical K-major layout inside one operand copy:
+  //   [chunk c = 0..7 (16 B of K)][row group = rows/8][row % 8][16 B]
+  //   LBO = rows*16 (next chunk), SBO = 128 (next 8-row group)
+  auto store_tile = [&](uint8_t* base_hi, uint8_t* base_lo, const float* src, int ld, int rows,
+                        int row0, int row_lim, int k0) {
+    // lane = chunk_local*8 + r8 ; a warp covers 8 rows × 4 chunks per pass
+    for (int it = warp; it < (rows / 8) * 2; it += 4) {
+      const int rg = it >> 1;               // 8-row group
+      const int ch = (it & 1) * 4 + (lane >> 3);
+      const int r = rg * 8 + (lane & 7);
+      const int grow = row0 + r;
+      const int gk = k0 + ch * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (grow < row_lim) {
+        const float* p = src + (long long)grow * ld + gk;
+        if (gk + 3 < g.K && (((uintptr_t)p) & 15u) == 0) {
+          v = __ldg(reinterpret_cast<const float4*>(p));
+        } else {
+          if (gk < g.K) v.x = __ldg(p);
+          if (gk + 1 < g.K) v.y = __ldg(p + 1);
+          if (gk + 2 < g.K) v.z = __ldg(p + 2);
+          if (gk + 3 < g.K) v.w = __ldg(p + 3);
+        }
+      }
+      float4 h, l;
+      h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
+      h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
+      h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
+      h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
+      const int off = ch * rows * 16 + rg * 128 + (lane & 7) * 16;
+      *reinterpret_cast<float4*>(base_hi + off) = h;
+      *reinterpret_cast<float4*>(base_lo + off) = l;
+    }
+  };
+
+  const int nkb = (g.K + BK - 1) / BK;
+  const uint32_t idesc = make_idesc(BN);
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int s = kb & 1;
+    uint8_t* st = gsm + s * STAGE;
+    if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);  // MMAs that read this stage are done
+    store_tile(st, st + A_BYTES, g.A, g.lda, BM, m0, g.M, kb * BK);
+    store_tile(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES, g.B, g.ldb, BN, n0, g.N, kb * BK);
+    asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy stores → tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a_hi = smem_u32(st), a_lo = a_hi + A_BYTES;
+      const uint32_t b_hi = smem_u32(st + 2 * A_BYTES), b_lo = b_hi + B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < BK / 8; ++ks) {  // K = 8 tf32 = 2 chunks per MMA
+        const uint32_t ao = ks * 2 * BM * 16, bo = ks * 2 * BN * 16;
+        const uint64_t dah = make_desc(a_hi + ao, BM * 16, 128);
+        const uint64_t dal = make_desc(a_lo + ao, BM * 16, 128);
+        const uint64_t dbh = make_desc(b_hi + bo, BN * 16, 128);
+        const uint64_t dbl = make_desc(b_lo + bo, BN * 16, 128);
+        const uint32_t acc0 = (kb >= NACC || ks > 0) ? 1u : 0u;  // first use zero-inits
+        const uint32_t d = tmem + static_cast<uint32_t>((kb % NACC) * BN);
+        umma_tf32(d, dah, dbh, idesc, acc0);  // hi·hi
+        umma_tf32(d, dah, dbl, idesc, 1u);    // hi·lo
+        umma_tf32(d, dal, dbh, idesc, 1u);    // lo·hi
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&mbar[s])));
+    }
+  }
+  // last K-block's MMAs complete ⇒ all complete (issue order)
+  const int last = nkb - 1;
+  mbar_wait(&mbar[last & 1], (last >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // ---- epilogue: TMEM → registers → fused op → HBM ----
+  const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    for (int a = 0; a < NACC && a < nkb; ++a) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + a * BN + c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+          "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+            "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(v[i]);
+    }
+    if (row < g.M) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int col = n0 + c0 + i;
+        if (col >= g.N) continue;
+        float o = acc[i];
+        if (g.epi == EPI_BIAS_ACT) {
+          o = act_f(o + g.bias[col], g.act);
+        } else if (g.epi == EPI_DACT) {
+          o *= dact_from_y(g.Y[(long long)row * g.ldy + col], g.act);
+        } else {
+          o *= g.alpha;
+        }
+        g.C[(long long)row * g.ldc + col] = o;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(TCOLS));
+}
+
+// Out-of-place transpose: out[c][r] = in[r][c] (32×32 smem tiles).
+static __global__ void transpose_kernel(float* __restrict__ out, const float* __restrict__ in, int rows,
+                                 int cols, int ldin, int ldout) {
+  __shared__ float t[32][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = blockIdx.y * 32 + i;
+    t[i][threadIdx.x] = (r < rows && c < cols) ? in[(long long)r * ldin + c] : 0.f;
+  }
+  __syncthreads();
+  const int r2 = blockIdx.y * 32 + threadIdx.x;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c2 = blockIdx.x * 32 + i;
+    if (c2 < cols && r2 < rows) out[(long long)c2 * ldout + r2] = t[threadIdx.x][i];
+  }
+}
+
+}  // namespace ghc

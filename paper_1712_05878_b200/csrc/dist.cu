@@ -222,19 +222,11 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
     if (total == 0) break;  // every worker has sent DONE
     const int32_t mine = cnt[comm->rank];
     if (mine > 0) {
-      StepArgs a{};
-      a.x = d_x;
-      a.y = d_y;
-      a.idx = d_idx ? d_idx + static_cast<int64_t>(r) * stride : nullptr;
-      a.n = mine;
-      a.rounds = 1;
-      a.grad_scale = static_cast<float>(1.0 / static_cast<double>(total));
-      a.w_in = w;
-      a.ms = p->ms;
-      a.g_out = comm->gbuf;
-      a.loss_out = comm->gbuf + P;
-      a.mode = MODE_GRAD;
-      if (ghc_status s = launch_step(p, a, mine)) return s;
+      if (ghc_status s = ghc_worker_grad(p, w, d_x, d_y,
+                                         d_idx ? d_idx + static_cast<int64_t>(r) * stride : nullptr,
+                                         mine, static_cast<float>(1.0 / static_cast<double>(total)),
+                                         comm->gbuf, comm->gbuf + P))
+        return s;
     } else {
       CU(cudaMemsetAsync(comm->gbuf, 0, sizeof(float) * (P + 1), ctx->stream));
     }

@@ -45,6 +45,15 @@ const std::vector<LstmEntry>& lstm_table() {
   return t;
 }
 
+const std::vector<LstmEntry>& trunk_table() {
+  static const std::vector<LstmEntry> t = {
+      make_entry<5, 20, 10, 1>("lstm_trunk<D5,H20,T10>"),  // wide variant
+      make_entry<5, 8, 10, 1>("lstm_trunk<D5,H8,T10>"),
+      make_entry<3, 4, 5, 1>("lstm_trunk<D3,H4,T5>"),
+  };
+  return t;
+}
+
 
 namespace {}  // namespace
 
@@ -173,12 +182,50 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
   if (L.size() == 2 && L[0].kind == LayerKind::lstm && L[1].kind == LayerKind::softmax) {
     for (const LstmEntry& e : lstm_table())
       if (e.D == L[0].a && e.H == L[0].b && e.T == L[0].c && e.K == L[1].b) p->lstm = &e;
+    if (!p->lstm) {
+      const std::string txt = arch_text;
+      delete p;
+      return fail(GHC_ERR_CONFIG, "no sm_100a kernel instantiated for architecture '" + txt +
+                                      "' (see DESIGN.md §Kernels for the supported shapes)");
+    }
+  } else {
+    // dense layers: LSTM trunk kernel (if any) + tcgen05 GEMMs (layered.cu)
+    p->layered = true;
+    if (L[0].kind == LayerKind::lstm) {
+      for (const LstmEntry& e : trunk_table())
+        if (e.D == L[0].a && e.H == L[0].b && e.T == L[0].c) p->trunk = &e;
+      if (!p->trunk) {
+        const std::string txt = arch_text;
+        delete p;
+        return fail(GHC_ERR_CONFIG, "no LSTM trunk kernel instantiated for '" + txt + "'");
+      }
+    }
   }
-  if (!p->lstm) {
-    const std::string txt = arch_text;
-    delete p;
-    return fail(GHC_ERR_CONFIG, "no sm_100a kernel instantiated for architecture '" + txt +
-                                    "' (see DESIGN.md §Kernels for the supported shapes)");
+  if (p->layered) {
+    p->kname = p->trunk ? std::string(p->trunk->name) + " + tcgen05 3xTF32 dense GEMMs"
+                        : std::string("tcgen05 3xTF32 dense GEMMs");
+    CU(cudaSetDevice(c->device));
+    p->max_ctas = c->num_sms;
+    if (p->trunk) {
+      CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(p->trunk->fn),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(p->trunk->smem(8))));
+      int per_sm = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, reinterpret_cast<const void*>(p->trunk->fn), 256, p->trunk->smem(8)));
+      p->max_ctas = (per_sm < 1 ? 1 : per_sm) * c->num_sms;
+      CU(cudaMalloc(&p->part, sizeof(float) * static_cast<size_t>(p->max_ctas) * p->trunk->ppad));
+    }
+    CU(cudaMalloc(&p->ms, sizeof(MasterDev)));
+    CU(cudaMemset(p->ms, 0, sizeof(MasterDev)));
+    CU(cudaMalloc(&p->err, sizeof(int)));
+    CU(cudaMemset(p->err, 0, sizeof(int)));
+    const size_t bar_bytes = sizeof(unsigned) * 32 * (2 + static_cast<size_t>(p->max_ctas));
+    CU(cudaMalloc(&p->bar, bar_bytes));
+    CU(cudaMemset(p->bar, 0, bar_bytes));
+    p->use_cluster = false;
+    *out = p;
+    return GHC_OK;
   }
   p->kname = std::string(p->lstm->name) + " [flat]";
   CU(cudaSetDevice(c->device));
@@ -270,6 +317,7 @@ void ghc_plan_destroy(ghc_plan* p) {
   cudaFree(p->ms);
   cudaFree(p->err);
   cudaFree(p->bar);
+  layered_free(p->ws);
   delete p;
 }
 
@@ -277,7 +325,7 @@ int64_t ghc_plan_n_params(const ghc_plan* p) { return p->model.n_params; }
 int64_t ghc_plan_input_width(const ghc_plan* p) { return p->model.input_width; }
 int32_t ghc_plan_n_classes(const ghc_plan* p) { return p->model.n_classes; }
 const char* ghc_plan_kernel_name(const ghc_plan* p) {
-  return p->use_cluster && p->max_clusters > 0 ? p->lstm->name : p->kname.c_str();
+  return p->lstm && p->use_cluster && p->max_clusters > 0 ? p->lstm->name : p->kname.c_str();
 }
 int32_t ghc_plan_max_clusters(const ghc_plan* p) { return p->use_cluster ? p->max_clusters : 0; }
 int32_t ghc_plan_cluster_size(const ghc_plan* p) { return p->use_cluster ? p->cluster_size : 0; }
@@ -326,6 +374,7 @@ ghc_status ghc_worker_grad(ghc_plan* p, const float* d_w, const float* d_x, cons
                            float* d_loss_sum) {
   if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");  // nn.cpp:104
   if (!d_w || !d_x || !d_y || !d_grad) return fail(GHC_ERR_CONFIG, "null device pointer");
+  if (p->layered) return layered_step(p, d_w, d_x, d_y, d_idx, n, grad_scale, d_grad, d_loss_sum, nullptr);
   StepArgs a{};
   a.x = d_x;
   a.y = d_y;
@@ -344,6 +393,7 @@ ghc_status ghc_worker_grad(ghc_plan* p, const float* d_w, const float* d_x, cons
 ghc_status ghc_forward(ghc_plan* p, const float* d_w, const float* d_x, const int32_t* d_y,
                        const int32_t* d_idx, int64_t n, float* d_probs, float* d_loss_sum) {
   if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");
+  if (p->layered) return layered_step(p, d_w, d_x, d_y, d_idx, n, 1.0f, nullptr, d_loss_sum, d_probs);
   StepArgs a{};
   a.x = d_x;
   a.y = d_y;
@@ -502,6 +552,7 @@ void ghc_master_destroy(ghc_master* m) {
   }
   cudaFree(m->ms);
   cudaFree(m->ms_apply);
+  cudaFree(m->g_scratch);
   delete m;
 }
 
@@ -540,6 +591,44 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
                                   int64_t n, int32_t n_rounds, float* d_loss_out) {
   if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");
   if (n_rounds < 1) return GHC_OK;
+  if (m->plan->layered) {
+    // layered archs: per round the layered worker step (scale 1/n_r) then the
+    // rejecting in-place sgd_step on the master's current buffers
+    ghc_ctx* c = m->plan->ctx;
+    std::vector<int32_t> cnt(static_cast<size_t>(n_rounds), static_cast<int32_t>(n));
+    if (d_counts) {
+      CU(cudaMemcpyAsync(cnt.data(), d_counts, sizeof(int32_t) * n_rounds, cudaMemcpyDeviceToHost,
+                         c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+    }
+    if (!m->g_scratch) CU(cudaMalloc(&m->g_scratch, sizeof(float) * static_cast<size_t>((m->P + 4) & ~3LL)));
+    int cur = 0;
+    if (ghc_status s = master_cur(m, cur)) return s;
+    for (int r = 0; r < n_rounds; ++r) {
+      const int32_t nr = cnt[static_cast<size_t>(r)];
+      if (ghc_status s = layered_step(m->plan, m->w[cur], d_x, d_y,
+                                      d_idx ? d_idx + static_cast<int64_t>(r) * stride : nullptr, nr,
+                                      1.0f / static_cast<float>(nr), m->g_scratch,
+                                      d_loss_out ? d_loss_out + r : nullptr, nullptr))
+        return s;
+      float* w = m->w[cur];
+      float* v = m->v[cur];
+      const float* g = m->g_scratch;
+      MasterDev* ms = m->ms_apply;
+      int vec = 1;
+      long long PP = m->P;
+      float lr = m->lr, mu = m->mu;
+      int* st = &m->ms->status;
+      unsigned long long* ver = &m->ms->version;
+      unsigned long long* rj = &m->ms->rejected;
+      void* args[] = {&w, &v, &g, &PP, &vec, &lr, &mu, &ms, &st, &ver, &rj};
+      const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
+      CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid),
+                                     dim3(256), args, 0, c->stream));
+      c->launches++;
+    }
+    return GHC_OK;
+  }
   StepArgs a{};
   a.x = d_x;
   a.y = d_y;

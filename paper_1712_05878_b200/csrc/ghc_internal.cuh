@@ -48,6 +48,8 @@ struct LstmEntry {
 
 // The instantiated fused-kernel shapes (defined in ghc.cu only).
 const std::vector<LstmEntry>& lstm_table();
+// LSTM trunk shapes for layered archs (K unused; defined in ghc.cu).
+const std::vector<LstmEntry>& trunk_table();
 
 struct ghc_ctx {
   int device = 0;
@@ -57,8 +59,13 @@ struct ghc_ctx {
   std::atomic<uint64_t> launches{0};
 };
 
+struct LayeredWorkspace;
+
 struct ghc_plan {
   ghc_ctx* ctx = nullptr;
+  bool layered = false;                 // dense layers: layered.cu path
+  const LstmEntry* trunk = nullptr;     // LSTM trunk kernel of a layered arch
+  LayeredWorkspace* ws = nullptr;
   int max_warps = 8;      // warps/CTA that fit the fused kernel's smem
   unsigned long long* probe = nullptr;  // phase-timing probe (diagnostics)
   unsigned* bar = nullptr;  // flag barrier: (2 + max_ctas) 128-B lines
@@ -78,6 +85,7 @@ struct ghc_plan {
 
 struct ghc_master {
   ghc_plan* plan = nullptr;
+  float* g_scratch = nullptr;  // layered archs: the round's combined gradient
   float* w[2] = {nullptr, nullptr};
   float* v[2] = {nullptr, nullptr};
   MasterDev* ms = nullptr;
@@ -168,3 +176,30 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 }  // namespace
 
+
+// layered.cu — worker step for archs with dense layers; g_out == nullptr ⇒
+// forward only (probs nullable, loss_out nullable).
+ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32_t* y,
+                        const int32_t* idx, int64_t n, float scale, float* g_out,
+                        float* loss_out, float* probs);
+void layered_free(LayeredWorkspace* ws);
+
+// LSTM trunk (flat kernel of p->trunk, modes MODE_TRUNK_*), cooperative.
+inline ghc_status launch_trunk(ghc_plan* p, StepArgs& a, int64_t n) {
+  const LstmEntry* e = p->trunk;
+  const int sms = p->ctx->num_sms;
+  int warps = static_cast<int>((n + sms - 1) / sms);
+  warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
+  int64_t ctas = (n + warps - 1) / warps;
+  if (ctas > p->max_ctas) ctas = p->max_ctas;
+  a.part = p->part;
+  a.pstride = e->ppad;
+  a.err = p->err;
+  a.bar = p->bar;
+  a.pipelined = 0;
+  void* args[] = {&a};
+  CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(e->fn), dim3(static_cast<unsigned>(ctas)),
+                                 dim3(warps * 32), args, e->smem(warps), p->ctx->stream));
+  p->ctx->launches++;
+  return GHC_OK;
+}

@@ -182,10 +182,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
           prb[sp] = (valid && a.probs_out) ? a.probs_out + (long long)(s + sp * NW) * K : nullptr;
         }
         unsigned long long* ps = (pr && warp == 0) ? pr : nullptr;
+        float* tio[SPW];
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp) tio[sp] = nullptr;
         if (a.mode == MODE_FWD)
-          lstm_samples<D, H, T, K, false, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps);
+          lstm_samples<D, H, T, K, false, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps, tio);
         else
-          lstm_samples<D, H, T, K, true, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps);
+          lstm_samples<D, H, T, K, true, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps, tio);
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
           if (s + sp * NW < s1) lsum += lo[sp];

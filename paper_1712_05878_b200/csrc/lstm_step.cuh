@@ -24,7 +24,13 @@
 
 namespace ghc {
 
-enum StepMode : int { MODE_GRAD = 0, MODE_SGD = 1, MODE_FWD = 2 };
+enum StepMode : int {
+  MODE_GRAD = 0,       // fused lstm→softmax: gradient + loss
+  MODE_SGD = 1,        // fused sync rounds with sgd_step
+  MODE_FWD = 2,        // fused forward: probs + loss
+  MODE_TRUNK_FWD = 3,  // LSTM trunk of a deeper net: write h_T rows (hio[s][H])
+  MODE_TRUNK_GRAD = 4  // LSTM trunk backward from dh_T rows (hio[s][H]): Wx, Wh, b grads
+};
 
 struct StepArgs {
   const float* x;         // dataset (or batch) rows, T*D floats each
@@ -50,6 +56,7 @@ struct StepArgs {
   float* probs_out;       // MODE_FWD: n×K (nullable)
   int* err;               // bit 0: label out of range (nn.cpp:241-244)
   unsigned long long* probe;  // nullable: [rounds][gridDim][16] %globaltimer per phase
+  float* hio;             // TRUNK modes: h_T out / dh_T in, [n][H]
   unsigned* bar;          // flag barrier: epoch, go, then one 128-B line per CTA
   int pipelined;          // every round has ≤ 1 sample per warp (cp.async prefetch path)
   int mode;
@@ -141,13 +148,17 @@ struct LstmNet {
 // gradient (scaled by scale[sp]; 0 masks an empty slot) is ADDED into the
 // warp partial `wp` — lane j touches only the entries of its own gate rows,
 // lane 0 the output bias — no atomics.  loss[sp] receives ℓ of slot sp.
-template <int D, int H, int T, int K, bool BWD, int SPW>
+// HEAD = false: the LSTM is the trunk of a deeper net (arch.cpp: lstm first,
+// dense layers after); the forward writes h_T to trunk_io[sp] and the
+// backward starts from dh_T read from trunk_io[sp] (already scaled).
+template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true>
 __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, float* __restrict__ ws,
                                              float* __restrict__ wp,
                                              const float* const (&xs)[SPW],
                                              const int (&label)[SPW], const float (&scale)[SPW],
                                              int lane, float* const (&probs_row)[SPW],
-                                             float (&loss)[SPW], unsigned long long* pr) {
+                                             float (&loss)[SPW], unsigned long long* pr,
+                                             float* const (&trunk_io)[SPW]) {
   using N = LstmNet<D, H, T, K>;
   constexpr int DP = N::DP;
   const bool act = lane < H;
@@ -257,6 +268,20 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   }
   if (pr && lane == 0) pr[9] = globaltimer();
 
+  float dh[SPW];
+  if constexpr (!HEAD) {
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) {
+      loss[sp] = 0.0f;
+      if (!BWD) {
+        if (act && trunk_io[sp]) trunk_io[sp][j] = hs[sp][(T - 1) * H + j];
+        dh[sp] = 0.0f;
+      } else {
+        dh[sp] = act ? trunk_io[sp][j] * (scale[sp] != 0.0f ? 1.0f : 0.0f) : 0.0f;
+      }
+    }
+    if constexpr (!BWD) return;
+  } else {
   // ---------------- softmax + loss (nn.cpp:202-248) ----------------
   float hT[SPW], e[SPW][K], inv_den[SPW];
 #pragma unroll
@@ -287,7 +312,6 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   if constexpr (!BWD) return;
 
   // ---------------- backward: softmax (nn.cpp:276-311) ----------------
-  float dh[SPW];
 #pragma unroll
   for (int sp = 0; sp < SPW; ++sp) dh[sp] = 0.0f;
 #pragma unroll
@@ -303,6 +327,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     if (act) wp[N::OFF_WS + k * H + j] += gws;
     if (lane == 0) wp[N::OFF_BS + k] += gbs;
   }
+  }  // HEAD
   if (pr && lane == 0) pr[10] = globaltimer();
 
   // ------- backward pass 1: the BPTT chain (nn.cpp:351-392), dz → smem -------
@@ -436,18 +461,19 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
 }
 
 // Single-sample convenience wrapper (flat kernel, non-pipelined paths).
-template <int D, int H, int T, int K, bool BWD>
+template <int D, int H, int T, int K, bool BWD, bool HEAD = true>
 __device__ __forceinline__ float lstm_sample(const float* __restrict__ wsm, float* __restrict__ ws,
                                              float* __restrict__ wp,
                                              const float* __restrict__ xs, int label,
                                              float scale, int lane, float* probs_row,
-                                             unsigned long long* pr) {
+                                             unsigned long long* pr, float* trunk = nullptr) {
   const float* xa[1] = {xs};
   const int la[1] = {label};
   const float sa[1] = {scale};
   float* pa[1] = {probs_row};
+  float* ta[1] = {trunk};
   float lo[1];
-  lstm_samples<D, H, T, K, BWD, 1>(wsm, ws, wp, xa, la, sa, lane, pa, lo, pr);
+  lstm_samples<D, H, T, K, BWD, 1, HEAD>(wsm, ws, wp, xa, la, sa, lane, pa, lo, pr, ta);
   return lo[0];
 }
 
@@ -553,6 +579,12 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
           lsum = lstm_sample<D, H, T, K, false>(
               wsm, ws, wp, xs, label, scale, lane,
               a.probs_out ? a.probs_out + (long long)s * K : nullptr, ps);
+        } else if (a.mode == MODE_TRUNK_FWD) {
+          lstm_sample<D, H, T, K, false, false>(wsm, ws, wp, xs, label, scale, lane, nullptr, ps,
+                                                a.hio + (long long)s * H);
+        } else if (a.mode == MODE_TRUNK_GRAD) {
+          lstm_sample<D, H, T, K, true, false>(wsm, ws, wp, xs, label, scale, lane, nullptr, ps,
+                                               a.hio + (long long)s * H);
         } else {
           lsum = lstm_sample<D, H, T, K, true>(wsm, ws, wp, xs, label, scale, lane, nullptr, ps);
         }
@@ -579,6 +611,12 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
           lsum += lstm_sample<D, H, T, K, false>(
               wsm, ws, wp, xs, label, scale, lane,
               a.probs_out ? a.probs_out + (long long)s * K : nullptr, nullptr);
+        } else if (a.mode == MODE_TRUNK_FWD) {
+          lstm_sample<D, H, T, K, false, false>(wsm, ws, wp, xs, label, scale, lane, nullptr,
+                                                nullptr, a.hio + (long long)s * H);
+        } else if (a.mode == MODE_TRUNK_GRAD) {
+          lstm_sample<D, H, T, K, true, false>(wsm, ws, wp, xs, label, scale, lane, nullptr,
+                                               nullptr, a.hio + (long long)s * H);
         } else {
           lsum += lstm_sample<D, H, T, K, true>(wsm, ws, wp, xs, label, scale, lane, nullptr,
                                                 nullptr);
@@ -609,8 +647,9 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
 
     // ---- distributed deterministic reduction of slice [p0,p1) over CTAs ----
     const int slice = (E + G - 1) / G;
-    const int p0 = a.mode == MODE_FWD ? (blockIdx.x == 0 ? N::P : E) : blockIdx.x * slice;
-    const int p1 = a.mode == MODE_FWD ? E : min(E, p0 + slice);
+    const bool fwd_only = a.mode == MODE_FWD || a.mode == MODE_TRUNK_FWD;
+    const int p0 = fwd_only ? (blockIdx.x == 0 ? N::P : E) : blockIdx.x * slice;
+    const int p1 = fwd_only ? E : min(E, p0 + slice);
     const float* wcur = w;
     float* wnext = cur ? a.w0 : a.w1;
     const float* vcur = cur ? a.v1 : a.v0;
@@ -652,6 +691,8 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
           if (a.loss_out) a.loss_out[r] = tot;
         } else if (a.mode == MODE_GRAD) {
           a.g_out[pp] = tot;
+        } else if (a.mode == MODE_TRUNK_GRAD) {
+          if (pp < N::OFF_WS) a.g_out[pp] = tot;  // trunk: Wx, Wh, b only
         } else if (a.mode == MODE_SGD) {
           if (!is_finite_f(tot)) bad = 1;
           // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v

@@ -157,20 +157,10 @@ ghc_status worker_step(ghc_session* s, int k, const float* w, int32_t& n_out) {
     return GHC_OK;
   }
   const Batch b = bl[cur++];
-  StepArgs a{};
-  a.x = s->X;
-  a.y = s->Y;
-  a.idx = s->streams + s->stream_off[static_cast<size_t>(k)] + b.off;
-  a.n = b.n;
-  a.rounds = 1;
-  a.grad_scale = 1.0f / static_cast<float>(b.n);
-  a.w_in = w;
-  a.ms = s->plan->ms;
-  a.g_out = s->scratch_g;
-  a.loss_out = s->scratch_g + s->P;
-  a.mode = MODE_GRAD;
   n_out = b.n;
-  return launch_step(s->plan, a, b.n);
+  return ghc_worker_grad(s->plan, w, s->X, s->Y,
+                         s->streams + s->stream_off[static_cast<size_t>(k)] + b.off, b.n,
+                         1.0f / static_cast<float>(b.n), s->scratch_g, s->scratch_g + s->P);
 }
 
 ghc_status apply_master(ghc_session* s, ghc_master* m, const float* g, float lr, float mu) {
