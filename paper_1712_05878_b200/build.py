@@ -16,8 +16,8 @@ LIB = os.path.join(OUT_DIR, "libghc.so")
 
 CU_SOURCES = ["ghc.cu", "dist.cu", "session.cu", "dense.cu", "layered.cu", "diag_barrier.cu"]
 CXX_SOURCES = ["host_model.cpp"]
-HEADERS = ["ghc_device.cuh", "lstm_step.cuh", "update_kernels.cuh", "host_model.hpp",
-           "ghc_internal.cuh", "lstm_round.cuh", "dense_gemm.cuh"]
+# every header in csrc/ is a dependency of every translation unit
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

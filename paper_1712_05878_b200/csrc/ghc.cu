@@ -12,22 +12,33 @@
 namespace {
 thread_local std::string g_err;
 
-template <int D, int H, int T, int K>
+template <int D, int H, int T, int K, int CS, bool TC>
+constexpr void (*tc_fn())(StepArgs) {
+  if constexpr (TC) return &lstm_round_tc_kernel<D, H, T, K, CS>;
+  else return nullptr;
+}
+
+template <int D, int H, int T, int K, bool TC = true>
 LstmEntry make_entry(const char* name) {
   using N = LstmNet<D, H, T, K>;
   using R4 = RoundLayout<D, H, T, K, 4>;
   using R8 = RoundLayout<D, H, T, K, 8>;
+  using C4 = TcLayout<D, H, T, K, 4>;
+  using C8 = TcLayout<D, H, T, K, 8>;
+  static_assert(C4::EP == R4::EP && C8::EP == R8::EP, "same partial-row layout");
   return LstmEntry{D,
                    H,
                    T,
                    K,
                    &lstm_softmax_step_kernel<D, H, T, K>,
                    {&lstm_round_kernel<D, H, T, K, 4>, &lstm_round_kernel<D, H, T, K, 8>},
+                   {tc_fn<D, H, T, K, 4, TC>(), tc_fn<D, H, T, K, 8, TC>()},
                    N::P,
                    N::PPAD,
                    {R4::EP, R8::EP},
                    &N::smem_bytes,
                    {&R4::smem_bytes, &R8::smem_bytes},
+                   {&C4::smem_bytes, &C8::smem_bytes},
                    name};
 }
 
@@ -47,9 +58,9 @@ const std::vector<LstmEntry>& lstm_table() {
 
 const std::vector<LstmEntry>& trunk_table() {
   static const std::vector<LstmEntry> t = {
-      make_entry<5, 20, 10, 1>("lstm_trunk<D5,H20,T10>"),  // wide variant
-      make_entry<5, 8, 10, 1>("lstm_trunk<D5,H8,T10>"),
-      make_entry<3, 4, 5, 1>("lstm_trunk<D3,H4,T5>"),
+      make_entry<5, 20, 10, 1, false>("lstm_trunk<D5,H20,T10>"),  // wide variant
+      make_entry<5, 8, 10, 1, false>("lstm_trunk<D5,H8,T10>"),
+      make_entry<3, 4, 5, 1, false>("lstm_trunk<D3,H4,T5>"),
   };
   return t;
 }
@@ -248,25 +259,31 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     return fail(GHC_ERR_CUDA, "fused kernel cannot be resident (smem/registers)");
   }
   p->max_ctas = per_sm * c->num_sms;
-  // cluster variant: for clusters of 8 and of 4, the largest block that fits
-  // and how many clusters can be co-resident (GPC-constrained; queried, not
-  // assumed).  Pick the size that gives every sample its own warp with the
-  // fewest warps per CTA (ties → 8: fewer rows in the cross-cluster reduce).
+  // cluster variants: for clusters of 8 and of 4, the largest block that
+  // fits and how many clusters can be co-resident (GPC-constrained; queried,
+  // not assumed).  SIMT variant (default): every sample its own warp with the
+  // fewest warps per CTA.  Tensor-core variant (GHC_STEP=tc): fewest passes of
+  // 8 samples per CTA over the bench batch — correct on every shape but slower
+  // on B200 (legacy HMMA.1688.TF32 ≈ 12.5 cycles/instr per SM sub-partition
+  // with distinct operands, tools/tc_micro.cu; 3×TF32 then delivers fewer
+  // fp32 FMA/clk than FFMA).  Ties → 8 (fewer rows in the
+  // cross-cluster reduce).
   {
     const char* env = std::getenv("GHC_STEP");
-    p->use_cluster = !(env && std::string(env) == "flat");
-    int best_warps = 1 << 30;
-    for (int ci = 1; ci >= 0; --ci) {
-      const int cs = ci ? 8 : 4;
-      int warps = 8;
-      while (warps > 1 && p->lstm->smem_round[ci](warps) > static_cast<size_t>(smem_optin)) --warps;
-      CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(p->lstm->fn_round[ci]),
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(p->lstm->smem_round[ci](warps))));
+    const std::string step = env ? env : "";
+    p->use_cluster = step != "flat";
+    auto max_clusters = [&](void (*fn)(StepArgs), int cs, int warps, size_t smem) {
+      if (smem > static_cast<size_t>(smem_optin)) return 0;
+      if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs * 64);
       cfg.blockDim = dim3(32 * warps);
-      cfg.dynamicSmemBytes = p->lstm->smem_round[ci](warps);
+      cfg.dynamicSmemBytes = smem;
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeClusterDimension;
       attr.val.clusterDim.x = cs;
@@ -275,20 +292,53 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(p->lstm->fn_round[ci]),
-                                         &cfg) != cudaSuccess)
+      if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(fn), &cfg) != cudaSuccess)
         ncl = 0;
       cudaGetLastError();
-      if (ncl < 1) continue;
-      const int64_t slots = static_cast<int64_t>(ncl) * cs * kSamplesPerWarp;
-      const int need = static_cast<int>((1000 + slots - 1) / slots);  // bench batch per worker
-      if (need < best_warps && need <= warps) {
-        best_warps = need;
-        p->cluster_size = cs;
-        p->cs_index = ci;
-        p->max_clusters = ncl;
-        p->round_warps = warps;
+      return ncl;
+    };
+    const int64_t bench_batch = 1000;  // per-worker batch of the bench config
+    if (step == "tc" && p->lstm->fn_tc[0]) {
+      int64_t best_passes = INT64_MAX;
+      for (int ci = 1; ci >= 0; --ci) {
+        const int cs = ci ? 8 : 4;
+        const int ncl = max_clusters(p->lstm->fn_tc[ci], cs, 8, p->lstm->smem_tc[ci](8));
+        if (ncl < 1) continue;
+        const int64_t slots = static_cast<int64_t>(ncl) * cs * kTcSamples;
+        const int64_t passes = (bench_batch + slots - 1) / slots;
+        if (passes < best_passes) {
+          best_passes = passes;
+          p->cluster_size = cs;
+          p->cs_index = ci;
+          p->max_clusters = ncl;
+          p->round_warps = 8;
+          p->use_tc = true;
+        }
       }
+    }
+    if (!p->use_tc) {
+      int best_warps = 1 << 30;
+      for (int ci = 1; ci >= 0; --ci) {
+        const int cs = ci ? 8 : 4;
+        int warps = 8;
+        while (warps > 1 && p->lstm->smem_round[ci](warps) > static_cast<size_t>(smem_optin)) --warps;
+        const int ncl = max_clusters(p->lstm->fn_round[ci], cs, warps, p->lstm->smem_round[ci](warps));
+        if (ncl < 1) continue;
+        const int64_t slots = static_cast<int64_t>(ncl) * cs * kSamplesPerWarp;
+        const int need = static_cast<int>((bench_batch + slots - 1) / slots);
+        if (need < best_warps && need <= warps) {
+          best_warps = need;
+          p->cluster_size = cs;
+          p->cs_index = ci;
+          p->max_clusters = ncl;
+          p->round_warps = warps;
+        }
+      }
+    }
+    if (p->use_cluster && p->max_clusters > 0) {
+      std::string nm = p->lstm->name;
+      if (p->use_tc) nm.replace(0, std::string("lstm_round").size(), "lstm_round_tc");
+      p->kname = nm + " [clusters of " + std::to_string(p->cluster_size) + "]";
     }
     if (p->max_clusters * p->cluster_size > p->max_ctas) p->max_ctas = p->max_clusters * p->cluster_size;
   }
@@ -325,7 +375,7 @@ int64_t ghc_plan_n_params(const ghc_plan* p) { return p->model.n_params; }
 int64_t ghc_plan_input_width(const ghc_plan* p) { return p->model.input_width; }
 int32_t ghc_plan_n_classes(const ghc_plan* p) { return p->model.n_classes; }
 const char* ghc_plan_kernel_name(const ghc_plan* p) {
-  return p->lstm && p->use_cluster && p->max_clusters > 0 ? p->lstm->name : p->kname.c_str();
+  return p->kname.c_str();
 }
 int32_t ghc_plan_max_clusters(const ghc_plan* p) { return p->use_cluster ? p->max_clusters : 0; }
 int32_t ghc_plan_cluster_size(const ghc_plan* p) { return p->use_cluster ? p->cluster_size : 0; }

@@ -17,6 +17,7 @@
 #include "host_model.hpp"
 #include "lstm_round.cuh"
 #include "lstm_step.cuh"
+#include "lstm_tc.cuh"
 #include "update_kernels.cuh"
 
 using namespace ghc;
@@ -38,9 +39,11 @@ struct LstmEntry {
   int D, H, T, K;
   void (*fn)(StepArgs);        // flat variant (grid barriers)      lstm_step.cuh
   void (*fn_round[2])(StepArgs);   // cluster variant, clusters of 4 / 8 (lstm_round.cuh)
+  void (*fn_tc[2])(StepArgs);      // tensor-core cluster variant (lstm_tc.cuh); null: n/a
   int P, ppad, ep[2];
   size_t (*smem)(int);
   size_t (*smem_round[2])(int);
+  size_t (*smem_tc[2])(int);
   const char* name;
 };
 
@@ -74,6 +77,7 @@ struct ghc_plan {
   int cs_index = 1;          // 0: clusters of 4, 1: clusters of 8
   int round_warps = 8;       // warps/CTA that fit the cluster variant's smem
   bool use_cluster = true;   // GHC_STEP=flat selects the flat variant
+  bool use_tc = false;       // cluster variant runs lstm_round_tc_kernel (8 samples/CTA pass)
   Model model;
   const LstmEntry* lstm = nullptr;
   int max_ctas = 0;       // co-resident CTAs of the fused kernel
@@ -114,23 +118,33 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
   a.probe = p->probe;
   a.bar = p->bar;
   if (p->use_cluster && p->max_clusters > 0) {
-    // clusters of 8 CTAs, ≈ one CTA per SM, one warp per sample
+    // ≈ one CTA per SM; SIMT variant: one warp per sample, TC variant: the
+    // CTA's 8 warps step 8 samples together (kTcSamples per pass)
     const int cs = p->cluster_size;
-    const int spw = kSamplesPerWarp;
-    const int64_t slots = static_cast<int64_t>(p->max_clusters) * cs * spw;
-    int warps = static_cast<int>((n_max + slots - 1) / slots);
-    warps = warps < 1 ? 1 : (warps > p->round_warps ? p->round_warps : warps);
-    int64_t ctas = (n_max + warps * spw - 1) / (warps * spw);
+    int warps;
+    int64_t per_cta;  // samples per CTA in one pass
+    if (p->use_tc) {
+      warps = 8;
+      per_cta = kTcSamples;
+    } else {
+      const int spw = kSamplesPerWarp;
+      const int64_t slots = static_cast<int64_t>(p->max_clusters) * cs * spw;
+      warps = static_cast<int>((n_max + slots - 1) / slots);
+      warps = warps < 1 ? 1 : (warps > p->round_warps ? p->round_warps : warps);
+      per_cta = static_cast<int64_t>(warps) * spw;
+    }
+    int64_t ctas = (n_max + per_cta - 1) / per_cta;
     int64_t nc = (ctas + cs - 1) / cs;
     if (nc < 1) nc = 1;
     if (nc > p->max_clusters) nc = p->max_clusters;
     a.part = p->part;
     a.pstride = p->lstm->ep[p->cs_index];
-    a.pipelined = n_max <= nc * cs * warps * spw;
+    a.pipelined = n_max <= nc * cs * per_cta;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(nc * cs));
     cfg.blockDim = dim3(static_cast<unsigned>(warps * 32));
-    cfg.dynamicSmemBytes = p->lstm->smem_round[p->cs_index](warps);
+    cfg.dynamicSmemBytes = p->use_tc ? p->lstm->smem_tc[p->cs_index](warps)
+                                     : p->lstm->smem_round[p->cs_index](warps);
     cfg.stream = p->ctx->stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -148,7 +162,8 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
       return e && e[0] == '1';
     }();
     cfg.numAttrs = no_coop ? 1 : 2;
-    CU(cudaLaunchKernelEx(&cfg, p->lstm->fn_round[p->cs_index], a));
+    CU(cudaLaunchKernelEx(&cfg, p->use_tc ? p->lstm->fn_tc[p->cs_index] : p->lstm->fn_round[p->cs_index],
+                          a));
     p->ctx->launches++;
     return GHC_OK;
   }

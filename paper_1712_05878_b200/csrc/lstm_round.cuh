@@ -49,17 +49,173 @@ struct RoundLayout {
   }
 };
 
+// Steps 2–5 of the round (file header) and the final publish, shared by the
+// SIMT kernel below and the tensor-core kernel of lstm_tc.cuh.  The caller
+// holds the complete CTA partial (P gradient entries + loss in slot P) in its
+// own shared memory at `cpart`, and every CTA of the cluster has passed a
+// cluster.sync() since its partial was completed.
+template <int P, int SL, int EP, int CS>
+struct ClusterXchg {
+  static constexpr int E = P + 1;
+  float* vsl;   // [SL] velocity slice (SGD), kept in smem across rounds
+  float* vtmp;  // [SL]
+  int* badv;    // [CS] non-finite flags, written by peers
+  int crank, cid, NC, e0, e1;
+  unsigned epoch;
+  unsigned long long accepted, rejected;
+  int last_status;
+  bool sgd;
+
+  __device__ void init(const StepArgs& a, cg::cluster_group& cluster, float* vs, float* vt, int* bv) {
+    vsl = vs;
+    vtmp = vt;
+    badv = bv;
+    crank = (int)cluster.block_rank();
+    cid = blockIdx.x / CS;
+    NC = gridDim.x / CS;
+    e0 = crank * SL;
+    e1 = min(E, e0 + SL);
+    epoch = __ldcg(a.bar);
+    accepted = rejected = 0;
+    last_status = 0;
+    sgd = a.mode == MODE_SGD;
+  }
+
+  // Master weights/velocity of the current buffer → wbuf (all P) and vsl.
+  __device__ void load_state(const StepArgs& a, const float* gw, const float* gv, float* wbuf) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) wbuf[p] = __ldcg(gw + p);
+    if (sgd)
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = e < P ? __ldcg(gv + e) : 0.f;
+  }
+
+  __device__ void exchange(const StepArgs& a, cg::cluster_group& cluster, int r, float* cpart,
+                           float*& wa, float*& wb, unsigned long long* pr) {
+    const int par = r & 1;
+    // ---- (2) slice j over the cluster via DSMEM → cluster partial in HBM ----
+    float* grow = a.part + ((long long)par * NC + cid) * EP;
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      float t = 0.0f;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) t += cluster.map_shared_rank(cpart, q)[e];
+      __stcg(grow + e, t);
+    }
+    if (pr && threadIdx.x == 0) pr[5] = globaltimer();
+
+    // ---- (3) column barrier: the NC CTAs that own slice j ----
+    ++epoch;
+    __syncthreads();
+    unsigned* flags = a.bar + 2 * kFlagStride;
+    if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * kFlagStride, epoch);
+    for (int c = threadIdx.x; c < NC; c += blockDim.x) {
+      const unsigned* f = flags + (c * CS + crank) * kFlagStride;
+      while ((int)(ld_relaxed_gpu(f) - epoch) < 0) {
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncthreads();
+    if (pr && threadIdx.x == 0) pr[6] = globaltimer();
+
+    // ---- (4) slice j over all clusters (fixed order) → update → broadcast ----
+    // float4 columns: SL and EP are multiples of 4, e0 too.
+    int bad = 0;
+    const float* gcol = a.part + (long long)par * NC * EP;
+    for (int e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = 0; c0 < NC; c0 += 8) {  // 8 float4 loads in flight, fixed-order sum
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[i] = c0 + i < NC
+                     ? __ldcg(reinterpret_cast<const float4*>(gcol + (long long)(c0 + i) * EP + e))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          t.x += v[i].x;
+          t.y += v[i].y;
+          t.z += v[i].z;
+          t.w += v[i].w;
+        }
+      }
+      const float tv[4] = {t.x, t.y, t.z, t.w};
+      float wn[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ee = e + i;
+        wn[i] = 0.0f;
+        if (ee >= e1) continue;
+        if (ee == P) {
+          if (cid == 0 && a.loss_out) a.loss_out[r] = tv[i];
+        } else if (a.mode == MODE_GRAD) {
+          if (cid == 0) a.g_out[ee] = tv[i];
+        } else if (sgd) {
+          if (!is_finite_f(tv[i])) bad = 1;
+          // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v
+          const float vn = fmaf(a.mu, vsl[ee - e0], -a.lr * tv[i]);
+          vtmp[ee - e0] = vn;
+          wn[i] = wa[ee] + vn;
+        }
+      }
+      if (sgd) {  // new weights → every CTA of the cluster (DSMEM, float4)
+        const float4 w4 = make_float4(wn[0], wn[1], wn[2], wn[3]);
+#pragma unroll
+        for (int q = 0; q < CS; ++q)
+          reinterpret_cast<float4*>(cluster.map_shared_rank(wb, q) + e)[0] = w4;
+      }
+    }
+    if (sgd) {
+      bad = __syncthreads_or(bad);
+      if (threadIdx.x < CS) cluster.map_shared_rank(badv, (int)threadIdx.x)[crank] = bad;
+    }
+    if (pr && threadIdx.x == 0) pr[7] = globaltimer();
+    cluster.sync();  // new weights + flags landed in every CTA of the cluster
+    if (pr && threadIdx.x == 0) pr[13] = globaltimer();
+    if (sgd) {
+      int rej = 0;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) rej |= badv[q];
+      if (rej) {
+        ++rejected;
+        last_status = 2;  // GHC_ERR_NONFINITE: keep w/v (optim.cpp:49-51)
+      } else {
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = vtmp[e - e0];
+        float* t = wa;
+        wa = wb;
+        wb = t;
+        ++accepted;
+        last_status = 0;
+      }
+      __syncthreads();
+    }
+  }
+
+  // Master state back to HBM (cluster 0 holds the same bits as every cluster).
+  __device__ void publish(const StepArgs& a, float* gw, float* gv, const float* wa,
+                          unsigned long long round0) {
+    if (sgd && cid == 0) {
+      for (int e = e0 + threadIdx.x; e < e1 && e < P; e += blockDim.x) {
+        gw[e] = wa[e];
+        gv[e] = vsl[e - e0];
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.bar[0] = epoch;
+      if (sgd) {
+        a.ms->version += accepted;
+        a.ms->rejected += rejected;
+        a.ms->round = round0 + (unsigned long long)a.rounds;
+        a.ms->status = last_status;
+      }
+    }
+  }
+};
+
 template <int D, int H, int T, int K, int CS>
 __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   using N = LstmNet<D, H, T, K>;
   using RL = RoundLayout<D, H, T, K, CS>;
   constexpr int SL = RL::SL;
-  constexpr int E = RL::E;
   constexpr int SPW = RL::SPW;
   cg::cluster_group cluster = cg::this_cluster();
-  const int crank = (int)cluster.block_rank();
-  const int cid = blockIdx.x / CS;
-  const int NC = gridDim.x / CS;
   const int G = gridDim.x;
 
   extern __shared__ __align__(16) float smem[];
@@ -70,28 +226,19 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   float* ws = smem + 2 * N::PPAD + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
   float* wpart = smem + 2 * N::PPAD + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
   float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
-  float* vtmp = vsl + SL;                                      // [SL]
-  int* badv = reinterpret_cast<int*>(vtmp + SL);               // [CS], written by peers
-  const int e0 = crank * SL;
-  const int e1 = min(E, e0 + SL);
+  ClusterXchg<N::P, SL, RL::EP, CS> xc;
+  xc.init(a, cluster, vsl, vsl + SL, reinterpret_cast<int*>(vsl + 2 * SL));
 
+  unsigned long long round0 = 0;
   int cur = 0;
-  unsigned long long round0 = 0, accepted = 0, rejected = 0;
-  int last_status = 0;
-  const bool sgd = a.mode == MODE_SGD;
+  const bool sgd = xc.sgd;
   if (sgd) {
     cur = __ldcg(&a.ms->cur);
     round0 = __ldcg(&a.ms->round);
   }
-  unsigned epoch = __ldcg(a.bar);
   float* gw = sgd ? (cur ? a.w1 : a.w0) : nullptr;  // master weights in HBM
   float* gv = sgd ? (cur ? a.v1 : a.v0) : nullptr;
-  {
-    const float* w = sgd ? gw : a.w_in;
-    for (int p = threadIdx.x; p < N::P; p += blockDim.x) wbuf0[p] = __ldcg(w + p);
-    if (sgd)
-      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = e < N::P ? __ldcg(gv + e) : 0.f;
-  }
+  xc.load_state(a, sgd ? gw : a.w_in, gv, wbuf0);
   float* wa = wbuf0;  // weights the samples use
   float* wb = wbuf1;  // peers deposit the next weights here
 
@@ -132,7 +279,6 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   for (int r = 0; r < a.rounds; ++r) {
     const int n = a.counts ? __ldg(a.counts + r) : a.n;
     const float scale = sgd ? 1.0f / (float)n : a.grad_scale;
-    const int par = r & 1;
     unsigned long long* pr =
         a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
     if (pr && threadIdx.x == 0) pr[0] = globaltimer();
@@ -160,7 +306,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         cp_async_commit();
       }
       if (s < s1) {
-        cp_async_wait<1>();  // this round's rows (older group) have landed
+        if (next) cp_async_wait<1>();  // this round's rows (older group) have landed
+        else cp_async_wait<0>();       // no newer group on the last round
         __syncwarp();
         const float* xsp[SPW];
         int lab[SPW];
@@ -246,119 +393,10 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     cluster.sync();  // CTA partials of the whole cluster complete
     if (pr && threadIdx.x == 0) pr[4] = globaltimer();
 
-    // ---- (2) slice j over the cluster via DSMEM → cluster partial in HBM ----
-    float* grow = a.part + ((long long)par * NC + cid) * RL::EP;
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      float t = 0.0f;
-#pragma unroll
-      for (int q = 0; q < CS; ++q) t += cluster.map_shared_rank(wpart, q)[e];
-      __stcg(grow + e, t);
-    }
-    if (pr && threadIdx.x == 0) pr[5] = globaltimer();
-
-    // ---- (3) column barrier: the NC CTAs that own slice j ----
-    ++epoch;
-    __syncthreads();
-    unsigned* flags = a.bar + 2 * kFlagStride;
-    if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * kFlagStride, epoch);
-    for (int c = threadIdx.x; c < NC; c += blockDim.x) {
-      const unsigned* f = flags + (c * CS + crank) * kFlagStride;
-      while ((int)(ld_relaxed_gpu(f) - epoch) < 0) {
-      }
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    }
-    __syncthreads();
-    if (pr && threadIdx.x == 0) pr[6] = globaltimer();
-
-    // ---- (4) slice j over all clusters (fixed order) → update → broadcast ----
-    // float4 columns: SL and EP are multiples of 4, e0 too.
-    int bad = 0;
-    const float* gcol = a.part + (long long)par * NC * RL::EP;
-    for (int e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
-      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c0 = 0; c0 < NC; c0 += 8) {  // 8 float4 loads in flight, fixed-order sum
-        float4 v[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          v[i] = c0 + i < NC
-                     ? __ldcg(reinterpret_cast<const float4*>(gcol + (long long)(c0 + i) * RL::EP + e))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          t.x += v[i].x;
-          t.y += v[i].y;
-          t.z += v[i].z;
-          t.w += v[i].w;
-        }
-      }
-      const float tv[4] = {t.x, t.y, t.z, t.w};
-      float wn[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ee = e + i;
-        wn[i] = 0.0f;
-        if (ee >= e1) continue;
-        if (ee == N::P) {
-          if (cid == 0 && a.loss_out) a.loss_out[r] = tv[i];
-        } else if (a.mode == MODE_GRAD) {
-          if (cid == 0) a.g_out[ee] = tv[i];
-        } else if (sgd) {
-          if (!is_finite_f(tv[i])) bad = 1;
-          // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v
-          const float vn = fmaf(a.mu, vsl[ee - e0], -a.lr * tv[i]);
-          vtmp[ee - e0] = vn;
-          wn[i] = wa[ee] + vn;
-        }
-      }
-      if (sgd) {  // new weights → every CTA of the cluster (DSMEM, float4)
-        const float4 w4 = make_float4(wn[0], wn[1], wn[2], wn[3]);
-#pragma unroll
-        for (int q = 0; q < CS; ++q)
-          reinterpret_cast<float4*>(cluster.map_shared_rank(wb, q) + e)[0] = w4;
-      }
-    }
-    if (sgd) {
-      bad = __syncthreads_or(bad);
-      if (threadIdx.x < CS) cluster.map_shared_rank(badv, (int)threadIdx.x)[crank] = bad;
-    }
-    if (pr && threadIdx.x == 0) pr[7] = globaltimer();
-    cluster.sync();  // new weights + flags landed in every CTA of the cluster
-    if (pr && threadIdx.x == 0) pr[13] = globaltimer();
-    if (sgd) {
-      int rej = 0;
-#pragma unroll
-      for (int q = 0; q < CS; ++q) rej |= badv[q];
-      if (rej) {
-        ++rejected;
-        last_status = 2;  // GHC_ERR_NONFINITE: keep w/v (optim.cpp:49-51)
-      } else {
-        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = vtmp[e - e0];
-        float* t = wa;
-        wa = wb;
-        wb = t;
-        ++accepted;
-        last_status = 0;
-      }
-      __syncthreads();
-    }
+    xc.exchange(a, cluster, r, wpart, wa, wb, pr);
   }
 
-  // ---- publish master state (cluster 0 holds the same bits as every cluster) ----
-  if (sgd && cid == 0) {
-    for (int e = e0 + threadIdx.x; e < e1 && e < N::P; e += blockDim.x) {
-      gw[e] = wa[e];
-      gv[e] = vsl[e - e0];
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.bar[0] = epoch;
-    if (sgd) {
-      a.ms->version += accepted;
-      a.ms->rejected += rejected;
-      a.ms->round = round0 + (unsigned long long)a.rounds;
-      a.ms->status = last_status;
-    }
-  }
+  xc.publish(a, gw, gv, wa, round0);
 }
 
 }  // namespace ghc

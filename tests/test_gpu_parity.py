@@ -19,6 +19,18 @@ import paper_1712_05878_b200 as g
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True, params=["tc", "simt"])
+def step_variant(request, monkeypatch):
+    """Every parity case runs on both cluster-round variants: the SIMT kernel
+    (default, lstm_round.cuh) and the tensor-core kernel (GHC_STEP=tc,
+    lstm_tc.cuh).  The variant is fixed when a plan is created."""
+    if request.param == "tc":
+        monkeypatch.setenv("GHC_STEP", "tc")
+    else:
+        monkeypatch.delenv("GHC_STEP", raising=False)
+    return request.param
+
 SHAPES = [BENCH_ARCH, "lstm(5,8,10),softmax(8,3)", "lstm(3,4,5),softmax(4,3)",
           "lstm(2,16,3),softmax(16,4)", "lstm(5,32,10),softmax(32,3)",
           "lstm(4,12,6),softmax(12,5)"]
@@ -37,7 +49,7 @@ def dataset(arch_text, n, seed=1234):
 
 
 @pytest.mark.parametrize("arch_text", SHAPES)
-@pytest.mark.parametrize("n", [1, 7, 100, 1000])
+@pytest.mark.parametrize("n", [1, 7, 100, 1000, 5000])
 def test_worker_grad_vs_oracle(ctx, oracle, arch_text, n):
     arch = g.Architecture(ctx, arch_text)
     w = g.init_weights(arch, 7)
