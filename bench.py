@@ -339,9 +339,17 @@ def run_ours_dist(args, rank, world, local):
 
 
 def run_e2e(args, g, ctx, arch, x, y, idx):
-    """Same metric through the C ABI with HOST batches: per step the batch is
-    copied from pinned host memory, one sync round runs, and the round's loss
-    is copied back; no host sync between steps."""
+    """Same metric through the public API with HOST batches, two ways:
+
+    * streaming (the headline ``e2e``): the K steps' batches sit in pinned
+      host memory (HostArray) and ONE ghc_master_sync_rounds call trains on
+      them — every round the persistent kernel prefetches its next batch rows
+      from host memory over PCIe (cp.async, one round ahead) and stores the
+      round's loss into pinned host memory.  All K·204 KB of inputs cross
+      host→device and all K losses cross device→host inside the timed region.
+    * per_call: one ghc_memcpy_h2d(batch) + ghc_master_sync_rounds(1 round) +
+      ghc_memcpy_d2h(loss) per step on one stream (the reference's
+      one-batch-per-call usage, launch and copy latencies exposed)."""
     import ctypes as C
     from paper_1712_05878_b200 import _lib
     lib = _lib.load()
@@ -350,18 +358,33 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
     width = x.shape[1]
     xb_bytes = B * width * 4
     yb_bytes = B * 4
-    hp = C.c_void_p()
-    _lib.check(lib.ghc_host_alloc(K * (xb_bytes + yb_bytes) + K * 4, C.byref(hp)))
-    base = hp.value
-    hx = np.ctypeslib.as_array((C.c_float * (K * B * width)).from_address(base)).reshape(K, B, width)
-    hy = np.ctypeslib.as_array((C.c_int32 * (K * B)).from_address(base + K * xb_bytes)).reshape(K, B)
-    hl = np.ctypeslib.as_array((C.c_float * K).from_address(base + K * (xb_bytes + yb_bytes)))
-    for k in range(K):
-        sel = idx[k * B:(k + 1) * B]
-        hx[k] = x[sel]
-        hy[k] = y[sel]
+    hx = ctx.host_array((K * B, width))
+    hy = ctx.host_array(K * B, np.int32)
+    hl = ctx.host_array(K)
+    sel = idx[: K * B]
+    hx.np[:] = x[sel]
+    hy.np[:] = y[sel]
+    hl.np[:] = np.nan
     w0 = g.init_weights(arch, 7)
     m = g.Master(arch, w0, 0.01, 0.9)
+    m.sync_rounds(hx, hy, None, B, B, 3, loss_out=hl)  # warm-up (first 3 batches)
+    ctx.sync()
+    m = g.Master(arch, w0, 0.01, 0.9)
+    hl.np[:] = np.nan
+    ctx.sync()
+    ctx.timer_start()
+    m.sync_rounds(hx, hy, None, B, B, K, loss_out=hl)
+    ms = ctx.timer_stop()
+    ctx.sync()
+    ok = bool(np.isfinite(hl.np).all())
+    streaming = {"value": B * K / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": xb_bytes + yb_bytes,
+                 "d2h_bytes_per_step": 4, "steps": K, "ms_per_step": ms / K, "losses_finite": ok,
+                 "path": "ghc_master_sync_rounds over K host batches (pinned HostArray, zero-copy): the "
+                         "persistent round kernel prefetches each round's rows from host memory one "
+                         "round ahead and stores each round's loss to host memory"}
+
+    # per_call: one batch per API call
+    Kc = min(K, 200)
     dxb = ctx.array((B, width))
     dyb = ctx.array(B, np.int32)
     dl = ctx.array(1)
@@ -369,21 +392,20 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
         m.sync_rounds(dxb, dyb, None, 0, B, 1, loss_out=dl)
     ctx.sync()
     ctx.timer_start()
-    for k in range(K):
-        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dxb.ptr, C.c_void_p(base + k * xb_bytes), xb_bytes))
-        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dyb.ptr, C.c_void_p(base + K * xb_bytes + k * yb_bytes),
-                                      yb_bytes))
+    for k in range(Kc):
+        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dxb.ptr, hx.offset(k * B * width), xb_bytes))
+        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dyb.ptr, hy.offset(k * B), yb_bytes))
         m.sync_rounds(dxb, dyb, None, 0, B, 1, loss_out=dl)
-        _lib.check(lib.ghc_memcpy_d2h(ctx.h, C.c_void_p(base + K * (xb_bytes + yb_bytes) + 4 * k),
-                                      dl.ptr, 4))
-    ms = ctx.timer_stop()
+        _lib.check(lib.ghc_memcpy_d2h(ctx.h, hl.offset(k), dl.ptr, 4))
+    msc = ctx.timer_stop()
     ctx.sync()
-    ok = bool(np.isfinite(hl).all())
-    lib.ghc_host_free(hp)
-    return {"value": B * K / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": xb_bytes + yb_bytes,
-            "d2h_bytes_per_step": 4, "steps": K, "ms_per_step": ms / K, "losses_finite": ok,
-            "path": "ghc_memcpy_h2d(batch) + ghc_master_sync_rounds(1 round) + "
-                    "ghc_memcpy_d2h(loss) per step, pinned host buffers, one stream"}
+    streaming["per_call"] = {"value": B * Kc / (msc / 1e3), "steps": Kc, "ms_per_step": msc / Kc,
+                             "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
+                             "path": "ghc_memcpy_h2d(batch) + ghc_master_sync_rounds(1 round) + "
+                                     "ghc_memcpy_d2h(loss) per step, pinned host buffers, one stream"}
+    for a in (hx, hy, hl):
+        a.free()
+    return streaming
 
 
 def update_roofline(args, g, ctx):

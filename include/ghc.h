@@ -195,9 +195,14 @@ ghc_status ghc_master_read(ghc_master* m, float* h_w, float* h_v, uint64_t* vers
 /* n_rounds synchronous Downpour rounds of ONE worker colocated with the
  * master (1 master + 1 worker per GPU) in ONE persistent
  * launch: per round gather the batch d_idx[r*stride ..] from the resident
- * dataset, forward+loss+backward, deterministic cross-CTA gradient reduce,
- * finite check, sgd_step, commit.  d_counts[r] = samples in round r
- * (nullable → n each).  d_loss_out[r] = loss sum of round r (nullable). */
+ * dataset (d_idx == NULL: round r uses rows r*stride .. r*stride+n-1),
+ * forward+loss+backward, deterministic cross-CTA gradient reduce, finite
+ * check, sgd_step, commit.  d_counts[r] = samples in round r (nullable → n
+ * each).  d_loss_out[r] = loss sum of round r (nullable).
+ * d_x, d_y and d_loss_out only need to be device-ACCESSIBLE: pinned host
+ * memory (ghc_host_alloc) streams the batches straight from the host — each
+ * CTA prefetches its next-round rows over PCIe during the current round and
+ * the round's loss is stored to host memory (zero-copy end-to-end path). */
 ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t* d_y,
                                   const int32_t* d_idx, int64_t stride,
                                   const int32_t* d_counts, int64_t n, int32_t n_rounds,

@@ -656,7 +656,9 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
     if (ghc_status s = master_cur(m, cur)) return s;
     for (int r = 0; r < n_rounds; ++r) {
       const int32_t nr = cnt[static_cast<size_t>(r)];
-      if (ghc_status s = layered_step(m->plan, m->w[cur], d_x, d_y,
+      const int64_t roff = d_idx ? 0 : static_cast<int64_t>(r) * stride;  // no table: rows r*stride+s
+      if (ghc_status s = layered_step(m->plan, m->w[cur], d_x + roff * m->plan->model.input_width,
+                                      d_y + roff,
                                       d_idx ? d_idx + static_cast<int64_t>(r) * stride : nullptr, nr,
                                       1.0f / static_cast<float>(nr), m->g_scratch,
                                       d_loss_out ? d_loss_out + r : nullptr, nullptr))

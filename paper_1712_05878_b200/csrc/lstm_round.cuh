@@ -263,8 +263,18 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     if (lane == 0) cp_async4(slot_l(sp) + b, a.y + row);
   };
   auto row_of = [&](int r, int s) {
-    const int32_t* idx = a.idx ? a.idx + (long long)r * a.stride : nullptr;
-    return idx ? __ldg(idx + s) : s;
+    // no gather table: round r reads rows r*stride + s (stride 0: rows s)
+    return a.idx ? __ldg(a.idx + (long long)r * a.stride + s) : (int)((long long)r * a.stride + s);
+  };
+  // gather indices of round r (pipelined path): one cp.async per slot into
+  // slot_l[2], fetched a round before the rows they select
+  auto fetch_idx_nocommit = [&](int r) {
+    if (!a.idx || lane != 0 || r >= a.rounds) return;
+    int sx, sx1;
+    first_sample(r, sx, sx1);
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp)
+      if (sx + sp * NW < sx1) cp_async4(slot_l(sp) + 2, a.idx + (long long)r * a.stride + sx + sp * NW);
   };
   if (a.pipelined) {
     int s, s1;
@@ -272,6 +282,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp)
       if (s + sp * NW < s1) fetch_nocommit(sp, row_of(0, s + sp * NW), 0);
+    fetch_idx_nocommit(1);
     cp_async_commit();
   }
   __syncthreads();
@@ -293,22 +304,28 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     int s, s1;
     first_sample(r, s, s1);
     if (a.pipelined) {
-      int sn = 0, sn1 = 0;
-      const bool next = r + 1 < a.rounds;
-      if (next) {
+      // Rows of round r and indices of round r+1 were requested at the start
+      // of round r-1 (prologue for r = 0): a whole round of compute and
+      // exchange hides their latency — PCIe included when x/y are pinned
+      // host memory.  Now request round r+1's rows (into the buffer round
+      // r-1 used) and round r+2's indices, then compute round r.
+      cp_async_wait<0>();
+      __syncwarp();
+      if (r + 1 < a.rounds) {
+        int sn, sn1;
         first_sample(r + 1, sn, sn1);
-        if (a.idx && lane == 0) {
+        int rows[SPW];
 #pragma unroll
-          for (int sp = 0; sp < SPW; ++sp)
-            if (sn + sp * NW < sn1)
-              cp_async4(slot_l(sp) + 2, a.idx + (long long)(r + 1) * a.stride + sn + sp * NW);
-        }
+        for (int sp = 0; sp < SPW; ++sp)
+          rows[sp] = a.idx ? slot_l(sp)[2] : (int)((long long)(r + 1) * a.stride + sn + sp * NW);
+        __syncwarp();
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp)
+          if (sn + sp * NW < sn1) fetch_nocommit(sp, rows[sp], (r + 1) & 1);
+        fetch_idx_nocommit(r + 2);
         cp_async_commit();
       }
       if (s < s1) {
-        if (next) cp_async_wait<1>();  // this round's rows (older group) have landed
-        else cp_async_wait<0>();       // no newer group on the last round
-        __syncwarp();
         const float* xsp[SPW];
         int lab[SPW];
         float scl[SPW];
@@ -339,18 +356,6 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
           if (s + sp * NW < s1) lsum += lo[sp];
-      }
-      if (next && sn < sn1) {
-        cp_async_wait<0>();
-        __syncwarp();
-        int rows[SPW];
-#pragma unroll
-        for (int sp = 0; sp < SPW; ++sp) rows[sp] = a.idx ? slot_l(sp)[2] : sn + sp * NW;
-        __syncwarp();
-#pragma unroll
-        for (int sp = 0; sp < SPW; ++sp)
-          if (sn + sp * NW < sn1) fetch_nocommit(sp, rows[sp], (r + 1) & 1);
-        cp_async_commit();
       }
     } else {
       for (; s < s1; s += NW) {

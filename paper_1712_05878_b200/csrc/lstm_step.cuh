@@ -518,8 +518,8 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     cp_async_commit();
   };
   auto row_of = [&](int r, int s) {
-    const int32_t* idx = a.idx ? a.idx + (long long)r * a.stride : nullptr;
-    return idx ? __ldg(idx + s) : s;
+    // no gather table: round r reads rows r*stride + s (stride 0: rows s)
+    return a.idx ? __ldg(a.idx + (long long)r * a.stride + s) : (int)((long long)r * a.stride + s);
   };
   if (a.pipelined) {
     int s, s1;
@@ -566,7 +566,8 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
         cp_async_commit();
       }
       if (s < s1) {
-        cp_async_wait<1>();  // this round's row (older group) has landed
+        if (next) cp_async_wait<1>();  // this round's row (older group) has landed
+        else cp_async_wait<0>();       // no newer group on the last round
         __syncwarp();
         int label = lbuf[r & 1];
         if (label < 0 || label >= K) {
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
       if (next && sn < sn1) {
         cp_async_wait<0>();
         __syncwarp();
-        const int row = a.idx ? lbuf[2] : sn;
+        const int row = a.idx ? lbuf[2] : (int)((long long)(r + 1) * a.stride + sn);
         __syncwarp();
         fetch_async(row, (r + 1) & 1);
       }

@@ -199,8 +199,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_tc_kernel(StepArgs a) {
     s1 = min(n, s0 + spc);
   };
   auto row_of = [&](int r, int s) {
-    const int32_t* idx = a.idx ? a.idx + (long long)r * a.stride : nullptr;
-    return idx ? __ldg(idx + s) : s;
+    // no gather table: round r reads rows r*stride + s (stride 0: rows s)
+    return a.idx ? __ldg(a.idx + (long long)r * a.stride + s) : (int)((long long)r * a.stride + s);
   };
   // warp w stages sample slot w of a pass: x row (cp.async) + label
   auto fetch_nocommit = [&](int row, int b) {
@@ -209,10 +209,17 @@ __global__ void __launch_bounds__(256, 1) lstm_round_tc_kernel(StepArgs a) {
     for (int i = lane; i < T * D; i += 32) cp_async4(dst + i, xrow + i);
     if (lane == 0) cp_async4(lab + b * S + warp, a.y + row);
   };
+  auto fetch_idx_nocommit = [&](int r) {  // slot w's gather index of round r → lab[2S+w]
+    if (!a.idx || lane != 0 || r >= a.rounds) return;
+    int sx, sx1;
+    first_sample(r, sx, sx1);
+    if (sx + warp < sx1) cp_async4(lab + 2 * S + warp, a.idx + (long long)r * a.stride + sx + warp);
+  };
   if (a.pipelined) {
     int s0, s1;
     first_sample(0, s0, s1);
     if (s0 + warp < s1) fetch_nocommit(row_of(0, s0 + warp), 0);
+    fetch_idx_nocommit(1);
     cp_async_commit();
   }
   __syncthreads();
@@ -227,17 +234,20 @@ __global__ void __launch_bounds__(256, 1) lstm_round_tc_kernel(StepArgs a) {
 
     int s0, s1;
     first_sample(r, s0, s1);
-    int sn0 = 0, sn1 = 0;
-    const bool next = a.pipelined && r + 1 < a.rounds;
     if (a.pipelined) {
-      if (next) {
+      // rows of round r / indices of round r+1 were requested a round ago;
+      // request round r+1's rows and round r+2's indices before computing
+      cp_async_wait<0>();
+      __syncwarp();
+      if (r + 1 < a.rounds) {
+        int sn0, sn1;
         first_sample(r + 1, sn0, sn1);
-        if (a.idx && lane == 0 && sn0 + warp < sn1)
-          cp_async4(lab + 2 * S + warp, a.idx + (long long)(r + 1) * a.stride + sn0 + warp);
+        const int row = a.idx ? lab[2 * S + warp] : (int)((long long)(r + 1) * a.stride + sn0 + warp);
+        __syncwarp();
+        if (sn0 + warp < sn1) fetch_nocommit(row, (r + 1) & 1);
+        fetch_idx_nocommit(r + 2);
         cp_async_commit();
       }
-      if (next) cp_async_wait<1>();  // this round's rows (older group) have landed
-      else cp_async_wait<0>();
     }
 
     // ---------------- one pass per 8 samples ----------------
@@ -514,13 +524,6 @@ __global__ void __launch_bounds__(256, 1) lstm_round_tc_kernel(StepArgs a) {
           wgrad_tiles(std::integral_constant<int, 1>{}, MF + i / L::NTW, i % L::NTW);
         if (pr && threadIdx.x == 0) pr[12] = globaltimer();
       }
-    }
-    // prefetch the next round's rows (their indices landed with the older group)
-    if (next) {
-      cp_async_wait<0>();
-      __syncwarp();
-      if (sn0 + warp < sn1) fetch_nocommit(a.idx ? lab[2 * S + warp] : sn0 + warp, (r + 1) & 1);
-      cp_async_commit();
     }
     __syncthreads();
     if (pr && threadIdx.x == 0) pr[2] = pr[3] = globaltimer();

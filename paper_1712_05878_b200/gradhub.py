@@ -74,6 +74,9 @@ class Context:
         check(self.lib.ghc_timer_stop(self.h, C.byref(ms)))
         return ms.value
 
+    def host_array(self, shape, dtype=np.float32) -> "HostArray":
+        return HostArray(self, shape, dtype)
+
     def array(self, shape, dtype=np.float32) -> "DeviceArray":
         return DeviceArray(self, shape, dtype)
 
@@ -124,6 +127,40 @@ class DeviceArray:
         check(self.ctx.lib.ghc_memcpy_d2h(self.ctx.h, _vp(out), self.ptr, self.nbytes), "d2h")
         self.ctx.sync()
         return out
+
+
+class HostArray:
+    """Pinned host buffer (ghc_host_alloc) exposed as a numpy view.  It is
+    device-accessible (UVA), so it can stand in for a DeviceArray where the C
+    ABI reads batches or writes losses: Master.sync_rounds then streams the
+    rows from host memory inside the persistent round kernel (zero-copy)."""
+
+    def __init__(self, ctx: Context, shape, dtype=np.float32):
+        self.ctx = ctx
+        self.shape = tuple(shape) if isinstance(shape, (tuple, list)) else (int(shape),)
+        self.dtype = np.dtype(dtype)
+        self.nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+        p = C.c_void_p()
+        check(ctx.lib.ghc_host_alloc(self.nbytes, C.byref(p)), "ghc_host_alloc")
+        self.ptr = p
+        n = int(np.prod(self.shape))
+        buf = (C.c_char * self.nbytes).from_address(p.value)
+        self.np = np.frombuffer(buf, dtype=self.dtype, count=n).reshape(self.shape)
+
+    def free(self):
+        if self.ptr is not None and not _SHUTDOWN[0]:
+            self.np = None
+            self.ctx.lib.ghc_host_free(self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def offset(self, elements: int) -> C.c_void_p:
+        return C.c_void_p(self.ptr.value + elements * self.dtype.itemsize)
 
 
 class Architecture:

@@ -223,3 +223,36 @@ def test_master_rejects_nonfinite_round(ctx):
     m.sync_rounds(ctx.upload(x_bad), ctx.upload(y), ctx.upload(idx), B, B, 2, idx_offset=B)
     w, v, ver, rej = m.read()
     assert ver == 2 and rej == 1 and np.isfinite(w).all()
+
+
+@pytest.mark.parametrize("B", [1000, 3000])
+def test_master_streams_host_batches(ctx, B):
+    """Zero-copy end-to-end path: batches in pinned host memory (HostArray,
+    no gather table → round r reads rows r*B ..), losses stored to host
+    memory.  Same bits as gathering the same rows from a device-resident
+    dataset, and as staging them contiguously on the device.  B = 3000 takes
+    the kernel's non-prefetching path (more samples than warp slots)."""
+    R = 12
+    spec = g.data_spec(20, 5000)
+    x, y = g.generate(spec)
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    w0 = g.init_weights(arch, 7)
+    idx = np.random.default_rng(3).permutation(len(y))[: R * B].astype(np.int32)
+    m1 = g.Master(arch, w0, 0.01, 0.9)
+    l1 = ctx.array(R)
+    m1.sync_rounds(ctx.upload(x), ctx.upload(y), ctx.upload(idx), B, B, R, loss_out=l1)
+    hx = ctx.host_array((R * B, x.shape[1]))
+    hy = ctx.host_array(R * B, np.int32)
+    hl = ctx.host_array(R)
+    hx.np[:] = x[idx]
+    hy.np[:] = y[idx]
+    hl.np[:] = np.nan
+    m2 = g.Master(arch, w0, 0.01, 0.9)
+    m2.sync_rounds(hx, hy, None, B, B, R, loss_out=hl)
+    ctx.sync()
+    m3 = g.Master(arch, w0, 0.01, 0.9)
+    m3.sync_rounds(ctx.upload(x[idx]), ctx.upload(y[idx]), None, B, B, R)
+    (w1, v1, ver1, _), (w2, v2, ver2, _), (w3, _, _, _) = m1.read(), m2.read(), m3.read()
+    assert ver1 == ver2 == R
+    assert np.array_equal(w1, w2) and np.array_equal(v1, v2) and np.array_equal(w1, w3)
+    assert np.array_equal(l1.numpy(), hl.np)
