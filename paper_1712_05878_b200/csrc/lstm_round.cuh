@@ -54,6 +54,11 @@ struct RoundLayout {
 // holds the complete CTA partial (P gradient entries + loss in slot P) in its
 // own shared memory at `cpart`, and every CTA of the cluster has passed a
 // cluster.sync() since its partial was completed.
+#ifndef GHC_XCHG_BATCH
+#define GHC_XCHG_BATCH 32
+#endif
+constexpr int kXchgBatch = GHC_XCHG_BATCH;  // cluster-partial rows loaded per batch (step 4)
+
 template <int P, int SL, int EP, int CS>
 struct ClusterXchg {
   static constexpr int E = P + 1;
@@ -121,15 +126,15 @@ struct ClusterXchg {
     const float* gcol = a.part + (long long)par * NC * EP;
     for (int e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
       float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c0 = 0; c0 < NC; c0 += 8) {  // 8 float4 loads in flight, fixed-order sum
-        float4 v[8];
+      for (int c0 = 0; c0 < NC; c0 += kXchgBatch) {  // loads in flight; fixed-order sum
+        float4 v[kXchgBatch];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < kXchgBatch; ++i)
           v[i] = c0 + i < NC
                      ? __ldcg(reinterpret_cast<const float4*>(gcol + (long long)(c0 + i) * EP + e))
                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < kXchgBatch; ++i) {
           t.x += v[i].x;
           t.y += v[i].y;
           t.z += v[i].z;
