@@ -258,7 +258,8 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
                    "global_batch": B * world, "seq_len": 10, "parallelism": f"dp{world}",
                    "rounds_per_launch": chunk,
                    "exchange": "in-kernel (DSMEM + L2)" if world == 1 else
-                               f"NCCL {args.exchange} over NVLink",
+                               ("in-kernel over NVLink peer memory (ghc_p2p)" if args.exchange == "p2p"
+                                else f"NCCL {args.exchange} over NVLink"),
                    "l2": "inputs larger than L2: 182 MB shard/GPU > 126 MB L2, fresh "
                          "shuffled batch gathered every round"},
         "roofline": {"bound": "tensor", "achieved": achieved_tflops / world * world,
@@ -284,7 +285,9 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
 
 
 def run_ours_dist(args, rank, world, local):
-    """N > 1: one worker per GPU; NCCL exchange (ghc_dist_sync_rounds)."""
+    """N > 1: one worker per GPU.  Default exchange: the fused NVLink path
+    (ghc_p2p_sync_rounds — the round kernels reduce through peer memory);
+    --exchange reduce_bcast / allreduce: NCCL per round (ghc_dist_sync_rounds)."""
     import torch
     import torch.distributed as tdist
 
@@ -294,9 +297,13 @@ def run_ours_dist(args, rank, world, local):
     ctx = g.Context(local)
     arch = g.Architecture(ctx, ARCH)
     B = args.batch
-    uid = gd.rendezvous(tdist, rank, gd.nccl_unique_id)
-    comm = gd.Comm(ctx, uid, rank, world)
-    exchange = gd.ALLREDUCE if args.exchange == "allreduce" else gd.REDUCE_BCAST
+    p2p = args.exchange == "p2p"
+    if p2p:
+        ex = gd.P2PExchange(arch, rank, world, dist=tdist)
+    else:
+        uid = gd.rendezvous(tdist, rank, gd.nccl_unique_id)
+        comm = gd.Comm(ctx, uid, rank, world)
+        exchange = gd.ALLREDUCE if args.exchange == "allreduce" else gd.REDUCE_BCAST
     t0 = time.time()
     spec = g.data_spec(96 * world, 9500)  # weak scaling: 96 files (182 MB) per worker
     total_rounds = args.warmup + args.steps
@@ -307,10 +314,20 @@ def run_ours_dist(args, rank, world, local):
     x, y = g.generate(spec, plan.first_file, plan.n_files)
     dx, dy = ctx.upload(x), ctx.upload(y)
     di = ctx.upload(plan.idx_local[: total_rounds * B])
+    dc = ctx.upload(np.ascontiguousarray(counts, np.int32))
     setup_s = time.time() - t0
     m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
     loss = ctx.array(total_rounds)
-    gd.dist_sync_rounds(m, comm, exchange, dx, dy, di, B, counts[: args.warmup], args.warmup, loss)
+
+    def rounds(r0, n, loss_offset):
+        if p2p:
+            ex.sync_rounds(m, dx, dy, di, B, 0, dc, B, n, loss_out=loss, idx_offset=r0 * B,
+                           counts_offset=r0 * world, loss_offset=loss_offset)
+        else:
+            gd.dist_sync_rounds(m, comm, exchange, dx, dy, di, B, counts[r0:r0 + n], n,
+                                loss, idx_offset=r0 * B)
+
+    rounds(0, args.warmup, 0)
     ctx.sync()
     tdist.barrier()
     launches0 = ctx.launches
@@ -318,8 +335,7 @@ def run_ours_dist(args, rank, world, local):
         ctx.sync()
         tdist.barrier()
         ctx.timer_start()
-        gd.dist_sync_rounds(m, comm, exchange, dx, dy, di, B, counts[args.warmup:], args.steps,
-                            loss, idx_offset=args.warmup * B)
+        rounds(args.warmup, args.steps, args.warmup)
         ms_local = ctx.timer_stop()
         ctx.sync()
         tdist.barrier()
@@ -329,13 +345,54 @@ def run_ours_dist(args, rank, world, local):
     launches = ctx.launches - launches0
     _, _, version, rejected = m.read()
     losses = loss.numpy() / (B * world)
+    e2e = None
+    if p2p:
+        e2e = run_e2e_dist(args, g, gd, tdist, ctx, arch, ex, x, y, plan, dc, rank, world)
     if rank == 0:
-        line = result_line(args, world, ms, None, 1, None, None, launches, clk.summary(),
+        line = result_line(args, world, ms, None, args.steps, e2e, None, launches, clk.summary(),
                            version, rejected, losses, setup_s, arch.kernel_name, None)
         print(json.dumps(line), flush=True)
     tdist.barrier()
+    if p2p:
+        ex.close()
     tdist.destroy_process_group()
     return 0
+
+
+def run_e2e_dist(args, g, gd, tdist, ctx, arch, ex, x, y, plan, dc, rank, world):
+    """e2e at N GPUs through the public API: every rank streams its K batches
+    from pinned host memory (zero-copy, as run_e2e) through ONE
+    ghc_p2p_sync_rounds call; time = max over ranks."""
+    import torch
+    B = args.batch
+    K = min(args.steps, args.e2e_steps)
+    width = x.shape[1]
+    hx = ctx.host_array((K * B, width))
+    hy = ctx.host_array(K * B, np.int32)
+    hl = ctx.host_array(K)
+    sel = plan.idx_local[: K * B]
+    hx.np[:] = x[sel]
+    hy.np[:] = y[sel]
+    hl.np[:] = np.nan
+    m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+    ctx.sync()
+    tdist.barrier()
+    ctx.timer_start()
+    ex.sync_rounds(m, hx, hy, None, B, 0, dc, B, K, loss_out=hl)
+    ms_local = ctx.timer_stop()
+    ctx.sync()
+    tdist.barrier()
+    t = torch.tensor([ms_local], dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = bool(np.isfinite(hl.np).all())
+    for a in (hx, hy, hl):
+        a.free()
+    return {"value": world * B * K / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": world * B * (width + 1) * 4, "d2h_bytes_per_step": world * 4,
+            "steps": K, "ms_per_step": ms / K, "losses_finite": ok,
+            "path": "per rank: ghc_p2p_sync_rounds over K host batches (pinned, zero-copy "
+                    "prefetch one round ahead, losses stored to host memory); max over ranks"}
 
 
 def run_e2e(args, g, ctx, arch, x, y, idx):
@@ -447,7 +504,7 @@ def main():
     ap.add_argument("--cpu-rounds", type=int, default=120)
     ap.add_argument("--ref-rounds", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--exchange", default="reduce_bcast", choices=["reduce_bcast", "allreduce"])
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "reduce_bcast", "allreduce"])
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes/launch from an ncu --set full capture")
     args = ap.parse_args()

@@ -250,6 +250,38 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
                                 float* d_loss_out);
 
 /* ------------------------------------------------------------------ */
+/* Fused NVLink exchange (replaces, for the sync round, Endpoint         */
+/* GRADIENT/WEIGHTS send/recv transport.hpp:22-44 + the master loop      */
+/* SPEC.md:340-366, and the NCCL reduce/broadcast of ghc_dist_*): the    */
+/* persistent round kernel of every rank pushes its rank-local gradient  */
+/* sub-slices into every rank's receive buffer over peer memory, counts  */
+/* arrivals per column, sums the ranks in rank order and applies         */
+/* sgd_step — each rank holds a bit-identical master replica.            */
+/* ------------------------------------------------------------------ */
+typedef struct ghc_p2p ghc_p2p;
+#define GHC_IPC_HANDLE_BYTES 64
+/* Rank `rank` of an nranks (2..8) exchange over plan's fused kernel (the
+ * same architecture, GPU model and batch size on every rank). */
+ghc_status ghc_p2p_create(ghc_plan* plan, int32_t rank, int32_t nranks, ghc_p2p** out);
+/* All nranks ranks as virtual ranks sharing ONE grid on this GPU (same
+ * kernel code, peer pointers into one allocation): single-GPU testing. */
+ghc_status ghc_p2p_create_virtual(ghc_plan* plan, int32_t nranks, ghc_p2p** out);
+/* This rank's cudaIpc handle (GHC_IPC_HANDLE_BYTES) for the bootstrap. */
+ghc_status ghc_p2p_export(ghc_p2p* p, uint8_t* out_handle);
+/* Map every other rank's buffers: handles = nranks handles in rank order. */
+ghc_status ghc_p2p_import(ghc_p2p* p, const uint8_t* handles);
+void ghc_p2p_destroy(ghc_p2p* p);
+/* n_rounds sync Downpour rounds in ONE persistent launch per rank.  Rank k
+ * (virtual rank k) trains in round r on rows d_idx[k*idx_vstride + r*stride
+ * + s] (rows r*stride + s with d_idx == NULL) for s < d_counts[r*nranks + k]
+ * (d_counts nullable → n_max each); the gradient is the sample-weighted mean
+ * over all ranks.  d_loss_out[r] = loss sum over ranks. */
+ghc_status ghc_p2p_sync_rounds(ghc_master* m, ghc_p2p* p, const float* d_x, const int32_t* d_y,
+                               const int32_t* d_idx, int64_t stride, int64_t idx_vstride,
+                               const int32_t* d_counts, int64_t n_max, int32_t n_rounds,
+                               float* d_loss_out);
+
+/* ------------------------------------------------------------------ */
 /* Data layer, host side, bit-identical to the oracle */
 /* ------------------------------------------------------------------ */
 typedef struct ghc_data_spec {

@@ -115,6 +115,12 @@ SIGNATURES = [
     ("ghc_comm_broadcast", C.c_int, [_vp, _vp, _i64, _i32]),
     ("ghc_comm_allreduce_sum", C.c_int, [_vp, _vp, _vp, _i64]),
     ("ghc_dist_sync_rounds", C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _i32, _vp]),
+    ("ghc_p2p_create", C.c_int, [_vp, _i32, _i32, _vp]),
+    ("ghc_p2p_create_virtual", C.c_int, [_vp, _i32, _vp]),
+    ("ghc_p2p_export", C.c_int, [_vp, _vp]),
+    ("ghc_p2p_import", C.c_int, [_vp, _vp]),
+    ("ghc_p2p_destroy", None, [_vp]),
+    ("ghc_p2p_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
     ("ghc_session_create", C.c_int, [_vp, _vp, _vp, _vp]),
     ("ghc_session_destroy", None, [_vp]),
     ("ghc_session_run", C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64]),

@@ -112,7 +112,9 @@ inline void step_geometry(const ghc_plan* p, int64_t n, int& ctas, int& warps) {
   ctas = static_cast<int>(c);
 }
 
-inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
+// vr > 1: vr virtual ranks share the grid (cross-rank exchange, SIMT kernel),
+// each with max_clusters / vr clusters and n_max samples per round.
+inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 1) {
   if (!p->lstm) return fail(GHC_ERR_CONFIG, "plan has no fused worker kernel");
   a.err = p->err;
   a.probe = p->probe;
@@ -121,14 +123,17 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
     // ≈ one CTA per SM; SIMT variant: one warp per sample, TC variant: the
     // CTA's 8 warps step 8 samples together (kTcSamples per pass)
     const int cs = p->cluster_size;
+    const bool tc = p->use_tc && a.GX <= 1;
+    const int maxc = p->max_clusters / vr;
+    if (maxc < 1) return fail(GHC_ERR_CONFIG, "too many virtual ranks for the co-resident clusters");
     int warps;
     int64_t per_cta;  // samples per CTA in one pass
-    if (p->use_tc) {
+    if (tc) {
       warps = 8;
       per_cta = kTcSamples;
     } else {
       const int spw = kSamplesPerWarp;
-      const int64_t slots = static_cast<int64_t>(p->max_clusters) * cs * spw;
+      const int64_t slots = static_cast<int64_t>(maxc) * cs * spw;
       warps = static_cast<int>((n_max + slots - 1) / slots);
       warps = warps < 1 ? 1 : (warps > p->round_warps ? p->round_warps : warps);
       per_cta = static_cast<int64_t>(warps) * spw;
@@ -136,15 +141,16 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
     int64_t ctas = (n_max + per_cta - 1) / per_cta;
     int64_t nc = (ctas + cs - 1) / cs;
     if (nc < 1) nc = 1;
-    if (nc > p->max_clusters) nc = p->max_clusters;
+    if (nc > maxc) nc = maxc;
+    a.VR = vr;
     a.part = p->part;
     a.pstride = p->lstm->ep[p->cs_index];
     a.pipelined = n_max <= nc * cs * per_cta;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(nc * cs));
+    cfg.gridDim = dim3(static_cast<unsigned>(nc * cs * vr));
     cfg.blockDim = dim3(static_cast<unsigned>(warps * 32));
-    cfg.dynamicSmemBytes = p->use_tc ? p->lstm->smem_tc[p->cs_index](warps)
-                                     : p->lstm->smem_round[p->cs_index](warps);
+    cfg.dynamicSmemBytes = tc ? p->lstm->smem_tc[p->cs_index](warps)
+                              : p->lstm->smem_round[p->cs_index](warps);
     cfg.stream = p->ctx->stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -162,8 +168,7 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max) {
       return e && e[0] == '1';
     }();
     cfg.numAttrs = no_coop ? 1 : 2;
-    CU(cudaLaunchKernelEx(&cfg, p->use_tc ? p->lstm->fn_tc[p->cs_index] : p->lstm->fn_round[p->cs_index],
-                          a));
+    CU(cudaLaunchKernelEx(&cfg, tc ? p->lstm->fn_tc[p->cs_index] : p->lstm->fn_round[p->cs_index], a));
     p->ctx->launches++;
     return GHC_OK;
   }

@@ -66,7 +66,8 @@ struct ClusterXchg {
   float* vtmp;  // [SL]
   int* badv;    // [CS] non-finite flags, written by peers
   int crank, cid, NC, e0, e1;
-  unsigned epoch;
+  int NCr, vrank, rank, cl;  // clusters per rank, this CTA's virtual/global rank, cluster in rank
+  unsigned epoch, xepoch;
   unsigned long long accepted, rejected;
   int last_status;
   bool sgd;
@@ -80,7 +81,13 @@ struct ClusterXchg {
     NC = gridDim.x / CS;
     e0 = crank * SL;
     e1 = min(E, e0 + SL);
+    NCr = NC / max(1, a.VR);
+    vrank = cid / NCr;
+    cl = cid % NCr;
+    rank = a.rank0 + vrank;
     epoch = __ldcg(a.bar);
+    // cross-rank exchange epoch: kept next to this rank's arrival counters
+    xepoch = a.GX > 1 ? __ldcg(a.gcnt[rank] + CS * kFlagStride) : 0u;
     accepted = rejected = 0;
     last_status = 0;
     sgd = a.mode == MODE_SGD;
@@ -91,6 +98,61 @@ struct ClusterXchg {
     for (int p = threadIdx.x; p < P; p += blockDim.x) wbuf[p] = __ldcg(gw + p);
     if (sgd)
       for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) vsl[e - e0] = e < P ? __ldcg(gv + e) : 0.f;
+  }
+
+  // Σ_{i<nrow} rows[i][e..e+3] in row order, kXchgBatch L2 loads in flight.
+  __device__ static float4 sum_rows(const float* rows, int nrow, long long stride, int e) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < nrow; c0 += kXchgBatch) {
+      float4 v[kXchgBatch];
+#pragma unroll
+      for (int i = 0; i < kXchgBatch; ++i)
+        v[i] = c0 + i < nrow ? __ldcg(reinterpret_cast<const float4*>(rows + (c0 + i) * stride + e))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < kXchgBatch; ++i) {
+        t.x += v[i].x;
+        t.y += v[i].y;
+        t.z += v[i].z;
+        t.w += v[i].w;
+      }
+    }
+    return t;
+  }
+
+  // (4x) Cross-rank exchange of slice j (NVLink peer memory, no NCCL):
+  //   a. cluster cl of this rank sums sub-slice cl of slice j over the rank's
+  //      NCr cluster partials (fixed order) and stores it into row `rank` of
+  //      EVERY rank's receive buffer (P2P stores), then bumps every rank's
+  //      arrival counter of column j (release, system scope);
+  //   b. wait until this rank's counter of column j holds all GX·NCr
+  //      sub-slices of this round (acquire).  The caller then sums the GX
+  //      rank rows in rank order — bit-identical on every rank.
+  // Parity-double-buffered receive rows: a rank reaches round r+2's pushes
+  // only after every rank's column-j CTAs have finished reading round r.
+  __device__ void xchg_ranks(const StepArgs& a, int par, const float* gcol) {
+    const int SS = (((SL + NCr - 1) / NCr) + 3) & ~3;
+    const int lo = e0 + cl * SS, hi = min(e1, lo + SS);
+    for (int e = lo + 4 * threadIdx.x; e < hi; e += 4 * blockDim.x) {
+      const float4 t = sum_rows(gcol, NCr, EP, e);
+      for (int q = 0; q < a.GX; ++q)
+        __stcg(reinterpret_cast<float4*>(a.gpart[q] + ((long long)par * a.GX + rank) * EP + e), t);
+    }
+    __threadfence_system();
+    __syncthreads();
+    ++xepoch;
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < a.GX; ++q)
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.gcnt[q] + crank * kFlagStride)
+                     : "memory");
+      const unsigned target = xepoch * (unsigned)(a.GX * NCr);
+      const unsigned* cnt = a.gcnt[rank] + crank * kFlagStride;
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+      } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
   }
 
   __device__ void exchange(const StepArgs& a, cg::cluster_group& cluster, int r, float* cpart,
@@ -111,7 +173,7 @@ struct ClusterXchg {
     __syncthreads();
     unsigned* flags = a.bar + 2 * kFlagStride;
     if (threadIdx.x == 0) st_release_gpu(flags + blockIdx.x * kFlagStride, epoch);
-    for (int c = threadIdx.x; c < NC; c += blockDim.x) {
+    for (int c = vrank * NCr + threadIdx.x; c < (vrank + 1) * NCr; c += blockDim.x) {
       const unsigned* f = flags + (c * CS + crank) * kFlagStride;
       while ((int)(ld_relaxed_gpu(f) - epoch) < 0) {
       }
@@ -122,25 +184,20 @@ struct ClusterXchg {
 
     // ---- (4) slice j over all clusters (fixed order) → update → broadcast ----
     // float4 columns: SL and EP are multiples of 4, e0 too.
+    // One rank: sum the NC cluster partials of slice j (every cluster does
+    // this redundantly — one barrier instead of two).  GX ranks: cross-rank
+    // two-level reduce (4x below), then sum the GX rank partials of slice j.
     int bad = 0;
-    const float* gcol = a.part + (long long)par * NC * EP;
+    const float* gcol = a.part + ((long long)par * NC + vrank * NCr) * EP;
+    int nrow = NCr;
+    long long rstride = EP;
+    if (a.GX > 1) {
+      xchg_ranks(a, par, gcol);
+      gcol = a.gpart[rank] + (long long)par * a.GX * EP;
+      nrow = a.GX;
+    }
     for (int e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
-      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c0 = 0; c0 < NC; c0 += kXchgBatch) {  // loads in flight; fixed-order sum
-        float4 v[kXchgBatch];
-#pragma unroll
-        for (int i = 0; i < kXchgBatch; ++i)
-          v[i] = c0 + i < NC
-                     ? __ldcg(reinterpret_cast<const float4*>(gcol + (long long)(c0 + i) * EP + e))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int i = 0; i < kXchgBatch; ++i) {
-          t.x += v[i].x;
-          t.y += v[i].y;
-          t.z += v[i].z;
-          t.w += v[i].w;
-        }
-      }
+      const float4 t = sum_rows(gcol, nrow, rstride, e);
       const float tv[4] = {t.x, t.y, t.z, t.w};
       float wn[4];
 #pragma unroll
@@ -204,6 +261,8 @@ struct ClusterXchg {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       a.bar[0] = epoch;
+      if (a.GX > 1)
+        for (int v = 0; v < max(1, a.VR); ++v) a.gcnt[a.rank0 + v][CS * kFlagStride] = xepoch;
       if (sgd) {
         a.ms->version += accepted;
         a.ms->rejected += rejected;
@@ -252,13 +311,19 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   // s0 + w + sp*NW.  Pipelined launches (n ≤ slots) prefetch every slot's
   // next-round row during the current round: the index one round ahead, the
   // row after this round's compute (cp.async into the slot's other buffer).
+  // Virtual rank v of the grid owns CTAs [v*Gr, (v+1)*Gr) and its own batch.
+  const int Gr = G / max(1, a.VR);
+  const int lb = blockIdx.x % Gr;
+  const int GX = max(1, a.GX);
+  auto n_of = [&](int r, int q) { return a.counts ? __ldg(a.counts + (long long)r * GX + q) : a.n; };
   auto first_sample = [&](int r, int& s, int& s1) {
-    const int n = a.counts ? __ldg(a.counts + r) : a.n;
-    const int spc = (n + G - 1) / G;
-    const int s0 = blockIdx.x * spc;
+    const int n = n_of(r, xc.rank);
+    const int spc = (n + Gr - 1) / Gr;
+    const int s0 = lb * spc;
     s1 = min(n, s0 + spc);
     s = s0 + warp;
   };
+  const int32_t* idxv = a.idx ? a.idx + (long long)xc.vrank * a.idx_vstride : nullptr;
   auto slot_x = [&](int sp, int b) { return ws + sp * N::WARP_FLOATS + N::S_X + b * N::XWP; };
   auto slot_l = [&](int sp) { return reinterpret_cast<int*>(ws + sp * N::WARP_FLOATS + N::S_L); };
   auto fetch_nocommit = [&](int sp, int row, int b) {
@@ -269,17 +334,17 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   };
   auto row_of = [&](int r, int s) {
     // no gather table: round r reads rows r*stride + s (stride 0: rows s)
-    return a.idx ? __ldg(a.idx + (long long)r * a.stride + s) : (int)((long long)r * a.stride + s);
+    return idxv ? __ldg(idxv + (long long)r * a.stride + s) : (int)((long long)r * a.stride + s);
   };
   // gather indices of round r (pipelined path): one cp.async per slot into
   // slot_l[2], fetched a round before the rows they select
   auto fetch_idx_nocommit = [&](int r) {
-    if (!a.idx || lane != 0 || r >= a.rounds) return;
+    if (!idxv || lane != 0 || r >= a.rounds) return;
     int sx, sx1;
     first_sample(r, sx, sx1);
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp)
-      if (sx + sp * NW < sx1) cp_async4(slot_l(sp) + 2, a.idx + (long long)r * a.stride + sx + sp * NW);
+      if (sx + sp * NW < sx1) cp_async4(slot_l(sp) + 2, idxv + (long long)r * a.stride + sx + sp * NW);
   };
   if (a.pipelined) {
     int s, s1;
@@ -293,8 +358,9 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   __syncthreads();
 
   for (int r = 0; r < a.rounds; ++r) {
-    const int n = a.counts ? __ldg(a.counts + r) : a.n;
-    const float scale = sgd ? 1.0f / (float)n : a.grad_scale;
+    int ntot = 0;  // samples of round r over all ranks (SPEC.md:358-366 weighted mean)
+    for (int q = 0; q < GX; ++q) ntot += n_of(r, q);
+    const float scale = sgd ? 1.0f / (float)ntot : a.grad_scale;
     unsigned long long* pr =
         a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
     if (pr && threadIdx.x == 0) pr[0] = globaltimer();
@@ -322,7 +388,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         int rows[SPW];
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
-          rows[sp] = a.idx ? slot_l(sp)[2] : (int)((long long)(r + 1) * a.stride + sn + sp * NW);
+          rows[sp] = idxv ? slot_l(sp)[2] : (int)((long long)(r + 1) * a.stride + sn + sp * NW);
         __syncwarp();
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)

@@ -32,6 +32,8 @@ enum StepMode : int {
   MODE_TRUNK_GRAD = 4  // LSTM trunk backward from dh_T rows (hio[s][H]): Wx, Wh, b grads
 };
 
+constexpr int kMaxRanks = 8;  // GPUs of one NVLink domain in the fused exchange
+
 struct StepArgs {
   const float* x;         // dataset (or batch) rows, T*D floats each
   const int32_t* y;       // labels
@@ -60,6 +62,16 @@ struct StepArgs {
   unsigned* bar;          // flag barrier: epoch, go, then one 128-B line per CTA
   int pipelined;          // every round has ≤ 1 sample per warp (cp.async prefetch path)
   int mode;
+  // ---- cross-rank exchange (lstm_round.cuh ClusterXchg, GX > 1) ----
+  // GX ranks (one per GPU, or virtual ranks sharing one grid) each train on
+  // their own batch and hold a bit-identical replica of the master.  counts
+  // is then [rounds][GX]; idx of virtual rank v starts at idx + v*idx_vstride.
+  int GX;                 // ranks in the exchange (1: single-GPU round)
+  int VR;                 // virtual ranks in this grid (1 with one process per GPU)
+  int rank0;              // global rank of this grid's first virtual rank
+  long long idx_vstride;
+  float* gpart[kMaxRanks];     // per rank: its receive buffer [2][GX][EP] (peer-mapped)
+  unsigned* gcnt[kMaxRanks];   // per rank: its per-column arrival counters
 };
 
 // Grid barrier for the persistent round loop (gather → broadcast):

@@ -1,0 +1,157 @@
+// p2p.cu — fused NVLink exchange for synchronous Downpour across GPUs.
+//
+// Replaces, for the sync round, the Endpoint GRADIENT/WEIGHTS round trip of
+// the reference (transport.hpp:22-44) AND the NCCL
+// reduce/broadcast pair of dist.cu: every rank runs the persistent round
+// kernel (lstm_round.cuh) on its own batch and holds a bit-identical replica
+// of the master; inside the kernel each cluster pushes its rank-local
+// sub-slice of the gradient straight into every rank's receive buffer (P2P
+// stores over NVLink), bumps per-column arrival counters (release, system
+// scope) and, once a column is complete, sums the ranks' rows in rank order
+// and applies sgd_step — one kernel, no host round trip, no collective call.
+//
+// Buffers: per rank one cudaMalloc holding gpart[2][GX][EP] (parity double
+// buffer) and CS+1 counter lines (one per column, the last keeps the
+// exchange epoch across launches).  Ranks exchange cudaIpc handles through
+// the caller (bytes over torch.distributed / any bootstrap); a "virtual"
+// exchange puts all GX ranks into ONE grid on one GPU (same kernel code, peer
+// pointers into one allocation) — how the path is tested on a single GPU.
+#include "ghc_internal.cuh"
+
+struct ghc_p2p {
+  ghc_plan* plan = nullptr;
+  int rank = 0, G = 1;
+  bool virt = false;
+  int ep = 0;
+  size_t rank_bytes = 0;
+  void* own = nullptr;                 // this process's allocation
+  void* opened[kMaxRanks] = {};        // IPC-opened peer allocations
+  float* gpart[kMaxRanks] = {};
+  unsigned* gcnt[kMaxRanks] = {};
+};
+
+namespace {
+
+size_t gpart_bytes(int G, int ep) { return ((sizeof(float) * 2 * G * ep) + 255) & ~size_t(255); }
+size_t cnt_bytes(int cs) { return sizeof(unsigned) * kFlagStride * (cs + 1); }
+
+ghc_status p2p_new(ghc_plan* plan, int rank, int G, bool virt, ghc_p2p** out) {
+  if (!out) return fail(GHC_ERR_CONFIG, "p2p: null out");
+  *out = nullptr;
+  if (!plan || plan->layered || !plan->lstm || !plan->use_cluster || plan->max_clusters < 1)
+    return fail(GHC_ERR_CONFIG, "p2p exchange needs the fused LSTM round kernel (cluster variant)");
+  if (G < 2 || G > kMaxRanks) return fail(GHC_ERR_CONFIG, "p2p: nranks must be in [2, 8]");
+  if (rank < 0 || rank >= G) return fail(GHC_ERR_CONFIG, "p2p: rank out of range");
+  if (virt && plan->max_clusters / G < 1)
+    return fail(GHC_ERR_CONFIG, "p2p: not enough co-resident clusters for the virtual ranks");
+  auto* p = new ghc_p2p;
+  p->plan = plan;
+  p->rank = rank;
+  p->G = G;
+  p->virt = virt;
+  p->ep = plan->lstm->ep[plan->cs_index];
+  p->rank_bytes = gpart_bytes(G, p->ep) + cnt_bytes(plan->cluster_size);
+  CU(cudaSetDevice(plan->ctx->device));
+  const size_t total = p->rank_bytes * (virt ? G : 1);
+  CU(cudaMalloc(&p->own, total));
+  CU(cudaMemset(p->own, 0, total));
+  auto bind = [&](int q, char* base) {
+    p->gpart[q] = reinterpret_cast<float*>(base);
+    p->gcnt[q] = reinterpret_cast<unsigned*>(base + gpart_bytes(G, p->ep));
+  };
+  if (virt)
+    for (int q = 0; q < G; ++q) bind(q, static_cast<char*>(p->own) + q * p->rank_bytes);
+  else
+    bind(rank, static_cast<char*>(p->own));
+  *out = p;
+  return GHC_OK;
+}
+
+}  // namespace
+
+ghc_status ghc_p2p_create(ghc_plan* plan, int32_t rank, int32_t nranks, ghc_p2p** out) {
+  return p2p_new(plan, rank, nranks, false, out);
+}
+
+ghc_status ghc_p2p_create_virtual(ghc_plan* plan, int32_t nranks, ghc_p2p** out) {
+  return p2p_new(plan, 0, nranks, true, out);
+}
+
+ghc_status ghc_p2p_export(ghc_p2p* p, uint8_t* out_handle) {
+  if (!p || !out_handle) return fail(GHC_ERR_CONFIG, "p2p_export: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == GHC_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CU(cudaSetDevice(p->plan->ctx->device));
+  CU(cudaIpcGetMemHandle(&h, p->own));
+  std::memcpy(out_handle, &h, sizeof(h));
+  return GHC_OK;
+}
+
+ghc_status ghc_p2p_import(ghc_p2p* p, const uint8_t* handles) {
+  if (!p || !handles) return fail(GHC_ERR_CONFIG, "p2p_import: null argument");
+  if (p->virt) return GHC_OK;
+  CU(cudaSetDevice(p->plan->ctx->device));
+  for (int q = 0; q < p->G; ++q) {
+    if (q == p->rank) continue;
+    if (p->opened[q]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + static_cast<size_t>(q) * GHC_IPC_HANDLE_BYTES, sizeof(h));
+    void* base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(GHC_ERR_TRANSPORT, "p2p_import: cannot map rank " + std::to_string(q) +
+                                         "'s buffer (no peer access between these GPUs?)");
+    }
+    p->opened[q] = base;
+    p->gpart[q] = static_cast<float*>(base);
+    p->gcnt[q] = reinterpret_cast<unsigned*>(static_cast<char*>(base) + gpart_bytes(p->G, p->ep));
+  }
+  return GHC_OK;
+}
+
+void ghc_p2p_destroy(ghc_p2p* p) {
+  if (!p) return;
+  cudaSetDevice(p->plan->ctx->device);
+  cudaStreamSynchronize(p->plan->ctx->stream);
+  for (int q = 0; q < kMaxRanks; ++q)
+    if (p->opened[q]) cudaIpcCloseMemHandle(p->opened[q]);
+  cudaFree(p->own);
+  delete p;
+}
+
+ghc_status ghc_p2p_sync_rounds(ghc_master* m, ghc_p2p* p, const float* d_x, const int32_t* d_y,
+                               const int32_t* d_idx, int64_t stride, int64_t idx_vstride,
+                               const int32_t* d_counts, int64_t n_max, int32_t n_rounds,
+                               float* d_loss_out) {
+  if (!m || !p) return fail(GHC_ERR_CONFIG, "p2p_sync_rounds: null handle");
+  if (m->plan != p->plan) return fail(GHC_ERR_CONFIG, "p2p_sync_rounds: master and exchange use different plans");
+  if (n_max < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");
+  if (n_rounds < 1) return GHC_OK;
+  for (int q = 0; q < p->G; ++q)
+    if (!p->gpart[q]) return fail(GHC_ERR_TRANSPORT, "p2p_sync_rounds: peers not imported");
+  StepArgs a{};
+  a.x = d_x;
+  a.y = d_y;
+  a.idx = d_idx;
+  a.stride = stride;
+  a.counts = d_counts;
+  a.n = static_cast<int>(n_max);
+  a.rounds = n_rounds;
+  a.w0 = m->w[0];
+  a.w1 = m->w[1];
+  a.v0 = m->v[0];
+  a.v1 = m->v[1];
+  a.lr = m->lr;
+  a.mu = m->mu;
+  a.ms = m->ms;
+  a.loss_out = d_loss_out;
+  a.mode = MODE_SGD;
+  a.GX = p->G;
+  a.rank0 = p->virt ? 0 : p->rank;
+  a.idx_vstride = idx_vstride;
+  for (int q = 0; q < p->G; ++q) {
+    a.gpart[q] = p->gpart[q];
+    a.gcnt[q] = p->gcnt[q];
+  }
+  return launch_step(m->plan, a, n_max, p->virt ? p->G : 1);
+}

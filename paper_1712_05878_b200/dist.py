@@ -12,7 +12,12 @@ torchrun and this module does the host-side parts of the new "nvlink" backend:
   sample-weighted mean needs no extra exchange (ghc_dist_sync_rounds);
 * `rendezvous` — moves the 128-byte NCCL unique id from rank 0 to every rank
   through torch.distributed (plumbing only; the exchange itself is NCCL over
-  NVLink inside libghc).
+  NVLink inside libghc);
+* `P2PExchange` — the fused NVLink exchange (p2p.cu): every rank's cudaIpc
+  handle is all-gathered through torch.distributed (`allgather_bytes`), then
+  the persistent round kernels of all ranks reduce the gradient through peer
+  memory themselves (no NCCL call per round).  `virtual=True` runs all ranks
+  in one grid on one GPU (same kernel code) — the single-GPU test of the path.
 
 Everything here is pure host logic and is covered by world-size-2 gloo tests on
 CPU (tests/test_dist_cpu.py).
@@ -122,3 +127,55 @@ def dist_sync_rounds(master: g.Master, comm: Comm, exchange: int, x, y, idx, str
         master.h, comm.h, exchange, x.ptr, y.ptr, idx.offset(idx_offset), stride,
         C.c_void_p(counts.ctypes.data), rounds,
         loss_out.ptr if loss_out is not None else None), "dist_sync_rounds")
+
+
+def allgather_bytes(dist, payload: bytes) -> list:
+    """Every rank's payload, in rank order, on every rank (torch.distributed)."""
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, payload)
+    return out
+
+
+class P2PExchange:
+    """ghc_p2p: fused NVLink exchange of the sync round (p2p.cu)."""
+
+    HANDLE_BYTES = 64
+
+    def __init__(self, arch: g.Architecture, rank: int, world: int, dist=None,
+                 virtual: bool = False):
+        self.ctx = arch.ctx
+        self.world = world
+        lib = self.ctx.lib
+        h = C.c_void_p()
+        if virtual:
+            g.check(lib.ghc_p2p_create_virtual(arch.h, world, C.byref(h)), "p2p_create_virtual")
+        else:
+            g.check(lib.ghc_p2p_create(arch.h, rank, world, C.byref(h)), "p2p_create")
+        self.h = h
+        if not virtual:
+            mine = (C.c_uint8 * self.HANDLE_BYTES)()
+            g.check(lib.ghc_p2p_export(h, mine), "p2p_export")
+            allh = allgather_bytes(dist, bytes(mine))
+            buf = (C.c_uint8 * (self.HANDLE_BYTES * world)).from_buffer_copy(b"".join(allh))
+            g.check(lib.ghc_p2p_import(h, buf), "p2p_import")
+
+    def sync_rounds(self, master: g.Master, x, y, idx, stride: int, idx_vstride: int, counts,
+                    n_max: int, rounds: int, loss_out=None, idx_offset: int = 0,
+                    counts_offset: int = 0, loss_offset: int = 0):
+        """ghc_p2p_sync_rounds; counts: device int32 [rounds][world] or None."""
+        g.check(self.ctx.lib.ghc_p2p_sync_rounds(
+            master.h, self.h, x.ptr, y.ptr, idx.offset(idx_offset) if idx is not None else None,
+            stride, idx_vstride, counts.offset(counts_offset) if counts is not None else None,
+            n_max, rounds, loss_out.offset(loss_offset) if loss_out is not None else None),
+            "p2p_sync_rounds")
+
+    def close(self):
+        if self.h is not None and self.ctx.h and not g._SHUTDOWN[0]:
+            self.ctx.lib.ghc_p2p_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

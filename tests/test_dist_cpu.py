@@ -42,6 +42,9 @@ def _worker(rank, world, port, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     uid = gd.rendezvous(dist, rank, lambda: bytes(range(128)))
     assert uid == bytes(range(128))
+    # P2PExchange bootstrap: every rank's 64-byte IPC handle, in rank order
+    hs = gd.allgather_bytes(dist, bytes([rank + 1]) * gd.P2PExchange.HANDLE_BYTES)
+    assert hs == [bytes([q + 1]) * 64 for q in range(world)]
 
     B, epochs, seed = 70, 1, 99
     spec = g.data_spec(6, 110)
