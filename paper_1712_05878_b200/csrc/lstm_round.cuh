@@ -120,39 +120,72 @@ struct ClusterXchg {
     return t;
   }
 
-  // (4x) Cross-rank exchange of slice j (NVLink peer memory, no NCCL):
-  //   a. cluster cl of this rank sums sub-slice cl of slice j over the rank's
-  //      NCr cluster partials (fixed order) and stores it into row `rank` of
-  //      EVERY rank's receive buffer (P2P stores), then bumps every rank's
-  //      arrival counter of column j (release, system scope);
-  //   b. wait until this rank's counter of column j holds all GX·NCr
-  //      sub-slices of this round (acquire).  The caller then sums the GX
-  //      rank rows in rank order — bit-identical on every rank.
-  // Parity-double-buffered receive rows: a rank reaches round r+2's pushes
-  // only after every rank's column-j CTAs have finished reading round r.
-  __device__ void xchg_ranks(const StepArgs& a, int par, const float* gcol) {
+  // (4x) Cross-rank exchange of slice j over NVLink peer memory, "LL" style
+  // (as NCCL's low-latency protocol): every value travels with the exchange
+  // epoch in ONE 8-byte store, so a reader that sees the epoch sees the
+  // value — no fences, no counters (a system-scope fence costs ~8 µs/round,
+  // measured).  Receive buffer per rank: uint2 [2 parity][GX][EP].
+  //   push: cluster cl of this rank sums sub-slice cl of slice j over the
+  //         rank's NCr cluster partials (fixed order) and stores it, tagged,
+  //         into row `rank` of EVERY rank's receive buffer;
+  //   sum:  every CTA of column j polls the GX rows of slice j in its own
+  //         receive buffer until all tags equal this epoch and adds them in
+  //         rank order — bit-identical on every rank.
+  // Parity double buffer: a rank pushes round r+2 only after every rank's
+  // column-j CTAs pushed round r+1, i.e. after they finished reading round r.
+  // (value, tag) as ONE 64-bit element: single-copy atomic in the PTX model
+  // (a v2.b32 vector access is only atomic per 32-bit element)
+  __device__ static void st_tagged(uint2* p, float v, unsigned tag) {
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+  }
+  __device__ static uint2 ld_tagged(const uint2* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return make_uint2((unsigned)w, (unsigned)(w >> 32));
+  }
+  __device__ void xchg_push(const StepArgs& a, int par, const float* gcol) {
+    ++xepoch;
     const int SS = (((SL + NCr - 1) / NCr) + 3) & ~3;
     const int lo = e0 + cl * SS, hi = min(e1, lo + SS);
     for (int e = lo + 4 * threadIdx.x; e < hi; e += 4 * blockDim.x) {
       const float4 t = sum_rows(gcol, NCr, EP, e);
-      for (int q = 0; q < a.GX; ++q)
-        __stcg(reinterpret_cast<float4*>(a.gpart[q] + ((long long)par * a.GX + rank) * EP + e), t);
+      for (int q = 0; q < a.GX; ++q) {
+        uint2* dst = reinterpret_cast<uint2*>(a.gpart[q]) + ((long long)par * a.GX + rank) * EP + e;
+        st_tagged(dst + 0, t.x, xepoch);
+        st_tagged(dst + 1, t.y, xepoch);
+        st_tagged(dst + 2, t.z, xepoch);
+        st_tagged(dst + 3, t.w, xepoch);
+      }
     }
-    __threadfence_system();
-    __syncthreads();
-    ++xepoch;
-    if (threadIdx.x == 0) {
-      for (int q = 0; q < a.GX; ++q)
-        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.gcnt[q] + crank * kFlagStride)
-                     : "memory");
-      const unsigned target = xepoch * (unsigned)(a.GX * NCr);
-      const unsigned* cnt = a.gcnt[rank] + crank * kFlagStride;
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-      } while ((int)(v - target) < 0);
+  }
+  // Σ_q row q of this rank's receive buffer at columns e..e+3, rank order.
+  __device__ float4 xchg_sum(const StepArgs& a, int par, int e) const {
+    const uint2* base = reinterpret_cast<const uint2*>(a.gpart[rank]) + (long long)par * a.GX * EP + e;
+    uint2 v[kMaxRanks][4];
+    bool ready;
+    do {
+      ready = true;
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q) {
+        if (q >= a.GX) break;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[q][i] = ld_tagged(base + (long long)q * EP + i);
+          ready &= v[q][i].y == xepoch;
+        }
+      }
+    } while (!ready);
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q) {
+      if (q >= a.GX) break;
+      t.x += __uint_as_float(v[q][0].x);
+      t.y += __uint_as_float(v[q][1].x);
+      t.z += __uint_as_float(v[q][2].x);
+      t.w += __uint_as_float(v[q][3].x);
     }
-    __syncthreads();
+    return t;
   }
 
   __device__ void exchange(const StepArgs& a, cg::cluster_group& cluster, int r, float* cpart,
@@ -189,15 +222,12 @@ struct ClusterXchg {
     // two-level reduce (4x below), then sum the GX rank partials of slice j.
     int bad = 0;
     const float* gcol = a.part + ((long long)par * NC + vrank * NCr) * EP;
-    int nrow = NCr;
-    long long rstride = EP;
     if (a.GX > 1) {
-      xchg_ranks(a, par, gcol);
-      gcol = a.gpart[rank] + (long long)par * a.GX * EP;
-      nrow = a.GX;
+      xchg_push(a, par, gcol);
+      if (pr && threadIdx.x == 0) pr[14] = pr[15] = globaltimer();
     }
     for (int e = e0 + 4 * threadIdx.x; e < e1; e += 4 * blockDim.x) {
-      const float4 t = sum_rows(gcol, nrow, rstride, e);
+      const float4 t = a.GX > 1 ? xchg_sum(a, par, e) : sum_rows(gcol, NCr, EP, e);
       const float tv[4] = {t.x, t.y, t.z, t.w};
       float wn[4];
 #pragma unroll

@@ -70,8 +70,8 @@ struct StepArgs {
   int VR;                 // virtual ranks in this grid (1 with one process per GPU)
   int rank0;              // global rank of this grid's first virtual rank
   long long idx_vstride;
-  float* gpart[kMaxRanks];     // per rank: its receive buffer [2][GX][EP] (peer-mapped)
-  unsigned* gcnt[kMaxRanks];   // per rank: its per-column arrival counters
+  float* gpart[kMaxRanks];     // per rank: tagged receive rows uint2[2][GX][EP] (peer-mapped)
+  unsigned* gcnt[kMaxRanks];   // per rank: line [CS*kFlagStride] keeps the exchange epoch
 };
 
 // Grid barrier for the persistent round loop (gather → broadcast):

@@ -6,13 +6,14 @@
 // kernel (lstm_round.cuh) on its own batch and holds a bit-identical replica
 // of the master; inside the kernel each cluster pushes its rank-local
 // sub-slice of the gradient straight into every rank's receive buffer (P2P
-// stores over NVLink), bumps per-column arrival counters (release, system
-// scope) and, once a column is complete, sums the ranks' rows in rank order
-// and applies sgd_step — one kernel, no host round trip, no collective call.
+// stores over NVLink), each value tagged with the exchange epoch in the same
+// 8-byte store (no fences, no counters), and every CTA sums the ranks' rows
+// of its slice in rank order once the tags match, then applies sgd_step —
+// one kernel, no host round trip, no collective call.
 //
-// Buffers: per rank one cudaMalloc holding gpart[2][GX][EP] (parity double
-// buffer) and CS+1 counter lines (one per column, the last keeps the
-// exchange epoch across launches).  Ranks exchange cudaIpc handles through
+// Buffers: per rank one cudaMalloc holding the tagged receive rows
+// uint2[2][GX][EP] (parity double buffer) and a line that keeps the exchange
+// epoch across launches.  Ranks exchange cudaIpc handles through
 // the caller (bytes over torch.distributed / any bootstrap); a "virtual"
 // exchange puts all GX ranks into ONE grid on one GPU (same kernel code, peer
 // pointers into one allocation) — how the path is tested on a single GPU.
@@ -32,7 +33,8 @@ struct ghc_p2p {
 
 namespace {
 
-size_t gpart_bytes(int G, int ep) { return ((sizeof(float) * 2 * G * ep) + 255) & ~size_t(255); }
+// receive rows are epoch-tagged values (uint2 per element, see ClusterXchg)
+size_t gpart_bytes(int G, int ep) { return ((sizeof(uint2) * 2 * G * ep) + 255) & ~size_t(255); }
 size_t cnt_bytes(int cs) { return sizeof(unsigned) * kFlagStride * (cs + 1); }
 
 ghc_status p2p_new(ghc_plan* plan, int rank, int G, bool virt, ghc_p2p** out) {

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1000)
     ap.add_argument("--arch", default="lstm(5,20,10),softmax(20,3)")
     ap.add_argument("--barriers", action="store_true", help="grid-barrier micro-benchmark")
+    ap.add_argument("--p2p", type=int, default=1,
+                    help="G > 1: fused cross-rank exchange with G virtual ranks (batch per rank)")
     args = ap.parse_args()
     ctx = g.Context(0)
     if args.barriers:
@@ -45,16 +47,32 @@ def main():
     idx = np.concatenate(g.batches(spec, 1, 0, B, 3, 99)[:R]).astype(np.int32)
     dx, dy, di = ctx.upload(x), ctx.upload(y), ctx.upload(idx)
     m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
-    m.sync_rounds(dx, dy, di, B, B, 5)
+    G = args.p2p
+    if G > 1:
+        from . import dist as gd
+        ex = gd.P2PExchange(arch, 0, G, virtual=True)
+        idx = np.concatenate([idx] * G)
+        di = ctx.upload(idx)
+        dc = ctx.upload(np.full((R, G), B, np.int32))
+        run = lambda n: ex.sync_rounds(m, dx, dy, di, B, R * B, dc, B, n)  # noqa: E731
+    else:
+        run = lambda n: m.sync_rounds(dx, dy, di, B, B, n)  # noqa: E731
+    run(5)
     maxc = int(ctx.lib.ghc_plan_max_clusters(arch.h))
     cs = int(ctx.lib.ghc_plan_cluster_size(arch.h))
     if maxc > 0:  # = launch_step() in ghc_internal.cuh (cluster variant)
         spw = int(os.environ.get("GHC_SPW_DIAG", "1"))
-        warps = min(8, max(1, -(-B // (maxc * cs * spw))))
-        ctas = min(maxc, -(-(-(-B // (warps * spw))) // cs)) * cs
+        mc = maxc // G
+        warps = min(8, max(1, -(-B // (mc * cs * spw))))
+        ctas = min(mc, -(-(-(-B // (warps * spw))) // cs)) * cs * G
         bounds = [(0, 2, "samples"), (2, 3, "cta_partial"), (3, 4, "cluster_sync1"),
-                  (4, 5, "dsmem_reduce_store"), (5, 6, "column_barrier"),
-                  (6, 7, "global_reduce_sgd_bcast"), (7, 13, "cluster_sync2")]
+                  (4, 5, "dsmem_reduce_store"), (5, 6, "column_barrier")]
+        if G > 1:
+            bounds += [(6, 14, "x_subslice_reduce_push"), (14, 15, "x_arrival_wait"),
+                       (15, 7, "rank_sum_sgd_bcast")]
+        else:
+            bounds += [(6, 7, "global_reduce_sgd_bcast")]
+        bounds += [(7, 13, "cluster_sync2")]
         last = 13
     else:          # = step_geometry()
         sms = ctx.num_sms
@@ -67,7 +85,7 @@ def main():
     probe.zero()
     ctx.lib.ghc_plan_set_probe(arch.h, probe.ptr)
     ctx.timer_start()
-    m.sync_rounds(dx, dy, di, B, B, R)
+    run(R)
     ms = ctx.timer_stop()
     ctx.lib.ghc_plan_set_probe(arch.h, None)
     pr = probe.numpy().reshape(R, ctas, 16).astype(np.int64)
