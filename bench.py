@@ -238,6 +238,16 @@ def run_ours(args):
     return 0
 
 
+# ncu --set full of one 200-round launch of lstm_round_kernel<5,20,10,3,4>
+# (profiles/r01_ncu_full_round_final_raw.csv): dram__bytes_read.sum 63.39 MB +
+# dram__bytes_write.sum 1.24 MB → per round.  Algorithmic: the gathered batch,
+# 1000 × (50 + 1) × 4 B = 204 KB; the excess is 32-B sector granularity on the
+# unaligned 200-B rows and 4-B labels.
+TRAFFIC_PER_ROUND = (63.392512e6 + 1.235456e6) / 200
+TRAFFIC_SOURCE = ("ncu --set full, 200-round launch (profiles/r01_ncu_full_round_final_raw.csv): "
+                  "dram read+write / 200; traffic = per round × timed rounds")
+
+
 def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks, version,
                 rejected, losses, setup_s, kernel, cpu):
     pk, pk_kind = peaks()
@@ -265,7 +275,10 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
         "roofline": {"bound": "tensor", "achieved": achieved_tflops / world * world,
                      "peak": tensor_peak * world, "unit": "TFLOP/s",
                      "frac": achieved_tflops / (tensor_peak * world),
-                     "traffic": args.traffic,
+                     "traffic": args.traffic * args.steps if args.traffic else None,
+                     "traffic_per_round_bytes": args.traffic,
+                     "algorithmic_bytes_per_round": B * (10 * 5 + 1) * 4,
+                     "traffic_source": TRAFFIC_SOURCE,
                      "kernel": kernel + " (fused fwd+bwd+reduce+SGD)",
                      "peak_kind": f"{pk_kind} bf16 sustained / 2 (TF32) per GPU",
                      "fp32_core": {"peak": fp32_peak * world,
@@ -505,8 +518,8 @@ def main():
     ap.add_argument("--ref-rounds", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "reduce_bcast", "allreduce"])
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes/launch from an ncu --set full capture")
+    ap.add_argument("--traffic", type=float, default=TRAFFIC_PER_ROUND,
+                    help="dram bytes per round of the fused kernel from an ncu --set full capture")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
