@@ -308,6 +308,13 @@ ghc_status ghc_data_epoch_indices(const ghc_data_spec* spec, int32_t n_workers,
                                   int32_t worker, int32_t epoch, uint64_t shuffle_seed,
                                   int32_t shuffle, int64_t* h_out, int64_t* count);
 
+/* validate: the master's serial held-out evaluation —
+ * one fused forward over the n held-out samples, then *h_correct = samples
+ * whose argmax_k p_k (lowest k on ties) equals the label and *h_loss_mean =
+ * mean -ln p_y.  Synchronous.  n < 1 → GHC_ERR_CONFIG. */
+ghc_status ghc_validate(ghc_plan* plan, const float* d_w, const float* d_x, const int32_t* d_y,
+                        int64_t n, int64_t* h_correct, double* h_loss_mean);
+
 /* ------------------------------------------------------------------ */
 /* Roles: a training session of W workers on this     */
 /* device ("virtual workers"), the C++ master/worker loops over the     */
@@ -355,6 +362,16 @@ ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_ord
  * stats = {version, rejected, samples absorbed, rounds/steps}. */
 ghc_status ghc_session_read(ghc_session* s, float* h_w, float* h_v, float* h_worker_w,
                             float* h_group_w, uint64_t* stats);
+/* Held-out set of the master's serial validation:
+ * validate every `every` master updates (0 = only at the end) and once at
+ * the end of every ghc_session_run (no duplicate if the cadence already
+ * validated that version).  Hierarchical sessions validate at the end. */
+ghc_status ghc_session_set_validation(ghc_session* s, const float* h_x, const int32_t* h_y,
+                                      int64_t n, int32_t every);
+/* VALIDATE_RESULT records so far: *count = total; the first min(cap, total)
+ * are written (version, accuracy = correct / n, mean loss). */
+ghc_status ghc_session_validations(ghc_session* s, int64_t cap, uint64_t* versions,
+                                   double* accuracy, double* loss, int64_t* count);
 
 #ifdef __cplusplus
 }

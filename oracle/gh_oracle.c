@@ -606,6 +606,29 @@ int gho_forward_backward(const gho_arch* a, const double* w, const double* x,
 }
 
 /* nn.cpp:407-426 */
+/* validate — SPEC.md:376-384 (no reference code: the roles are SPEC-only). */
+int gho_validate(const gho_arch* a, const double* w, const double* x, const int32_t* y,
+                 int64_t n, int64_t* correct, double* loss_mean) {
+  if (n < 1) return GHO_CONFIG;
+  const int32_t K = gho_arch_n_classes(a);
+  double* probs = (double*)malloc(sizeof(double) * (size_t)n * (size_t)K);
+  if (!probs) return GHO_CONFIG;
+  int rc = gho_forward_backward(a, w, x, y, n, NULL, probs, loss_mean);
+  if (rc == GHO_OK) {
+    int64_t ok = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double* p = probs + i * K;
+      int32_t best = 0;
+      for (int32_t k = 1; k < K; ++k)
+        if (p[k] > p[best]) best = k;  /* strict: ties keep the lowest index */
+      ok += best == y[i];
+    }
+    *correct = ok;
+  }
+  free(probs);
+  return rc;
+}
+
 int gho_finite_diff(const gho_arch* a, const double* w, const double* x,
                     const int32_t* y, int64_t n, double eps, double* grad) {
   if (!(eps > 0.0)) return GHO_CONFIG;

@@ -83,6 +83,12 @@ void gho_init_weights(const gho_arch* a, uint64_t seed, double* w);
 int gho_forward_backward(const gho_arch* a, const double* w, const double* x,
                          const int32_t* y, int64_t n, double* grad,
                          double* probs, double* loss_out);
+/* validate (SPEC-only): forward over a held-out set;
+ * *correct = samples whose argmax_k p_k (lowest k on ties, the
+ * std::max_element convention) equals the label, *loss_mean = mean -ln p_y.
+ * n < 1 → GHO_CONFIG ("empty held-out set → configuration error"). */
+int gho_validate(const gho_arch* a, const double* w, const double* x, const int32_t* y,
+                 int64_t n, int64_t* correct, double* loss_mean);
 /* finite_diff_gradient (nn.cpp:407-426). */
 int gho_finite_diff(const gho_arch* a, const double* w, const double* x,
                     const int32_t* y, int64_t n, double eps, double* grad);

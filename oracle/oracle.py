@@ -183,6 +183,19 @@ def forward_backward(arch: Arch, w, x, y, want_grad=True):
     return g, probs, lo.value
 
 
+def validate(arch: Arch, w, x, y):
+    """gho_validate: (correct count, mean loss) over a held-out set."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.int32)
+    ok = C.c_int64(0)
+    lo = C.c_double(0.0)
+    rc = lib().gho_validate(C.byref(arch), _p(np.ascontiguousarray(w, np.float64)), _p(x),
+                            _p(y, C.c_int32), C.c_int64(len(y)), C.byref(ok), C.byref(lo))
+    if rc != OK:
+        raise RuntimeError(f"gho_validate status {rc}")
+    return ok.value, lo.value
+
+
 def finite_diff(arch: Arch, w, x, y, eps=1e-5):
     g = np.zeros(n_params(arch), np.float64)
     rc = lib().gho_finite_diff(C.byref(arch), _p(np.ascontiguousarray(w, np.float64)),

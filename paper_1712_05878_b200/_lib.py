@@ -124,6 +124,9 @@ SIGNATURES = [
     ("ghc_session_create", C.c_int, [_vp, _vp, _vp, _vp]),
     ("ghc_session_destroy", None, [_vp]),
     ("ghc_session_run", C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64]),
+    ("ghc_session_set_validation", C.c_int, [_vp, _vp, _vp, _i64, _i32]),
+    ("ghc_session_validations", C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
+    ("ghc_validate", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     ("ghc_session_read", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("ghc_data_generate", C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     ("ghc_data_shard", C.c_int, [_i32, _i32, _i32, _vp, _vp]),

@@ -458,6 +458,57 @@ ghc_status ghc_forward(ghc_plan* p, const float* d_w, const float* d_x, const in
   return launch_step(p, a, n);
 }
 
+// ---------------------------------------------------------------- validate
+// argmax_k probs (lowest k on ties) == label, counted exactly (integer atomics
+// are order-independent, so the count is deterministic).
+static __global__ void argmax_correct_kernel(const float* __restrict__ probs,
+                                             const int32_t* __restrict__ y, long long n, int K,
+                                             unsigned long long* correct) {
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float* p = probs + i * K;
+    int best = 0;
+    for (int k = 1; k < K; ++k)
+      if (p[k] > p[best]) best = k;
+    c += best == __ldg(y + i);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(correct, c);
+}
+
+ghc_status ghc_validate(ghc_plan* p, const float* d_w, const float* d_x, const int32_t* d_y,
+                        int64_t n, int64_t* h_correct, double* h_loss_mean) {
+  // "empty held-out set → configuration error"
+  if (n < 1) return fail(GHC_ERR_CONFIG, "validate: empty held-out set");
+  ghc_ctx* c = p->ctx;
+  const int K = p->model.n_classes;
+  char* ws = nullptr;
+  const size_t pb = (sizeof(float) * static_cast<size_t>(n) * K + 255) & ~size_t(255);
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&ws), pb + 256, c->stream));
+  float* probs = reinterpret_cast<float*>(ws);
+  float* loss = reinterpret_cast<float*>(ws + pb);
+  auto* cnt = reinterpret_cast<unsigned long long*>(ws + pb + 128);
+  CU(cudaMemsetAsync(ws + pb, 0, 256, c->stream));
+  ghc_status st = ghc_forward(p, d_w, d_x, d_y, nullptr, n, probs, loss);
+  if (st == GHC_OK) {
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4L * c->num_sms));
+    argmax_correct_kernel<<<grid, 256, 0, c->stream>>>(probs, d_y, n, K, cnt);
+    c->launches++;
+    CU(cudaGetLastError());
+    float lsum = 0.0f;
+    unsigned long long ok = 0;
+    CU(cudaMemcpyAsync(&lsum, loss, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(&ok, cnt, sizeof(ok), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (h_correct) *h_correct = static_cast<int64_t>(ok);
+    if (h_loss_mean) *h_loss_mean = static_cast<double>(lsum) / static_cast<double>(n);
+  }
+  CU(cudaFreeAsync(ws, c->stream));
+  return st;
+}
+
 // ---------------------------------------------------------------- algo
 static ghc_status validate_sgd(float lr, float mu) {  // optim.cpp:20-29
   if (!(lr > 0.0f)) return fail(GHC_ERR_CONFIG, "learning_rate must be > 0");

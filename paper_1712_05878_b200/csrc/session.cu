@@ -99,6 +99,16 @@ struct ghc_session {
   // accounting
   int64_t updates = 0, samples = 0, rounds = 0;
   int64_t trace_cap = 0;  // entries of the caller's loss / staleness buffers
+  // the master's serial validation
+  float* Xv = nullptr;
+  int32_t* Yv = nullptr;
+  int64_t nv = 0;
+  int32_t v_every = 0;
+  struct VRec {
+    uint64_t version;
+    double accuracy, loss;
+  };
+  std::vector<VRec> vrec;
 };
 
 namespace {
@@ -177,6 +187,29 @@ ghc_status apply_master(ghc_session* s, ghc_master* m, const float* g, float lr,
   return coop(c, reinterpret_cast<const void*>(sgd_apply_kernel), args);
 }
 
+// VALIDATE_RESULT of the current master weights (EASGD: the center), appended
+// to the run log; a second request at the same version is not repeated.
+ghc_status validate_now(ghc_session* s) {
+  if (s->nv < 1) return GHC_OK;
+  const float* w = nullptr;
+  uint64_t version = 0;
+  if (s->cfg.algo == GHC_ALGO_EASGD && s->cfg.groups == 0) {
+    w = s->center;
+    CU(cudaMemcpy(&version, s->cver, sizeof(version), cudaMemcpyDeviceToHost));
+  } else {
+    float* dw = nullptr;
+    if (ghc_status st = ghc_master_weights(s->master, &dw, nullptr)) return st;
+    w = dw;
+    CU(cudaMemcpy(&version, &s->master->ms->version, sizeof(version), cudaMemcpyDeviceToHost));
+  }
+  if (!s->vrec.empty() && s->vrec.back().version == version) return GHC_OK;
+  int64_t correct = 0;
+  double loss = 0.0;
+  if (ghc_status st = ghc_validate(s->plan, w, s->Xv, s->Yv, s->nv, &correct, &loss)) return st;
+  s->vrec.push_back({version, static_cast<double>(correct) / static_cast<double>(s->nv), loss});
+  return GHC_OK;
+}
+
 ghc_status run_sync(ghc_session* s, float* h_loss) {
   // Round r = one fused launch over the active workers' batches, rank order.
   const int B = s->cfg.batch_size;
@@ -226,8 +259,16 @@ ghc_status run_sync(ghc_session* s, float* h_loss) {
   CU(cudaMalloc(&d_loss, sizeof(float) * counts.size()));
   CU(cudaMemcpy(d_table, table.data(), sizeof(int32_t) * table.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_counts, counts.data(), sizeof(int32_t) * counts.size(), cudaMemcpyHostToDevice));
-  ghc_status st = ghc_master_sync_rounds(s->master, s->X, s->Y, d_table, stride, d_counts,
-                                         stride, R, d_loss);
+  // one persistent launch for all rounds, or chunks of V rounds with the
+  // master's serial validation in between (split launches are bit-identical)
+  ghc_status st = GHC_OK;
+  const int V = s->nv > 0 && s->v_every > 0 ? s->v_every : R;
+  for (int r0 = 0; r0 < R && st == GHC_OK; r0 += V) {
+    const int nr = std::min(V, R - r0);
+    st = ghc_master_sync_rounds(s->master, s->X, s->Y, d_table + static_cast<int64_t>(r0) * stride,
+                                stride, d_counts + r0, stride, nr, d_loss + r0);
+    if (st == GHC_OK && V < R) st = validate_now(s);
+  }
   if (st == GHC_OK && h_loss) {
     std::vector<float> lo(static_cast<size_t>(R));
     CU(cudaMemcpyAsync(lo.data(), d_loss, sizeof(float) * R, cudaMemcpyDeviceToHost,
@@ -273,6 +314,8 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
       CU(cudaMemcpyAsync(wk, s->master->w[0], sizeof(float) * P, cudaMemcpyDeviceToDevice,
                          c->stream));
       s->basis[static_cast<size_t>(k)] = version;
+      if (s->v_every > 0 && version % s->v_every == 0)
+        if (ghc_status st = validate_now(s)) return st;
     } else {
       const uint64_t bi = s->bidx[static_cast<size_t>(k)]++;
       int exch = (bi % static_cast<uint64_t>(s->cfg.tau)) == 0;
@@ -291,6 +334,8 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
       if (exch) {
         ++version;
         s->basis[static_cast<size_t>(k)] = version;
+        if (s->v_every > 0 && version % s->v_every == 0)
+          if (ghc_status st = validate_now(s)) return st;
       }
     }
   }
@@ -503,6 +548,8 @@ void ghc_session_destroy(ghc_session* s) {
   cudaFree(s->cver);
   cudaFree(s->ms);
   cudaFree(s->err);
+  cudaFree(s->Xv);
+  cudaFree(s->Yv);
   delete s;
 }
 
@@ -540,6 +587,39 @@ ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_ord
   int err = 0;
   CU(cudaMemcpy(&err, s->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err & 2) return fail(GHC_ERR_NONFINITE, "easgd_worker_step: gradient has NaN/Inf entries");
+  return validate_now(s);  // "and once at end"
+}
+
+ghc_status ghc_session_set_validation(ghc_session* s, const float* h_x, const int32_t* h_y,
+                                      int64_t n, int32_t every) {
+  if (!s) return fail(GHC_ERR_CONFIG, "session: null handle");
+  if (n < 1 || !h_x || !h_y) return fail(GHC_ERR_CONFIG, "validate: empty held-out set");
+  if (every < 0) return fail(GHC_ERR_CONFIG, "validation cadence must be >= 0");
+  const int64_t width = s->plan->model.input_width;
+  cudaFree(s->Xv);
+  cudaFree(s->Yv);
+  s->Xv = nullptr;
+  s->Yv = nullptr;
+  CU(cudaMalloc(&s->Xv, sizeof(float) * n * width));
+  CU(cudaMalloc(&s->Yv, sizeof(int32_t) * n));
+  CU(cudaMemcpy(s->Xv, h_x, sizeof(float) * n * width, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(s->Yv, h_y, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  s->nv = n;
+  s->v_every = every;
+  return GHC_OK;
+}
+
+ghc_status ghc_session_validations(ghc_session* s, int64_t cap, uint64_t* versions,
+                                   double* accuracy, double* loss, int64_t* count) {
+  if (!s) return fail(GHC_ERR_CONFIG, "session: null handle");
+  const int64_t n = static_cast<int64_t>(s->vrec.size());
+  for (int64_t i = 0; i < n && i < cap; ++i) {
+    const auto& v = s->vrec[static_cast<size_t>(i)];
+    if (versions) versions[i] = v.version;
+    if (accuracy) accuracy[i] = v.accuracy;
+    if (loss) loss[i] = v.loss;
+  }
+  if (count) *count = n;
   return GHC_OK;
 }
 

@@ -373,6 +373,20 @@ class Master:
         return wp
 
 
+def validate(w, arch: Architecture, x, y):
+    """validate: (accuracy, mean loss, correct count) of
+    weights w over a held-out set, one fused forward on the device."""
+    ctx = arch.ctx
+    dw = ctx.upload(np.ascontiguousarray(w, np.float32))
+    dx = ctx.upload(np.ascontiguousarray(x, np.float32))
+    dy = ctx.upload(np.ascontiguousarray(y, np.int32))
+    ok = C.c_int64(0)
+    lo = C.c_double(0.0)
+    check(ctx.lib.ghc_validate(arch.h, dw.ptr, dx.ptr, dy.ptr, len(y), C.byref(ok), C.byref(lo)),
+          "validate")
+    return ok.value / len(y), lo.value, ok.value
+
+
 # ---------------------------------------------------------------- data layer
 def data_spec(n_files, samples_per_file, seq_len=10, input_dim=5, n_classes=3, delta=5.0,
               seed=1234) -> DataSpec:
@@ -467,6 +481,25 @@ class Session:
         check(self.ctx.lib.ghc_session_run(self.h, None if o is None else _vp(o), n, _vp(loss),
                                            _vp(stale), cap), "session_run")
         return loss, stale[:n]
+
+    def set_validation(self, x: np.ndarray, y: np.ndarray, every: int = 0):
+        """Held-out set of the master's serial validation:
+        every `every` master updates (0: only at the end) and once at the end."""
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.ascontiguousarray(y, np.int32)
+        check(self.ctx.lib.ghc_session_set_validation(self.h, _vp(x), _vp(y), len(y), every),
+              "set_validation")
+
+    def validations(self):
+        """VALIDATE_RESULT records: list of (version, accuracy, mean loss)."""
+        n = C.c_int64(0)
+        check(self.ctx.lib.ghc_session_validations(self.h, 0, None, None, None, C.byref(n)))
+        ver = np.zeros(n.value, np.uint64)
+        acc = np.zeros(n.value, np.float64)
+        lo = np.zeros(n.value, np.float64)
+        check(self.ctx.lib.ghc_session_validations(self.h, n.value, _vp(ver), _vp(acc), _vp(lo),
+                                                   C.byref(n)))
+        return [(int(a), float(b), float(c)) for a, b, c in zip(ver, acc, lo)]
 
     def read(self):
         P = self.arch.n_params

@@ -134,3 +134,45 @@ def test_session_config_errors(ctx):
     with pytest.raises(g.ProtocolError):
         g.Session(arch, g.train_config(n_workers=2, mode=g.REPLAY, batch_size=10),
                   g.data_spec(4, 10)).run(np.zeros(3, np.int32))  # worker 0 has 2 batches
+
+
+def test_validate_vs_oracle(ctx, oracle):
+    """ghc_validate: correct count exact, mean loss ≤ 1e-5."""
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    spec, x, y = oracle_data(oracle, 4, 500)
+    a = oracle.parse_arch(BENCH_ARCH)
+    for w in (g.init_weights(arch, 7), np.zeros(arch.n_params)):
+        acc, lo, ok = g.validate(w, arch, x.astype(np.float32), y)
+        oko, loo = oracle.validate(a, np.asarray(w, np.float32).astype(np.float64), x, y)
+        assert ok == oko and acc == oko / len(y)
+        assert abs(lo - loo) / loo <= 1e-5
+    with pytest.raises(g.ConfigError):
+        g.validate(g.init_weights(arch, 7), arch, x[:0].astype(np.float32), y[:0])
+
+
+@pytest.mark.parametrize("mode", ["sync", "replay"])
+def test_session_validation_cadence(ctx, oracle, mode):
+    """Validation every V master updates and once at the end (SPEC.md:378,
+    384); each record equals ghc_validate of the weights at that version, and
+    V = 0 leaves only the final record."""
+    W, B, V = 4, 50, 5
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    spec, x, y = oracle_data(oracle, 8, 300)
+    hx, hy = x[:400].astype(np.float32), y[:400]
+    kw = dict(n_workers=W, batch_size=B, epochs=1)
+    if mode == "replay":
+        kw["mode"] = g.REPLAY
+    order = np.repeat(np.arange(W, dtype=np.int32), 12) if mode == "replay" else None
+    recs = {}
+    for every in (V, 0):
+        s = g.Session(arch, g.train_config(**kw), g.data_spec(8, 300))
+        s.set_validation(hx, hy, every)
+        s.run(order)
+        recs[every] = s.validations()
+        out = s.read()
+    n_upd = out["version"]
+    assert [r[0] for r in recs[V]] == list(range(V, n_upd + 1, V)) + \
+        ([n_upd] if n_upd % V else [])
+    assert len(recs[0]) == 1 and recs[0][0][0] == n_upd
+    acc, lo, _ = g.validate(out["w"], arch, hx, hy)
+    assert recs[V][-1][1] == acc == recs[0][0][1] and abs(recs[V][-1][2] - lo) <= 1e-6 * lo

@@ -266,3 +266,18 @@ class TestAgainstReferenceBuild:
             r2 = oracle.ref_run_sync(BENCH_ARCH, spec, x, y, cfg)
             assert np.array_equal(r1.w, r2.w) and np.array_equal(r1.v, r2.v)
             assert r1.stats.updates == r2.stats.updates
+
+
+def test_validate_oracle_pins(oracle):
+    """validate pins: zero weights → uniform p, argmax 0 on
+    the tie, so accuracy = share of label 0 and loss = ln K; the count equals
+    an independent numpy argmax over the oracle's probabilities."""
+    a = oracle.parse_arch("lstm(5,20,10),softmax(20,3)")
+    s = oracle.data_spec(2, 150)
+    x, y = oracle.generate(s)
+    ok, lo = oracle.validate(a, np.zeros(oracle.n_params(a)), x, y)
+    assert ok == int((y == 0).sum()) and abs(lo - np.log(3)) < 1e-12
+    w = oracle.init_weights(a, 7)
+    ok, lo = oracle.validate(a, w, x, y)
+    _, probs, loo = oracle.forward_backward(a, w, x, y, want_grad=False)
+    assert ok == int((np.argmax(probs, 1) == y).sum()) and lo == loo
