@@ -308,6 +308,25 @@ ghc_status ghc_data_epoch_indices(const ghc_data_spec* spec, int32_t n_workers,
                                   int32_t worker, int32_t epoch, uint64_t shuffle_seed,
                                   int32_t shuffle, int64_t* h_out, int64_t* count);
 
+/* Wire frames on the device (proto.cpp:214-386): the
+ * reference's GHUB frame of a WEIGHTS (kind 1, version) / GRADIENT (kind 2,
+ * basis_version, sample_count ≥ 1) message over the arch's tensors, f32
+ * (wire_f64 = 0) or f64 values; kind 0 = SHUTDOWN.  Byte-identical to the
+ * reference encoder.  d_out must be 16-byte aligned (cudaMalloc is). */
+ghc_status ghc_frame_size(const ghc_plan* plan, int32_t kind, int32_t wire_f64, int64_t* bytes);
+ghc_status ghc_encode_frame(ghc_plan* plan, int32_t kind, int32_t wire_f64, const float* d_w,
+                            uint64_t version, uint64_t sample_count, uint8_t* d_out, int64_t cap,
+                            int64_t* len);
+/* Validates the frame (bad magic / unsupported version / truncated / length
+ * overflow / unknown type / malformed payload → GHC_ERR_PROTOCOL with
+ * *decode_status = the reference's DecodeStatus 1..6; tensors not matching
+ * the arch → GHC_ERR_SHAPE) and unpacks the values into d_w[P] (f64 frames
+ * rounded to f32).  *kind: 1 WEIGHTS, 2 GRADIENT, 0 SHUTDOWN, -type for the
+ * other message types. */
+ghc_status ghc_decode_frame(ghc_plan* plan, const uint8_t* d_frame, int64_t len, int32_t* kind,
+                            float* d_w, uint64_t* version, uint64_t* sample_count,
+                            int32_t* wire_f64, int32_t* decode_status);
+
 /* validate: the master's serial held-out evaluation —
  * one fused forward over the n held-out samples, then *h_correct = samples
  * whose argmax_k p_k (lowest k on ties) equals the label and *h_loss_mean =

@@ -1170,3 +1170,164 @@ out:
   free(yb);
   return rc;
 }
+
+/* ==================================================================== */
+/* proto.cpp frames — restated (encode proto.cpp:214-272, decode 288-386) */
+/* ==================================================================== */
+#define GHO_MAX_T 64
+static void le_put(uint8_t* p, uint64_t v, int n) {
+  for (int i = 0; i < n; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+static uint64_t le_get(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = 0; i < n; ++i) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+int64_t gho_frame_size(const gho_arch* a, int kind, int wire_f64) {
+  if (kind == 0) return 15;
+  int64_t off[GHO_MAX_T], sz[GHO_MAX_T], d0[GHO_MAX_T], d1[GHO_MAX_T];
+  const int nt = gho_arch_tensors(a, off, sz, d0, d1, GHO_MAX_T);
+  const int64_t es = wire_f64 ? 8 : 4;
+  int64_t block = 4;
+  for (int t = 0; t < nt; ++t) block += 1 + 4 * (d1[t] ? 2 : 1) + es * sz[t];
+  return 15 + (kind == 1 ? 8 : 16) + block;
+}
+
+int gho_encode_frame(const gho_arch* a, int kind, const double* w, uint64_t version,
+                     uint64_t sample_count, int wire_f64, uint8_t* out, int64_t cap,
+                     int64_t* len) {
+  if (kind < 0 || kind > 2) return GHO_CONFIG;
+  if (kind == 2 && sample_count < 1) return GHO_CONFIG; /* proto.cpp:231-233 */
+  const int64_t n = gho_frame_size(a, kind, wire_f64);
+  *len = n;
+  if (n > cap) return GHO_SHAPE;
+  uint8_t type = kind == 0 ? 0x06 : (kind == 1 ? 0x02 : 0x03);
+  if (kind != 0 && wire_f64) type |= 0x40;
+  uint8_t* p = out;
+  p[0] = 'G'; p[1] = 'H'; p[2] = 'U'; p[3] = 'B';
+  le_put(p + 4, 1, 2);
+  p[6] = type;
+  le_put(p + 7, (uint64_t)(n - 15), 8);
+  p += 15;
+  if (kind == 0) return GHO_OK;
+  le_put(p, version, 8);
+  p += 8;
+  if (kind == 2) {
+    le_put(p, sample_count, 8);
+    p += 8;
+  }
+  int64_t off[GHO_MAX_T], sz[GHO_MAX_T], d0[GHO_MAX_T], d1[GHO_MAX_T];
+  const int nt = gho_arch_tensors(a, off, sz, d0, d1, GHO_MAX_T);
+  le_put(p, (uint64_t)nt, 4);
+  p += 4;
+  for (int t = 0; t < nt; ++t) {
+    const int rank = d1[t] ? 2 : 1;
+    *p++ = (uint8_t)rank;
+    le_put(p, (uint64_t)d0[t], 4);
+    p += 4;
+    if (rank == 2) {
+      le_put(p, (uint64_t)d1[t], 4);
+      p += 4;
+    }
+    for (int64_t i = 0; i < sz[t]; ++i) {
+      const double v = w[off[t] + i];
+      if (wire_f64) {
+        uint64_t b;
+        memcpy(&b, &v, 8);
+        le_put(p, b, 8);
+        p += 8;
+      } else {
+        const float f = (float)v;
+        uint32_t b;
+        memcpy(&b, &f, 4);
+        le_put(p, b, 4);
+        p += 4;
+      }
+    }
+  }
+  return GHO_OK;
+}
+
+int gho_decode_frame(const gho_arch* a, const uint8_t* in, int64_t len, int* kind, double* w,
+                     uint64_t* version, uint64_t* sample_count, int* wire_f64, int* status) {
+  *status = 0;
+  if (len < 4) { *status = 3; return GHO_PROTOCOL; }
+  if (memcmp(in, "GHUB", 4) != 0) { *status = 1; return GHO_PROTOCOL; }
+  if (len < 15) { *status = 3; return GHO_PROTOCOL; }
+  if (le_get(in + 4, 2) != 1) { *status = 2; return GHO_PROTOCOL; }
+  const uint8_t type = in[6], base = type & (uint8_t)~0x40;
+  const int f64 = (type & 0x40) != 0;
+  if (!(base >= 0x01 && base <= 0x06) || (f64 && base != 0x02 && base != 0x03)) {
+    *status = 5;
+    return GHO_PROTOCOL;
+  }
+  const uint64_t plen = le_get(in + 7, 8);
+  if (plen > (1ull << 40)) { *status = 4; return GHO_PROTOCOL; }
+  if (plen > (uint64_t)(len - 15)) { *status = 3; return GHO_PROTOCOL; }
+  const uint8_t* p = in + 15;
+  uint64_t rem = plen;
+#define NEED(n) do { if (rem < (uint64_t)(n)) { *status = 6; return GHO_PROTOCOL; } } while (0)
+  *wire_f64 = f64;
+  if (base != 0x02 && base != 0x03) {
+    /* HELLO/VALIDATE_RESULT/DONE/SHUTDOWN: not parameter frames */
+    *kind = base == 0x06 ? 0 : -(int)base;
+    const uint64_t want = base == 0x01 ? 5 : base == 0x04 ? 24 : base == 0x05 ? 4 : 0;
+    if (rem != want) { *status = 6; return GHO_PROTOCOL; }
+    return GHO_OK;
+  }
+  *kind = base == 0x02 ? 1 : 2;
+  NEED(8);
+  *version = le_get(p, 8); p += 8; rem -= 8;
+  *sample_count = 0;
+  if (base == 0x03) {
+    NEED(8);
+    *sample_count = le_get(p, 8); p += 8; rem -= 8;
+    if (*sample_count < 1) { *status = 6; return GHO_PROTOCOL; }
+  }
+  NEED(4);
+  const uint64_t count = le_get(p, 4); p += 4; rem -= 4;
+  if (count > rem) { *status = 6; return GHO_PROTOCOL; }
+  int64_t off[GHO_MAX_T], sz[GHO_MAX_T], d0[GHO_MAX_T], d1[GHO_MAX_T];
+  const int nt = gho_arch_tensors(a, off, sz, d0, d1, GHO_MAX_T);
+  int shape_ok = (int64_t)count == nt;
+  const int es = f64 ? 8 : 4;
+  for (uint64_t t = 0; t < count; ++t) {
+    NEED(1);
+    const int rank = *p++; rem -= 1;
+    if (rank == 0) { *status = 6; return GHO_PROTOCOL; }
+    uint64_t elems = 1, dims[2] = {0, 0};
+    for (int r = 0; r < rank; ++r) {
+      NEED(4);
+      const uint64_t d = le_get(p, 4); p += 4; rem -= 4;
+      if (d == 0) { *status = 6; return GHO_PROTOCOL; }
+      if (r < 2) dims[r] = d;
+      if (elems > (1ull << 40) / d) { *status = 6; return GHO_PROTOCOL; }
+      elems *= d;
+    }
+    if (elems * (uint64_t)es > rem) { *status = 6; return GHO_PROTOCOL; }
+    if (shape_ok && (int)t < nt) {
+      const int want_rank = d1[t] ? 2 : 1;
+      shape_ok = rank == want_rank && (int64_t)dims[0] == d0[t] &&
+                 (want_rank == 1 || (int64_t)dims[1] == d1[t]);
+    }
+    for (uint64_t i = 0; i < elems; ++i) {
+      double v;
+      if (f64) {
+        const uint64_t b = le_get(p, 8);
+        memcpy(&v, &b, 8);
+      } else {
+        const uint32_t b = (uint32_t)le_get(p, 4);
+        float f;
+        memcpy(&f, &b, 4);
+        v = (double)f;
+      }
+      if (shape_ok && w) w[off[t] + (int64_t)i] = v;
+      p += es;
+      rem -= (uint64_t)es;
+    }
+  }
+#undef NEED
+  if (rem != 0) { *status = 6; return GHO_PROTOCOL; }
+  return shape_ok ? GHO_OK : GHO_SHAPE;
+}

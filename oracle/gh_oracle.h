@@ -107,6 +107,24 @@ int gho_easgd_center_step(double* c, const double* worker, int64_t p,
 
 /* ---- proto.cpp wire rounding (proto.cpp:79,125) ---------------------- */
 void gho_wire_round(double* dst, const double* src, int64_t p, int wire_f64);
+/* ---- proto.cpp frames (restated) -------------------------------------- */
+/* kind: 0 SHUTDOWN, 1 WEIGHTS {version}, 2 GRADIENT {basis_version,
+ * sample_count}; tensors = the arch's parameter tensors in weight-set order
+ * (arch.cpp:95-112), values f32 (wire_f64 = 0) or f64 (type | 0x40).
+ * Layout (proto.cpp:214-272): "GHUB" | u16 version 1 | u8 type | u64 payload
+ * length | payload; tensor block = u32 count, per tensor u8 rank, u32 dims,
+ * values; all little-endian. */
+int64_t gho_frame_size(const gho_arch* a, int kind, int wire_f64);
+int gho_encode_frame(const gho_arch* a, int kind, const double* w, uint64_t version,
+                     uint64_t sample_count, int wire_f64, uint8_t* out, int64_t cap,
+                     int64_t* len);
+/* decode (proto.cpp:288-386) + the arch check the roles do when they build a
+ * WeightSet: *status = DecodeStatus (0 ok, 1 bad_magic, 2 unsupported_version,
+ * 3 truncated, 4 length_overflow, 5 unknown_type, 6 malformed_payload);
+ * returns GHO_PROTOCOL on a decode failure, GHO_SHAPE when the tensors do not
+ * match the arch; w receives the values widened to f64. */
+int gho_decode_frame(const gho_arch* a, const uint8_t* in, int64_t len, int* kind, double* w,
+                     uint64_t* version, uint64_t* sample_count, int* wire_f64, int* status);
 
 /* ---- data (decisions in DESIGN.md "Data layer") ---- */
 typedef struct {

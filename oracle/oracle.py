@@ -76,6 +76,8 @@ def lib():
         _lib.gho_arch_input_width.restype = C.c_int64
         _lib.gho_epoch_indices.restype = C.c_int64
         _lib.gho_mix_seed.restype = C.c_uint64
+        _lib.gho_frame_size.restype = C.c_int64
+        _lib.gho_frame_size.argtypes = [C.c_void_p, C.c_int, C.c_int]
         _lib.gho_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
         _lib.gho_rng_u64.restype = C.c_uint64
         _lib.gho_rng_normal.restype = C.c_double
@@ -194,6 +196,44 @@ def validate(arch: Arch, w, x, y):
     if rc != OK:
         raise RuntimeError(f"gho_validate status {rc}")
     return ok.value, lo.value
+
+
+def encode_frame(arch: Arch, kind: int, w, version=0, sample_count=1, wire_f64=0) -> bytes:
+    """gho_encode_frame: kind 0 SHUTDOWN, 1 WEIGHTS, 2 GRADIENT."""
+    n = lib().gho_frame_size(C.byref(arch), kind, wire_f64)
+    buf = np.zeros(n, np.uint8)
+    ln = C.c_int64(0)
+    wv = None if w is None else np.ascontiguousarray(w, np.float64)
+    rc = lib().gho_encode_frame(C.byref(arch), kind, _p(wv), C.c_uint64(version),
+                                C.c_uint64(sample_count), wire_f64, _p(buf, C.c_uint8),
+                                C.c_int64(n), C.byref(ln))
+    if rc != OK:
+        raise RuntimeError(f"gho_encode_frame status {rc}")
+    return bytes(buf[: ln.value])
+
+
+def decode_frame(arch: Arch, frame: bytes):
+    """gho_decode_frame → (rc, decode_status, kind, w, version, sample_count, f64)."""
+    buf = np.frombuffer(frame, np.uint8).copy() if len(frame) else np.zeros(1, np.uint8)
+    w = np.zeros(n_params(arch), np.float64)
+    kind, st, f64 = C.c_int(0), C.c_int(0), C.c_int(0)
+    ver, cnt = C.c_uint64(0), C.c_uint64(0)
+    rc = lib().gho_decode_frame(C.byref(arch), _p(buf, C.c_uint8), C.c_int64(len(frame)),
+                                C.byref(kind), _p(w), C.byref(ver), C.byref(cnt), C.byref(f64),
+                                C.byref(st))
+    return rc, st.value, kind.value, w, ver.value, cnt.value, f64.value
+
+
+def ref_encode(arch_text: str, kind: int, w, version=0, sample_count=1, wire_f64=0) -> bytes:
+    """The reference's own encoder (oracle/_ref, proto.cpp encode)."""
+    buf = np.zeros(1 << 26, np.uint8) if w is not None and len(w) > 1 << 20 else np.zeros(1 << 20, np.uint8)
+    n = C.c_int64(0)
+    wv = None if w is None else np.ascontiguousarray(w, np.float64)
+    rc = ref().ghr_encode(kind, None if arch_text is None else arch_text.encode(), _p(wv),
+                          version, sample_count, wire_f64, _p(buf, C.c_uint8), len(buf), C.byref(n))
+    if rc != 0:
+        raise RuntimeError(f"ghr_encode status {rc}")
+    return bytes(buf[: n.value])
 
 
 def finite_diff(arch: Arch, w, x, y, eps=1e-5):

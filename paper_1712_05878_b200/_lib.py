@@ -127,6 +127,9 @@ SIGNATURES = [
     ("ghc_session_set_validation", C.c_int, [_vp, _vp, _vp, _i64, _i32]),
     ("ghc_session_validations", C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
     ("ghc_validate", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    ("ghc_frame_size", C.c_int, [_vp, _i32, _i32, _vp]),
+    ("ghc_encode_frame", C.c_int, [_vp, _i32, _i32, _vp, _u64, _u64, _vp, _i64, _vp]),
+    ("ghc_decode_frame", C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ghc_session_read", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     ("ghc_data_generate", C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     ("ghc_data_shard", C.c_int, [_i32, _i32, _i32, _vp, _vp]),

@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libghc.so")
 
-CU_SOURCES = ["ghc.cu", "dist.cu", "p2p.cu", "session.cu", "dense.cu", "layered.cu", "diag_barrier.cu"]
+CU_SOURCES = ["ghc.cu", "dist.cu", "p2p.cu", "codec.cu", "session.cu", "dense.cu", "layered.cu", "diag_barrier.cu"]
 CXX_SOURCES = ["host_model.cpp"]
 # every header in csrc/ is a dependency of every translation unit
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h")))

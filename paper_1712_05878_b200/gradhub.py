@@ -387,6 +387,44 @@ def validate(w, arch: Architecture, x, y):
     return ok.value / len(y), lo.value, ok.value
 
 
+# ---------------------------------------------------------------- wire frames
+FRAME_SHUTDOWN, FRAME_WEIGHTS, FRAME_GRADIENT = 0, 1, 2
+
+
+def encode_frame(arch: Architecture, kind: int, w=None, version: int = 0, sample_count: int = 1,
+                 wire_f64: bool = False) -> bytes:
+    """GHUB frame (proto.cpp:214-272) packed on the device (ghc_encode_frame)."""
+    ctx = arch.ctx
+    n = C.c_int64(0)
+    check(ctx.lib.ghc_frame_size(arch.h, kind, int(wire_f64), C.byref(n)), "frame_size")
+    out = ctx.array(max(n.value, 16), np.uint8)
+    dw = ctx.upload(np.ascontiguousarray(w, np.float32)) if w is not None else None
+    ln = C.c_int64(0)
+    check(ctx.lib.ghc_encode_frame(arch.h, kind, int(wire_f64), dw.ptr if dw else None, version,
+                                   sample_count, out.ptr, out.nbytes, C.byref(ln)), "encode")
+    return out.numpy()[: ln.value].tobytes()
+
+
+def decode_frame(arch: Architecture, frame: bytes):
+    """ghc_decode_frame → (kind, w f32[P] or None, version, sample_count, wire_f64);
+    raises ProtocolError (with .decode_status) / ShapeError like the reference."""
+    ctx = arch.ctx
+    buf = np.frombuffer(frame, np.uint8) if len(frame) else np.zeros(1, np.uint8)
+    d = ctx.upload(np.ascontiguousarray(buf))
+    w = ctx.array(arch.n_params)
+    kind, f64, st = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    ver, cnt = C.c_uint64(0), C.c_uint64(0)
+    rc = ctx.lib.ghc_decode_frame(arch.h, d.ptr, len(frame), C.byref(kind), w.ptr, C.byref(ver),
+                                  C.byref(cnt), C.byref(f64), C.byref(st))
+    try:
+        check(rc, "decode")
+    except GradhubError as e:
+        e.decode_status = st.value
+        raise
+    wv = w.numpy() if kind.value in (FRAME_WEIGHTS, FRAME_GRADIENT) else None
+    return kind.value, wv, ver.value, cnt.value, bool(f64.value)
+
+
 # ---------------------------------------------------------------- data layer
 def data_spec(n_files, samples_per_file, seq_len=10, input_dim=5, n_classes=3, delta=5.0,
               seed=1234) -> DataSpec:

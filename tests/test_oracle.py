@@ -246,6 +246,29 @@ def test_async_replay_staleness(oracle):
                                                     "_ref", "libghref.so")),
                     reason="oracle/_ref not built (needs /root/reference)")
 class TestAgainstReferenceBuild:
+    def test_frame_codec_bitexact(self, oracle):
+        """gho_encode_frame == the reference encoder (proto.cpp encode) byte for
+        byte; gho_decode_frame inverts it and reports DecodeStatus like decode."""
+        for arch in [BENCH_ARCH, "dense(50,8,tanh),dense(8,6,relu),softmax(6,3)"]:
+            a = oracle.parse_arch(arch)
+            w = oracle.init_weights(a, 3)
+            for kind in (1, 2):
+                for f64 in (0, 1):
+                    fr = oracle.encode_frame(a, kind, w, 99, 17, f64)
+                    assert fr == oracle.ref_encode(arch, kind, w, 99, 17, f64)
+                    rc, st, k, w2, ver, cnt, ff = oracle.decode_frame(a, fr)
+                    assert (rc, st, k, ver, ff) == (0, 0, kind, 99, f64)
+                    want = w if f64 else w.astype(np.float32).astype(np.float64)
+                    assert np.array_equal(w2, want) and cnt == (17 if kind == 2 else 0)
+        assert oracle.encode_frame(a, 0, None) == oracle.ref_encode(None, 0, None)
+        fr = oracle.encode_frame(oracle.parse_arch(BENCH_ARCH), 2, oracle.init_weights(
+            oracle.parse_arch(BENCH_ARCH), 1), 1, 5, 0)
+        for bad, st in [(b"XHUB" + fr[4:], 1), (fr[:4] + b"\x02\x00" + fr[6:], 2), (fr[:-3], 3),
+                         (fr[:6] + b"\x09" + fr[7:], 5), (fr[:3], 3),
+                         (fr[:7] + (int.from_bytes(fr[7:15], "little") + 1).to_bytes(8, "little")
+                          + fr[15:] + b"\x00", 6)]:
+            assert oracle.decode_frame(oracle.parse_arch(BENCH_ARCH), bad)[:2] == (6, st)
+
     def test_forward_backward_bitexact(self, oracle):
         for arch in [BENCH_ARCH, "dense(50,8,tanh),dense(8,6,relu),softmax(6,3)",
                      "lstm(5,7,10),dense(7,4,identity),softmax(4,3)"]:
