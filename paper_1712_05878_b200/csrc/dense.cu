@@ -1,4 +1,9 @@
 // dense.cu — C ABI for the dense-layer GEMM (tcgen05, 3×TF32) and transpose.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <string>
+
 #include "dense_gemm.cuh"
 #include "ghc_internal.cuh"
 
@@ -21,6 +26,58 @@ ghc_status launch_gemm(ghc_ctx* c, const GemmArgs& g) {
   c->launches++;
   return GHC_OK;
 }
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// fp32 [rows][ld] K-major operand, box = one 16-byte K-chunk × box_rows rows.
+bool make_map(CUtensorMap* tm, const float* base, int rows, int K, int ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15u) || (ld % 4)) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+  const cuuint32_t box[2] = {4, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// GHC_GEMM=legacy forces the register-staged kernel (A/B comparisons).
+bool tma_allowed() {
+  static const bool ok = [] {
+    const char* e = std::getenv("GHC_GEMM");
+    return !(e && std::string(e) == "legacy");
+  }();
+  return ok;
+}
+
+template <int BN>
+ghc_status launch_gemm_tma(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta,
+                           const CUtensorMap& tb) {
+  constexpr int stage = 2 * gemm_detail::BM * gemm_detail::BK * 4 + 2 * BN * gemm_detail::BK * 4;
+  const size_t smem = gemm_detail::kTmaStages * stage;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CU(cudaFuncSetAttribute(tcgen05_gemm_tma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    attr_set = true;
+  }
+  dim3 grid((g.N + BN - 1) / BN, (g.M + gemm_detail::BM - 1) / gemm_detail::BM);
+  tcgen05_gemm_tma_kernel<BN><<<grid, 192, smem, c->stream>>>(ta, tb, g);
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -31,6 +88,11 @@ ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_
                        float alpha) {
   if (M < 1 || N < 1 || K < 1) return ghc_fail(GHC_ERR_SHAPE, "gemm: empty operand");
   GemmArgs g{d_a, d_b, d_c, d_bias, d_y, M, N, K, lda, ldb, ldc, ldy, act, alpha, epi};
+  const int bn = N <= 32 ? 32 : 128;
+  CUtensorMap ta, tb;
+  if (tma_allowed() && make_map(&ta, d_a, M, K, lda, gemm_detail::BM) &&
+      make_map(&tb, d_b, N, K, ldb, bn))
+    return bn == 32 ? launch_gemm_tma<32>(c, g, ta, tb) : launch_gemm_tma<128>(c, g, ta, tb);
   if (N <= 32) return launch_gemm<32>(c, g);
   return launch_gemm<128>(c, g);
 }

@@ -18,6 +18,7 @@
 //   activation-derivative / scale → st.global.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -273,6 +274,216 @@ __global__ void __launch_bounds__(128, 1) tcgen05_gemm_nt_kernel(GemmArgs g) {
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(TCOLS));
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed, warp-specialised variant (the default when strides allow TMA).
+//
+//   warp 0      : TMA producer — per stage 8 boxes of A (16 B of K × 128 rows)
+//                 and 8 of B; a box of one 16-byte K-chunk lands as rows × 16 B
+//                 contiguous = one column of core matrices of the canonical
+//                 K-major SWIZZLE_NONE layout (LBO = rows·16, SBO = 128).  TMA
+//                 zero-fills the M/N/K edges.
+//   warp 1      : TMEM allocation, one elected thread issues the 12 MMAs of a
+//                 stage (4 K-steps × 3×TF32) and commits to the stage's
+//                 "empty" barrier.
+//   warps 2..5  : split — the raw fp32 tile IS the "hi" operand (the tensor
+//                 core ignores the low 13 mantissa bits); they write only
+//                 lo = x − trunc_tf32(x) (exact), then the epilogue (TMEM lane
+//                 quarter = warp % 4).
+// Stages: STAGES × (A_hi, A_lo, B_hi, B_lo) in smem; barriers full (TMA bytes),
+// split (128 arrivals), empty (MMA commit), done (last commit).
+namespace gemm_detail {
+
+constexpr int kTmaStages = 3;
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace gemm_detail
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    tcgen05_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+                            const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  using namespace gemm_detail;
+  static_assert(BN == 32 || BN == 64 || BN == 128, "N tile");
+  constexpr int S = kTmaStages;
+  constexpr int A_BYTES = BM * BK * 4;
+  constexpr int B_BYTES = BN * BK * 4;
+  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi | A_lo | B_hi | B_lo
+  constexpr int NACC = 4;                           // rotating accumulators (accuracy)
+  constexpr int TCOLS = NACC * BN < 32 ? 32 : NACC * BN;
+  static_assert(TCOLS <= 512, "TMEM columns");
+  extern __shared__ __align__(1024) uint8_t gsm[];
+  __shared__ uint64_t full[S], split[S], empty[S], done;
+  __shared__ uint32_t tmem_base_s;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nkb = (g.K + BK - 1) / BK;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        if (kb >= S) mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+        uint8_t* st = gsm + s * STAGE;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+#pragma unroll
+        for (int c = 0; c < BK / 4; ++c) {
+          tma_load_2d(st + c * BM * 16, &tmA, kb * BK + 4 * c, m0, &full[s]);
+          tma_load_2d(st + 2 * A_BYTES + c * BN * 16, &tmB, kb * BK + 4 * c, n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        mbar_wait(&split[s], (kb / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_hi = smem_u32(gsm + s * STAGE), a_lo = a_hi + A_BYTES;
+        const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+        const uint32_t d = tmem + static_cast<uint32_t>((kb % NACC) * BN);
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t ao = ks * 2 * BM * 16, bo = ks * 2 * BN * 16;
+          const uint64_t dah = make_desc(a_hi + ao, BM * 16, 128);
+          const uint64_t dal = make_desc(a_lo + ao, BM * 16, 128);
+          const uint64_t dbh = make_desc(b_hi + bo, BN * 16, 128);
+          const uint64_t dbl = make_desc(b_lo + bo, BN * 16, 128);
+          const uint32_t acc0 = (kb >= NACC || ks > 0) ? 1u : 0u;
+          umma_tf32(d, dal, dbh, idesc, acc0);  // lo·hi (small terms first)
+          umma_tf32(d, dah, dbl, idesc, 1u);    // hi·lo
+          umma_tf32(d, dah, dbh, idesc, 1u);    // hi·hi
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&empty[s])));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(&done)));
+    }
+  } else {
+    // ---------------- split: lo = x - trunc_tf32(x) ----------------
+    const int t = tid - 64;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % S;
+      mbar_wait(&full[s], (kb / S) & 1);
+      uint8_t* st = gsm + s * STAGE;
+      auto split_tile = [&](const uint8_t* hi, uint8_t* lo, int bytes) {
+        for (int i = t; i < bytes / 16; i += 128) {
+          const uint4 x = reinterpret_cast<const uint4*>(hi)[i];
+          float4 l;
+          l.x = __uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u);
+          l.y = __uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u);
+          l.z = __uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u);
+          l.w = __uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u);
+          reinterpret_cast<float4*>(lo)[i] = l;
+        }
+      };
+      split_tile(st, st + A_BYTES, A_BYTES);
+      split_tile(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES, B_BYTES);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores → tensor core
+      mbar_arrive(&split[s]);
+    }
+    // ---------------- epilogue: TMEM lane quarter = warp % 4 ----------------
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    const bool vec = (g.N % 4 == 0) && (g.ldc % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(g.C) & 15u) == 0);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      for (int a = 0; a < NACC && a < nkb; ++a) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + a * BN + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(v[i]);
+      }
+      if (row < g.M) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int col = n0 + c0 + i;
+          float o = acc[i];
+          if (col < g.N) {
+            if (g.epi == EPI_BIAS_ACT) o = act_f(o + __ldg(g.bias + col), g.act);
+            else if (g.epi == EPI_DACT) o *= dact_from_y(__ldg(g.Y + (long long)row * g.ldy + col), g.act);
+            else o *= g.alpha;
+          }
+          acc[i] = o;
+        }
+        float* crow = g.C + (long long)row * g.ldc + n0 + c0;
+        if (vec && n0 + c0 + 32 <= g.N) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            reinterpret_cast<float4*>(crow)[i / 4] = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (n0 + c0 + i < g.N) crow[i] = acc[i];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
 // Out-of-place transpose: out[c][r] = in[r][c] (32×32 smem tiles).
