@@ -395,15 +395,19 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
     if (pr && threadIdx.x == 0) pr[0] = globaltimer();
 
-    float* wp = wpart + warp * N::PPAD;
-    for (int p = lane; p < N::PPAD / 4; p += 32)
-      reinterpret_cast<float4*>(wp)[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncwarp();
-
     // ---- samples ----
     float lsum = 0.0f;
     int s, s1;
     first_sample(r, s, s1);
+    // One sample per warp (pipelined, SPW = 1): lstm_samples STORES every
+    // gradient entry of the warp partial; otherwise zero it and accumulate.
+    constexpr bool kStore = SPW == 1;
+    float* wp = wpart + warp * N::PPAD;
+    if (!(a.pipelined && kStore) || s >= s1) {
+      for (int p = lane; p < N::PPAD / 4; p += 32)
+        reinterpret_cast<float4*>(wp)[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncwarp();
+    }
     if (a.pipelined) {
       // Rows of round r and indices of round r+1 were requested at the start
       // of round r-1 (prologue for r = 0): a whole round of compute and
@@ -451,9 +455,11 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp) tio[sp] = nullptr;
         if (a.mode == MODE_FWD)
-          lstm_samples<D, H, T, K, false, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps, tio);
+          lstm_samples<D, H, T, K, false, SPW, true, !kStore>(wa, ws, wp, xsp, lab, scl, lane, prb,
+                                                              lo, ps, tio);
         else
-          lstm_samples<D, H, T, K, true, SPW>(wa, ws, wp, xsp, lab, scl, lane, prb, lo, ps, tio);
+          lstm_samples<D, H, T, K, true, SPW, true, !kStore>(wa, ws, wp, xsp, lab, scl, lane, prb, lo,
+                                                             ps, tio);
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
           if (s + sp * NW < s1) lsum += lo[sp];

@@ -163,7 +163,9 @@ struct LstmNet {
 // HEAD = false: the LSTM is the trunk of a deeper net (arch.cpp: lstm first,
 // dense layers after); the forward writes h_T to trunk_io[sp] and the
 // backward starts from dh_T read from trunk_io[sp] (already scaled).
-template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true>
+// ACC = false: the gradient entries are STORED into wp (one sample per warp
+// and round: no zeroing of the 8.6 KB partial needed); true: added.
+template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true, bool ACC = true>
 __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, float* __restrict__ ws,
                                              float* __restrict__ wp,
                                              const float* const (&xs)[SPW],
@@ -175,6 +177,10 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   constexpr int DP = N::DP;
   const bool act = lane < H;
   const int j = act ? lane : 0;
+  auto put = [](float& dst, float v) {
+    if constexpr (ACC) dst += v;
+    else dst = v;
+  };
   float* hs[SPW];
   float* cs[SPW];
   float* dzs[SPW];
@@ -336,8 +342,8 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
       gbs += dzk;
       dh[sp] = fmaf(act ? wsm[N::OFF_WS + k * H + j] : 0.0f, dzk, dh[sp]);
     }
-    if (act) wp[N::OFF_WS + k * H + j] += gws;
-    if (lane == 0) wp[N::OFF_BS + k] += gbs;
+    if (act) put(wp[N::OFF_WS + k * H + j], gws);
+    if (lane == 0) put(wp[N::OFF_BS + k], gbs);
   }
   }  // HEAD
   if (pr && lane == 0) pr[10] = globaltimer();
@@ -410,7 +416,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
       for (int sp = 0; sp < SPW; ++sp)
 #pragma unroll
         for (int t = 0; t < T; ++t) acc += dz[sp][t][q];
-      wp[N::OFF_B + q * H + j] += acc;
+      put(wp[N::OFF_B + q * H + j], acc);
     }
     {
       float acc[4][D];
@@ -432,7 +438,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int d = 0; d < D; ++d) wp[N::OFF_WX + (q * H + j) * D + d] += acc[q][d];
+        for (int d = 0; d < D; ++d) put(wp[N::OFF_WX + (q * H + j) * D + d], acc[q][d]);
     }
     // dWh in column blocks of 4: 16 accumulators, h_{t-1} read as float4
     constexpr int KB = N::HV ? 4 : 1;
@@ -465,7 +471,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int kk = 0; kk < KB; ++kk) wp[N::OFF_WH + (q * H + j) * H + k0 + kk] += acc[kk][q];
+        for (int kk = 0; kk < KB; ++kk) put(wp[N::OFF_WH + (q * H + j) * H + k0 + kk], acc[kk][q]);
     }
   }
   __syncwarp();
