@@ -343,6 +343,13 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     if (p->max_clusters * p->cluster_size > p->max_ctas) p->max_ctas = p->max_clusters * p->cluster_size;
   }
   CU(cudaMalloc(&p->part, sizeof(float) * static_cast<size_t>(p->max_ctas) * p->lstm->ppad));
+  {  // tagged rows of the single-GPU exchange: [2][clusters][EP] + [2][EP], tags start at 0
+    const size_t ep = static_cast<size_t>(std::max(p->lstm->ep[0], p->lstm->ep[1]));
+    const size_t n = 2 * static_cast<size_t>(p->max_ctas) * ep + 2 * ep;
+    CU(cudaMalloc(&p->tpart, sizeof(unsigned long long) * n));
+    CU(cudaMemset(p->tpart, 0, sizeof(unsigned long long) * n));
+    p->tw = p->tpart + 2 * static_cast<size_t>(p->max_ctas) * ep;
+  }
   CU(cudaMalloc(&p->ms, sizeof(MasterDev)));
   CU(cudaMemset(p->ms, 0, sizeof(MasterDev)));
   CU(cudaMalloc(&p->err, sizeof(int)));
@@ -364,6 +371,7 @@ void ghc_plan_destroy(ghc_plan* p) {
   cudaSetDevice(p->ctx->device);
   cudaStreamSynchronize(p->ctx->stream);
   cudaFree(p->part);
+  cudaFree(p->tpart);
   cudaFree(p->ms);
   cudaFree(p->err);
   cudaFree(p->bar);

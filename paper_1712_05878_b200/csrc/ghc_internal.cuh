@@ -82,6 +82,8 @@ struct ghc_plan {
   const LstmEntry* lstm = nullptr;
   int max_ctas = 0;       // co-resident CTAs of the fused kernel
   float* part = nullptr;  // [max_ctas][ppad]
+  unsigned long long* tpart = nullptr;  // tagged rows of the single-GPU exchange
+  unsigned long long* tw = nullptr;
   MasterDev* ms = nullptr;  // scratch barrier state for grad/fwd launches
   int* err = nullptr;
   std::string kname;
@@ -144,6 +146,8 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 
     if (nc > maxc) nc = maxc;
     a.VR = vr;
     a.part = p->part;
+    a.tpart = p->tpart;
+    a.tw = p->tw;
     a.pstride = p->lstm->ep[p->cs_index];
     a.pipelined = n_max <= nc * cs * per_cta;
     cudaLaunchConfig_t cfg = {};

@@ -36,6 +36,272 @@ namespace cg = cooperative_groups;
 #endif
 constexpr int kSamplesPerWarp = GHC_SPW;
 
+// ---------------------------------------------------------------------------
+// Single-GPU exchange, reduce-scatter / all-gather over epoch-tagged L2 rows
+// (the default of the SIMT round kernel).  Per round:
+//   a. every CTA pushes slice q of its CTA partial to cluster peer q
+//      (st.async + the peer's mbarrier complete_tx — no cluster barrier);
+//   b. CTA j sums its CS received rows (rank order) = the cluster partial of
+//      slice j and stores it to L2 as 64-bit (value, tag) elements;
+//   c. CTA (cluster c, rank j) polls the NC cluster rows of SUB-slice c of
+//      slice j until every tag is this round's, sums them in cluster order,
+//      applies sgd_step to the sub-slice (its velocity lives here) and stores
+//      the new weights tagged (tag = 2·epoch + non-finite bit);
+//   d. CTA j polls the NC sub-slices of slice j, ORs their non-finite bits and
+//      pushes the slice (+ its flag) to every CTA of its cluster (st.async);
+//   e. every CTA waits for its CS slices; reject (optim.cpp:49-51) if any flag.
+// A 64-bit element store is single-copy atomic, so a reader that sees the
+// tag sees the value: no fences, no flag barriers.  Rows are double-buffered
+// by epoch parity; a cluster reaches round r+2's stores only after every
+// cluster consumed round r (its round r+1 rows depend on them).
+template <int P, int SL, int EP, int CS>
+struct ClusterRS {
+  static constexpr int E = P + 1;
+  static constexpr int kRowBatch = 32;  // tagged cluster rows polled per batch (all of them for ≤ 32 clusters)
+  float* recv;           // [2][CS][SL]
+  float* vsub;           // [SL] velocity of this CTA's sub-slice
+  float* vnew;           // [SL]
+  float* wnew;           // [SL] new weights of the sub-slice (staged until its flag is known)
+  int* badr;             // [2][CS][4] non-finite flags pushed by the slice owners
+  uint64_t* mbp;         // [2] partial rows arrived
+  uint64_t* mbw;         // [2] new weights arrived
+  int crank, cid, NC, e0, SS, s0, s1;
+  unsigned epoch;
+  unsigned long long accepted, rejected;
+  int last_status;
+  bool sgd;
+
+  __device__ static uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+  __device__ static uint32_t mapa(const void* p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sa(p)), "r"(rank));
+    return r;
+  }
+  __device__ static void st_async(uint32_t addr, float4 v, uint32_t mbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
+        : "memory");
+  }
+  __device__ static void wait(uint64_t* bar, unsigned parity) {
+    for (long long spin = 0;; ++spin) {
+      uint32_t done;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(sa(bar)), "r"(parity)
+          : "memory");
+      if (done) return;
+      if (spin > (1ll << 28)) __trap();  // never hang the GPU on a protocol bug
+    }
+  }
+  __device__ static void st_tag(unsigned long long* p, float v, unsigned tag) {
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+  }
+  __device__ static unsigned long long ld_tag(const unsigned long long* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+  }
+
+  // smem: recv (2·CS·SL floats), vsub / vnew / wnew (SL each), badr (8·CS ints), 4 mbarriers
+  static constexpr int smem_floats() { return 2 * CS * SL + 3 * SL + 8 * CS + 8; }
+
+  __device__ void init(const StepArgs& a, cg::cluster_group& cluster, float* base) {
+    recv = base;
+    vsub = recv + 2 * CS * SL;
+    vnew = vsub + SL;
+    wnew = vnew + SL;
+    badr = reinterpret_cast<int*>(wnew + SL);
+    mbp = reinterpret_cast<uint64_t*>(badr + 8 * CS);  // 8-byte aligned: offsets are multiples of 4 floats
+    mbw = mbp + 2;
+    crank = (int)cluster.block_rank();
+    cid = blockIdx.x / CS;
+    NC = gridDim.x / CS;
+    e0 = crank * SL;
+    SS = (((SL + NC - 1) / NC) + 3) & ~3;
+    s0 = e0 + cid * SS;
+    s1 = min(min(e0 + SL, E), s0 + SS);
+    epoch = __ldcg(a.bar);
+    accepted = rejected = 0;
+    last_status = 0;
+    sgd = a.mode == MODE_SGD;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 2; ++i) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(mbp + i)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(mbw + i)));
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+
+  __device__ void load_state(const float* gw, const float* gv, float* wbuf) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) wbuf[p] = __ldcg(gw + p);
+    if (sgd)
+      for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) vsub[e - s0] = e < P ? __ldcg(gv + e) : 0.f;
+  }
+
+  // wparts: nw warp partials [nw][pstride] (P gradient entries + loss slot);
+  // their sum (warp order) is the CTA partial, formed while pushing.
+  __device__ void exchange(const StepArgs& a, int r, const float* wparts, int nw, int pstride,
+                           float*& wa, float*& wb, unsigned long long* pr) {
+    ++epoch;
+    const int par = epoch & 1;                 // L2 rows: epoch parity (survives launches)
+    const int mb = r & 1;                      // mbarriers: re-initialised per launch
+    const unsigned ph = (unsigned)(r >> 1) & 1;
+    const unsigned tag = epoch << 1;
+    if (threadIdx.x == 0) {  // arm: bytes the peers will push this round
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(mbp + mb)),
+                   "r"(CS * SL * 4)
+                   : "memory");
+      if (sgd)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(mbw + mb)),
+                     "r"(CS * (SL * 4 + 16))
+                     : "memory");
+    }
+    // (a) slice q of the CTA partial (Σ warp partials, warp order) → peer q
+    for (int i = threadIdx.x; i < CS * (SL / 4); i += blockDim.x) {
+      const int q = i / (SL / 4), k = 4 * (i % (SL / 4));
+      const int e = q * SL + k;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < E) {
+        v = reinterpret_cast<const float4*>(wparts + e)[0];
+        for (int w = 1; w < nw; ++w) {
+          const float4 u = reinterpret_cast<const float4*>(wparts + (long long)w * pstride + e)[0];
+          v.x += u.x;
+          v.y += u.y;
+          v.z += u.z;
+          v.w += u.w;
+        }
+      }
+      st_async(mapa(recv + (mb * CS + crank) * SL + k, q), v, mapa(mbp + mb, q));
+    }
+    wait(mbp + mb, ph);
+    if (pr && threadIdx.x == 0) pr[4] = globaltimer();
+    // (b) cluster partial of slice j → tagged L2 row
+    unsigned long long* rows = a.tpart + (long long)par * NC * EP;
+    for (int k = threadIdx.x; k < SL; k += blockDim.x) {
+      float t = 0.0f;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) t += recv[(mb * CS + q) * SL + k];
+      st_tag(rows + (long long)cid * EP + e0 + k, t, tag);
+    }
+    if (pr && threadIdx.x == 0) pr[5] = globaltimer();
+    // (c) sub-slice [s0, s1) over the NC clusters (cluster order) → sgd_step
+    unsigned long long* tw = a.tw + (long long)par * EP;
+    int bad = 0;
+    for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
+      float t = 0.0f;
+      for (int c0 = 0; c0 < NC; c0 += kRowBatch) {
+        unsigned long long v[kRowBatch];
+        bool ok;
+        long long spin = 0;
+        do {
+          if (++spin > (1ll << 26)) __trap();  // never hang the GPU on a protocol bug
+          ok = true;
+#pragma unroll
+          for (int i = 0; i < kRowBatch; ++i) {
+            v[i] = c0 + i < NC ? ld_tag(rows + (long long)(c0 + i) * EP + e) : ((unsigned long long)tag << 32);
+            ok &= (unsigned)(v[i] >> 32) == tag;
+          }
+        } while (!ok);
+#pragma unroll
+        for (int i = 0; i < kRowBatch; ++i)
+          if (c0 + i < NC) t += __uint_as_float((unsigned)v[i]);
+      }
+      if (e == P) {
+        if (a.loss_out) a.loss_out[r] = t;
+      } else if (a.mode == MODE_GRAD) {
+        a.g_out[e] = t;
+      } else if (sgd) {
+        bad |= !is_finite_f(t);
+        // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v
+        const float vn = fmaf(a.mu, vsub[e - s0], -a.lr * t);
+        vnew[e - s0] = vn;
+        wnew[e - s0] = wa[e] + vn;
+      }
+    }
+    if (!sgd) {
+      __syncthreads();
+      return;
+    }
+    // publish the sub-slice once its non-finite bit is known (tag = 2·epoch + bit)
+    bad = __syncthreads_or(bad);
+    for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x)
+      if (e != P) st_tag(tw + e, wnew[e - s0], tag | (unsigned)bad);
+    // weights-row elements that no sub-slice owns (e ≥ E, e == P) get a plain tag
+    if (cid == 0)
+      for (int e = max(E - 1, e0) + threadIdx.x; e < e0 + SL; e += blockDim.x)
+        if (e >= E || e == P) st_tag(tw + e, 0.0f, tag);
+    if (pr && threadIdx.x == 0) pr[6] = globaltimer();
+    // (d) gather slice j of the new weights, OR the flags, push to the cluster
+    int sbad = 0;
+    for (int k = 4 * threadIdx.x; k < SL; k += 4 * blockDim.x) {
+      unsigned long long v[4];
+      bool ok;
+      long long spin = 0;
+      do {
+        if (++spin > (1ll << 26)) __trap();
+        ok = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[i] = ld_tag(tw + e0 + k + i);
+          ok &= ((unsigned)(v[i] >> 32) | 1u) == (tag | 1u);
+        }
+      } while (!ok);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sbad |= (int)((v[i] >> 32) & 1u);
+      const float4 w4 = make_float4(__uint_as_float((unsigned)v[0]), __uint_as_float((unsigned)v[1]),
+                                    __uint_as_float((unsigned)v[2]), __uint_as_float((unsigned)v[3]));
+#pragma unroll
+      for (int q = 0; q < CS; ++q) st_async(mapa(wb + e0 + k, q), w4, mapa(mbw + mb, q));
+    }
+    sbad = __syncthreads_or(sbad);
+    if (threadIdx.x < CS)
+      st_async(mapa(badr + (mb * CS + crank) * 4, threadIdx.x), make_float4(__int_as_float(sbad), 0.f, 0.f, 0.f),
+               mapa(mbw + mb, threadIdx.x));
+    if (pr && threadIdx.x == 0) pr[7] = globaltimer();
+    // (e) all CS slices + flags landed → commit or reject
+    wait(mbw + mb, ph);
+    if (pr && threadIdx.x == 0) pr[13] = globaltimer();
+    int rej = 0;
+#pragma unroll
+    for (int q = 0; q < CS; ++q) rej |= badr[(mb * CS + q) * 4];
+    if (rej) {
+      ++rejected;
+      last_status = 2;  // GHC_ERR_NONFINITE: keep w/v (optim.cpp:49-51)
+    } else {
+      for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) vsub[e - s0] = vnew[e - s0];
+      float* t = wa;
+      wa = wb;
+      wb = t;
+      ++accepted;
+      last_status = 0;
+    }
+    __syncthreads();
+  }
+
+  __device__ void publish(const StepArgs& a, float* gw, float* gv, const float* wa,
+                          unsigned long long round0) {
+    if (sgd) {
+      if (cid == 0)
+        for (int e = threadIdx.x; e < P; e += blockDim.x) gw[e] = wa[e];
+      for (int e = s0 + threadIdx.x; e < s1 && e < P; e += blockDim.x) gv[e] = vsub[e - s0];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.bar[0] = epoch;
+      if (sgd) {
+        a.ms->version += accepted;
+        a.ms->rejected += rejected;
+        a.ms->round = round0 + (unsigned long long)a.rounds;
+        a.ms->status = last_status;
+      }
+    }
+  }
+};
+
 template <int D, int H, int T, int K, int CS>
 struct RoundLayout {
   using N = LstmNet<D, H, T, K>;
@@ -43,9 +309,12 @@ struct RoundLayout {
   static constexpr int E = N::P + 1;                          // grad + loss
   static constexpr int SL = (((E + CS - 1) / CS) + 3) & ~3;   // slice per cluster rank
   static constexpr int EP = SL * CS;                          // padded row
+  // weight buffers receive whole slices (st.async) → at least EP floats
+  static constexpr int WBP = N::PPAD > EP ? N::PPAD : EP;
+  static constexpr int RSF = ClusterRS<N::P, SL, EP, CS>::smem_floats();
   static size_t smem_bytes(int nw) {
-    return sizeof(float) *
-           (size_t)(2 * N::PPAD + nw * SPW * N::WARP_FLOATS + nw * N::PPAD + 2 * SL + CS + 8);
+    return sizeof(float) * (size_t)(2 * WBP + nw * SPW * N::WARP_FLOATS + nw * N::PPAD + 2 * SL +
+                                    ((CS + 3) & ~3) + RSF);
   }
 };
 
@@ -316,12 +585,15 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   const int NW = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* wbuf0 = smem;
-  float* wbuf1 = smem + N::PPAD;
-  float* ws = smem + 2 * N::PPAD + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
-  float* wpart = smem + 2 * N::PPAD + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
+  float* wbuf1 = smem + RL::WBP;
+  float* ws = smem + 2 * RL::WBP + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
+  float* wpart = smem + 2 * RL::WBP + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
   float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
-  ClusterXchg<N::P, SL, RL::EP, CS> xc;
+  ClusterXchg<N::P, SL, RL::EP, CS> xc;                        // cross-rank exchange (GX > 1)
   xc.init(a, cluster, vsl, vsl + SL, reinterpret_cast<int*>(vsl + 2 * SL));
+  ClusterRS<N::P, SL, RL::EP, CS> rs;                          // single-GPU exchange (default)
+  const bool single = a.GX <= 1;
+  if (single) rs.init(a, cluster, vsl + 2 * SL + ((CS + 3) & ~3));
 
   unsigned long long round0 = 0;
   int cur = 0;
@@ -332,7 +604,9 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   }
   float* gw = sgd ? (cur ? a.w1 : a.w0) : nullptr;  // master weights in HBM
   float* gv = sgd ? (cur ? a.v1 : a.v0) : nullptr;
-  xc.load_state(a, sgd ? gw : a.w_in, gv, wbuf0);
+  if (single) rs.load_state(sgd ? gw : a.w_in, gv, wbuf0);
+  else xc.load_state(a, sgd ? gw : a.w_in, gv, wbuf0);
+  if (single) cluster.sync();  // peers' mbarriers initialised before any st.async
   float* wa = wbuf0;  // weights the samples use
   float* wb = wbuf1;  // peers deposit the next weights here
 
@@ -489,7 +763,9 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     __syncthreads();
     if (pr && threadIdx.x == 0) pr[2] = globaltimer();
 
-    // ---- (1) CTA partial in smem: wpart[0] += wpart[1..NW-1] (fixed order) ----
+    // ---- (1) CTA partial in smem: wpart[0] += wpart[1..NW-1] (fixed order);
+    //      the single-GPU exchange forms it while pushing (ClusterRS (a)) ----
+    if (!single)
     for (int p = threadIdx.x; p < N::PPAD / 4; p += blockDim.x) {
       float4 t = reinterpret_cast<const float4*>(wpart)[p];
       for (int w2 = 1; w2 < NW; ++w2) {
@@ -502,13 +778,21 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       reinterpret_cast<float4*>(wpart)[p] = t;
     }
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
-    cluster.sync();  // CTA partials of the whole cluster complete
-    if (pr && threadIdx.x == 0) pr[4] = globaltimer();
-
-    xc.exchange(a, cluster, r, wpart, wa, wb, pr);
+    if (single) {
+      rs.exchange(a, r, wpart, NW, N::PPAD, wa, wb, pr);
+    } else {
+      cluster.sync();  // CTA partials of the whole cluster complete
+      if (pr && threadIdx.x == 0) pr[4] = globaltimer();
+      xc.exchange(a, cluster, r, wpart, wa, wb, pr);
+    }
   }
 
-  xc.publish(a, gw, gv, wa, round0);
+  if (single) {
+    rs.publish(a, gw, gv, wa, round0);
+    cluster.sync();  // no CTA leaves while a peer may still address its shared memory
+  } else {
+    xc.publish(a, gw, gv, wa, round0);
+  }
 }
 
 }  // namespace ghc

@@ -71,6 +71,8 @@ struct StepArgs {
   int rank0;              // global rank of this grid's first virtual rank
   long long idx_vstride;
   float* gpart[kMaxRanks];     // per rank: tagged receive rows uint2[2][GX][EP] (peer-mapped)
+  unsigned long long* tpart;   // single-GPU exchange: tagged cluster rows [2][clusters][EP]
+  unsigned long long* tw;      // single-GPU exchange: tagged new weights [2][EP]
   unsigned* gcnt[kMaxRanks];   // per rank: line [CS*kFlagStride] keeps the exchange epoch
 };
 
