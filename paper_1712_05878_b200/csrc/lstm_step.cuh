@@ -221,38 +221,44 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   if (pr && lane == 0) pr[8] = globaltimer();
 
   // ---------------- forward recurrence (nn.cpp:160-200) ----------------
+  // Packed FP32x2 FMAs (FFMA2, sm_100): each gate keeps two partial sums
+  // (even / odd input index) — one FFMA2 advances both with the same rounding
+  // as two FFMAs, so results are bit-identical to the scalar loop at half the
+  // issue slots (3-register FFMA issues once per 2 cycles per SM sub-partition).
   {
-    float wx[4][D], wh[4][H], bb[4];
+    constexpr int DH = D / 2, HH = H / 2;
+    float2 wxp[4][DH > 0 ? DH : 1], whp[4][HH > 0 ? HH : 1];
+    float wxt[4], wht[4], bb[4];  // odd-length tails (into the even partial sum)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      const float* rx = wsm + N::OFF_WX + (q * H + j) * D;
+      const float* rh = wsm + N::OFF_WH + (q * H + j) * H;
       bb[q] = wsm[N::OFF_B + q * H + j];
 #pragma unroll
-      for (int d = 0; d < D; ++d) wx[q][d] = wsm[N::OFF_WX + (q * H + j) * D + d];
+      for (int m = 0; m < DH; ++m) wxp[q][m] = make_float2(rx[2 * m], rx[2 * m + 1]);
 #pragma unroll
-      for (int k = 0; k < H; ++k) wh[q][k] = wsm[N::OFF_WH + (q * H + j) * H + k];
+      for (int m = 0; m < HH; ++m) whp[q][m] = make_float2(rh[2 * m], rh[2 * m + 1]);
+      wxt[q] = (D & 1) ? rx[D - 1] : 0.0f;
+      wht[q] = (H & 1) ? rh[H - 1] : 0.0f;
     }
     float c[SPW];
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp) c[sp] = 0.0f;
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
-      float a0[SPW][4], a1[SPW][4];
+      float2 acc[SPW][4];  // (Σ even-index terms + bias, Σ odd-index terms)
 #pragma unroll
       for (int sp = 0; sp < SPW; ++sp) {
         float xv[DP];
         load_x(sp, t, xv);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          a0[sp][q] = bb[q];
-          a1[sp][q] = 0.0f;
+          acc[sp][q] = make_float2(bb[q], 0.0f);
+#pragma unroll
+          for (int m = 0; m < DH; ++m)
+            acc[sp][q] = __ffma2_rn(wxp[q][m], make_float2(xv[2 * m], xv[2 * m + 1]), acc[sp][q]);
+          if (D & 1) acc[sp][q].x = fmaf(wxt[q], xv[D - 1], acc[sp][q].x);
         }
-#pragma unroll
-        for (int d = 0; d < D; ++d)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (d & 1) a1[sp][q] = fmaf(wx[q][d], xv[d], a1[sp][q]);
-            else a0[sp][q] = fmaf(wx[q][d], xv[d], a0[sp][q]);
-          }
       }
       if (t > 0) {
 #pragma unroll
@@ -260,14 +266,23 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
           float hv[H];
           load_h(sp, t - 1, hv);
 #pragma unroll
-          for (int k = 0; k < H; ++k)
+          for (int m = 0; m < HH; ++m)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (k & 1) a1[sp][q] = fmaf(wh[q][k], hv[k], a1[sp][q]);
-              else a0[sp][q] = fmaf(wh[q][k], hv[k], a0[sp][q]);
-            }
+            for (int q = 0; q < 4; ++q)
+              acc[sp][q] = __ffma2_rn(whp[q][m], make_float2(hv[2 * m], hv[2 * m + 1]), acc[sp][q]);
+          if (H & 1)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[sp][q].x = fmaf(wht[q], hv[H - 1], acc[sp][q].x);
         }
       }
+      float a0[SPW][4], a1[SPW][4];
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a0[sp][q] = acc[sp][q].x;
+          a1[sp][q] = acc[sp][q].y;
+        }
 #pragma unroll
       for (int sp = 0; sp < SPW; ++sp) {
         const float ig = sigmoid_f(a0[sp][0] + a1[sp][0]);
@@ -385,16 +400,14 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp) {
           const float4* dz4 = reinterpret_cast<const float4*>(dzs[sp] + t * 4 * H);
-          float p[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          float2 p01 = make_float2(0.0f, 0.0f), p23 = make_float2(0.0f, 0.0f);  // FFMA2 pairs
 #pragma unroll
           for (int r4 = 0; r4 < H; ++r4) {
             const float4 u = dz4[r4];
-            p[0] = fmaf(wt[4 * r4], u.x, p[0]);
-            p[1] = fmaf(wt[4 * r4 + 1], u.y, p[1]);
-            p[2] = fmaf(wt[4 * r4 + 2], u.z, p[2]);
-            p[3] = fmaf(wt[4 * r4 + 3], u.w, p[3]);
+            p01 = __ffma2_rn(make_float2(wt[4 * r4], wt[4 * r4 + 1]), make_float2(u.x, u.y), p01);
+            p23 = __ffma2_rn(make_float2(wt[4 * r4 + 2], wt[4 * r4 + 3]), make_float2(u.z, u.w), p23);
           }
-          dh[sp] = (p[0] + p[1]) + (p[2] + p[3]);
+          dh[sp] = (p01.x + p01.y) + (p23.x + p23.y);
           dc[sp] *= fgs[sp];
         }
       }
