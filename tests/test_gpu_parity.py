@@ -20,15 +20,17 @@ import paper_1712_05878_b200 as g
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["tc", "simt"])
+@pytest.fixture(autouse=True, params=["simt", "tc", "flat"])
 def step_variant(request, monkeypatch):
-    """Every parity case runs on both cluster-round variants: the SIMT kernel
-    (default, lstm_round.cuh) and the tensor-core kernel (GHC_STEP=tc,
-    lstm_tc.cuh).  The variant is fixed when a plan is created."""
-    if request.param == "tc":
-        monkeypatch.setenv("GHC_STEP", "tc")
-    else:
+    """Every parity case runs on all three fused-step variants: the SIMT
+    cluster kernel with the reduce-scatter exchange (default, lstm_round.cuh),
+    the tensor-core kernel (GHC_STEP=tc, lstm_tc.cuh) and the flat
+    grid-barrier kernel (GHC_STEP=flat, lstm_step.cuh).  The variant is fixed
+    when a plan is created."""
+    if request.param == "simt":
         monkeypatch.delenv("GHC_STEP", raising=False)
+    else:
+        monkeypatch.setenv("GHC_STEP", request.param)
     return request.param
 
 SHAPES = [BENCH_ARCH, "lstm(5,8,10),softmax(8,3)", "lstm(3,4,5),softmax(4,3)",
