@@ -343,9 +343,9 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     if (p->max_clusters * p->cluster_size > p->max_ctas) p->max_ctas = p->max_clusters * p->cluster_size;
   }
   CU(cudaMalloc(&p->part, sizeof(float) * static_cast<size_t>(p->max_ctas) * p->lstm->ppad));
-  {  // tagged rows of the single-GPU exchange: [2][clusters][EP] + [2][EP], tags start at 0
+  {  // tagged rows of the exchange: [2][clusters][EP] + weights [ranks][2][EP], tags start at 0
     const size_t ep = static_cast<size_t>(std::max(p->lstm->ep[0], p->lstm->ep[1]));
-    const size_t n = 2 * static_cast<size_t>(p->max_ctas) * ep + 2 * ep;
+    const size_t n = 2 * static_cast<size_t>(p->max_ctas) * ep + 2 * kMaxRanks * ep;  // + weights per rank
     CU(cudaMalloc(&p->tpart, sizeof(unsigned long long) * n));
     CU(cudaMemset(p->tpart, 0, sizeof(unsigned long long) * n));
     p->tw = p->tpart + 2 * static_cast<size_t>(p->max_ctas) * ep;

@@ -66,7 +66,9 @@ struct ClusterRS {
   uint64_t* mbp;         // [2] partial rows arrived
   uint64_t* mbw;         // [2] new weights arrived
   int crank, cid, NC, e0, SS, s0, s1;
-  unsigned epoch;
+  int GX, NCr, vrank, rank, cl;  // ranks; clusters per rank; this CTA's (virtual) rank, cluster in rank
+  unsigned epoch;   // this plan's round counter: tags of the rank-local rows
+  unsigned xepoch;  // the cross-rank exchange's counter (kept with its buffers, equal on all ranks)
   unsigned long long accepted, rejected;
   int last_status;
   bool sgd;
@@ -121,10 +123,16 @@ struct ClusterRS {
     cid = blockIdx.x / CS;
     NC = gridDim.x / CS;
     e0 = crank * SL;
-    SS = (((SL + NC - 1) / NC) + 3) & ~3;
-    s0 = e0 + cid * SS;
+    GX = max(1, a.GX);
+    NCr = NC / max(1, a.VR);
+    vrank = cid / NCr;
+    cl = cid % NCr;
+    rank = a.rank0 + vrank;
+    SS = (((SL + NCr - 1) / NCr) + 3) & ~3;
+    s0 = e0 + cl * SS;
     s1 = min(min(e0 + SL, E), s0 + SS);
     epoch = __ldcg(a.bar);
+    xepoch = GX > 1 ? __ldcg(a.gcnt[rank] + CS * kFlagStride) : 0u;
     accepted = rejected = 0;
     last_status = 0;
     sgd = a.mode == MODE_SGD;
@@ -143,11 +151,46 @@ struct ClusterRS {
       for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) vsub[e - s0] = e < P ? __ldcg(gv + e) : 0.f;
   }
 
+  // Push this rank's sum of element e into row `rank` of every rank's receive
+  // rows (uint64 [2][GX][EP], P2P-mapped; system scope — the ranks are other
+  // GPUs), then poll this rank's copy of the GX rows and sum in rank order.
+  __device__ float cross_rank_sum(const StepArgs& a, int par, int e, float mine, unsigned tag) const {
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(mine);
+    for (int q = 0; q < GX; ++q) {
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.gpart[q]) +
+                                ((long long)par * GX + rank) * EP + e;
+      asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+    }
+    const unsigned long long* src =
+        reinterpret_cast<const unsigned long long*>(a.gpart[rank]) + (long long)par * GX * EP + e;
+    unsigned long long v[kMaxRanks];
+    bool ok;
+    long long spin = 0;
+    do {
+      if (++spin > (1ll << 26)) __trap();
+      ok = true;
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q) {
+        if (q >= GX) break;
+        asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v[q]) : "l"(src + (long long)q * EP) : "memory");
+        ok &= (unsigned)(v[q] >> 32) == tag;
+      }
+    } while (!ok);
+    float t = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q) {
+      if (q >= GX) break;
+      t += __uint_as_float((unsigned)v[q]);
+    }
+    return t;
+  }
+
   // wparts: nw warp partials [nw][pstride] (P gradient entries + loss slot);
   // their sum (warp order) is the CTA partial, formed while pushing.
   __device__ void exchange(const StepArgs& a, int r, const float* wparts, int nw, int pstride,
                            float*& wa, float*& wb, unsigned long long* pr) {
     ++epoch;
+    ++xepoch;
     const int par = epoch & 1;                 // L2 rows: epoch parity (survives launches)
     const int mb = r & 1;                      // mbarriers: re-initialised per launch
     const unsigned ph = (unsigned)(r >> 1) & 1;
@@ -189,12 +232,16 @@ struct ClusterRS {
       st_tag(rows + (long long)cid * EP + e0 + k, t, tag);
     }
     if (pr && threadIdx.x == 0) pr[5] = globaltimer();
-    // (c) sub-slice [s0, s1) over the NC clusters (cluster order) → sgd_step
-    unsigned long long* tw = a.tw + (long long)par * EP;
+    // (c) sub-slice [s0, s1) over this rank's NCr clusters (cluster order);
+    //     GX ranks: + one hop over NVLink — push the rank sum, tagged, into
+    //     row `rank` of every rank's receive rows, then sum the GX rows in rank
+    //     order (bit-identical on every rank) → sgd_step
+    unsigned long long* tw = a.tw + ((long long)vrank * 2 + par) * EP;
+    const unsigned long long* myrows = rows + (long long)vrank * NCr * EP;
     int bad = 0;
     for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
       float t = 0.0f;
-      for (int c0 = 0; c0 < NC; c0 += kRowBatch) {
+      for (int c0 = 0; c0 < NCr; c0 += kRowBatch) {
         unsigned long long v[kRowBatch];
         bool ok;
         long long spin = 0;
@@ -203,14 +250,15 @@ struct ClusterRS {
           ok = true;
 #pragma unroll
           for (int i = 0; i < kRowBatch; ++i) {
-            v[i] = c0 + i < NC ? ld_tag(rows + (long long)(c0 + i) * EP + e) : ((unsigned long long)tag << 32);
+            v[i] = c0 + i < NCr ? ld_tag(myrows + (long long)(c0 + i) * EP + e) : ((unsigned long long)tag << 32);
             ok &= (unsigned)(v[i] >> 32) == tag;
           }
         } while (!ok);
 #pragma unroll
         for (int i = 0; i < kRowBatch; ++i)
-          if (c0 + i < NC) t += __uint_as_float((unsigned)v[i]);
+          if (c0 + i < NCr) t += __uint_as_float((unsigned)v[i]);
       }
+      if (GX > 1) t = cross_rank_sum(a, xepoch & 1, e, t, xepoch);
       if (e == P) {
         if (a.loss_out) a.loss_out[r] = t;
       } else if (a.mode == MODE_GRAD) {
@@ -232,7 +280,7 @@ struct ClusterRS {
     for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x)
       if (e != P) st_tag(tw + e, wnew[e - s0], tag | (unsigned)bad);
     // weights-row elements that no sub-slice owns (e ≥ E, e == P) get a plain tag
-    if (cid == 0)
+    if (cl == 0)
       for (int e = max(E - 1, e0) + threadIdx.x; e < e0 + SL; e += blockDim.x)
         if (e >= E || e == P) st_tag(tw + e, 0.0f, tag);
     if (pr && threadIdx.x == 0) pr[6] = globaltimer();
@@ -292,6 +340,8 @@ struct ClusterRS {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       a.bar[0] = epoch;
+      if (GX > 1)
+        for (int v = 0; v < max(1, a.VR); ++v) a.gcnt[a.rank0 + v][CS * kFlagStride] = xepoch;
       if (sgd) {
         a.ms->version += accepted;
         a.ms->rejected += rejected;
@@ -589,24 +639,20 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   float* ws = smem + 2 * RL::WBP + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
   float* wpart = smem + 2 * RL::WBP + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
   float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
-  ClusterXchg<N::P, SL, RL::EP, CS> xc;                        // cross-rank exchange (GX > 1)
-  xc.init(a, cluster, vsl, vsl + SL, reinterpret_cast<int*>(vsl + 2 * SL));
-  ClusterRS<N::P, SL, RL::EP, CS> rs;                          // single-GPU exchange (default)
-  const bool single = a.GX <= 1;
-  if (single) rs.init(a, cluster, vsl + 2 * SL + ((CS + 3) & ~3));
+  ClusterRS<N::P, SL, RL::EP, CS> rs;  // the round's exchange (one GPU or GX ranks)
+  rs.init(a, cluster, vsl + 2 * SL + ((CS + 3) & ~3));
 
   unsigned long long round0 = 0;
   int cur = 0;
-  const bool sgd = xc.sgd;
+  const bool sgd = rs.sgd;
   if (sgd) {
     cur = __ldcg(&a.ms->cur);
     round0 = __ldcg(&a.ms->round);
   }
   float* gw = sgd ? (cur ? a.w1 : a.w0) : nullptr;  // master weights in HBM
   float* gv = sgd ? (cur ? a.v1 : a.v0) : nullptr;
-  if (single) rs.load_state(sgd ? gw : a.w_in, gv, wbuf0);
-  else xc.load_state(a, sgd ? gw : a.w_in, gv, wbuf0);
-  if (single) cluster.sync();  // peers' mbarriers initialised before any st.async
+  rs.load_state(sgd ? gw : a.w_in, gv, wbuf0);
+  cluster.sync();  // peers' mbarriers initialised before any st.async
   float* wa = wbuf0;  // weights the samples use
   float* wb = wbuf1;  // peers deposit the next weights here
 
@@ -621,13 +667,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   const int GX = max(1, a.GX);
   auto n_of = [&](int r, int q) { return a.counts ? __ldg(a.counts + (long long)r * GX + q) : a.n; };
   auto first_sample = [&](int r, int& s, int& s1) {
-    const int n = n_of(r, xc.rank);
+    const int n = n_of(r, rs.rank);
     const int spc = (n + Gr - 1) / Gr;
     const int s0 = lb * spc;
     s1 = min(n, s0 + spc);
     s = s0 + warp;
   };
-  const int32_t* idxv = a.idx ? a.idx + (long long)xc.vrank * a.idx_vstride : nullptr;
+  const int32_t* idxv = a.idx ? a.idx + (long long)rs.vrank * a.idx_vstride : nullptr;
   auto slot_x = [&](int sp, int b) { return ws + sp * N::WARP_FLOATS + N::S_X + b * N::XWP; };
   auto slot_l = [&](int sp) { return reinterpret_cast<int*>(ws + sp * N::WARP_FLOATS + N::S_L); };
   auto fetch_nocommit = [&](int sp, int row, int b) {
@@ -763,36 +809,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     __syncthreads();
     if (pr && threadIdx.x == 0) pr[2] = globaltimer();
 
-    // ---- (1) CTA partial in smem: wpart[0] += wpart[1..NW-1] (fixed order);
-    //      the single-GPU exchange forms it while pushing (ClusterRS (a)) ----
-    if (!single)
-    for (int p = threadIdx.x; p < N::PPAD / 4; p += blockDim.x) {
-      float4 t = reinterpret_cast<const float4*>(wpart)[p];
-      for (int w2 = 1; w2 < NW; ++w2) {
-        const float4 u = reinterpret_cast<const float4*>(wpart + w2 * N::PPAD)[p];
-        t.x += u.x;
-        t.y += u.y;
-        t.z += u.z;
-        t.w += u.w;
-      }
-      reinterpret_cast<float4*>(wpart)[p] = t;
-    }
+    // (the CTA partial — Σ warp partials, warp order — is formed by ClusterRS (a))
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
-    if (single) {
-      rs.exchange(a, r, wpart, NW, N::PPAD, wa, wb, pr);
-    } else {
-      cluster.sync();  // CTA partials of the whole cluster complete
-      if (pr && threadIdx.x == 0) pr[4] = globaltimer();
-      xc.exchange(a, cluster, r, wpart, wa, wb, pr);
-    }
+    rs.exchange(a, r, wpart, NW, N::PPAD, wa, wb, pr);
   }
 
-  if (single) {
-    rs.publish(a, gw, gv, wa, round0);
-    cluster.sync();  // no CTA leaves while a peer may still address its shared memory
-  } else {
-    xc.publish(a, gw, gv, wa, round0);
-  }
+  rs.publish(a, gw, gv, wa, round0);
+  cluster.sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
 }  // namespace ghc

@@ -65,15 +65,10 @@ def main():
         mc = maxc // G
         warps = min(8, max(1, -(-B // (mc * cs * spw))))
         ctas = min(mc, -(-(-(-B // (warps * spw))) // cs)) * cs * G
-        if G > 1:  # cross-rank path: cluster barriers + column barrier + tagged P2P rows
-            bounds = [(0, 2, "samples"), (2, 3, "cta_partial"), (3, 4, "cluster_sync1"),
-                      (4, 5, "dsmem_reduce_store"), (5, 6, "column_barrier"),
-                      (6, 14, "x_subslice_reduce_push"), (14, 15, "x_arrival_wait"),
-                      (15, 7, "rank_sum_sgd_bcast"), (7, 13, "cluster_sync2")]
-        else:      # single GPU: ClusterRS (st.async pushes + tagged L2 rows)
-            bounds = [(0, 2, "samples"), (2, 3, "cta_partial"), (3, 4, "push_partials_wait"),
-                      (4, 5, "cluster_row_store"), (5, 6, "subslice_poll_sgd_store"),
-                      (6, 7, "weights_gather_push"), (7, 13, "weights_wait")]
+        # ClusterRS (st.async pushes + tagged L2 rows; G > 1 adds the NVLink hop in (c))
+        bounds = [(0, 2, "samples"), (2, 3, "cta_partial"), (3, 4, "push_partials_wait"),
+                  (4, 5, "cluster_row_store"), (5, 6, "subslice_poll_sgd_store"),
+                  (6, 7, "weights_gather_push"), (7, 13, "weights_wait")]
         last = 13
     else:          # = step_geometry()
         sms = ctx.num_sms
