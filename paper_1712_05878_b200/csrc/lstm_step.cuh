@@ -236,8 +236,17 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
       bb[q] = wsm[N::OFF_B + q * H + j];
 #pragma unroll
       for (int m = 0; m < DH; ++m) wxp[q][m] = make_float2(rx[2 * m], rx[2 * m + 1]);
+      if constexpr (N::HV) {  // row of Wh: 16-B aligned, lane stride 4H floats → conflict-free LDS.128
 #pragma unroll
-      for (int m = 0; m < HH; ++m) whp[q][m] = make_float2(rh[2 * m], rh[2 * m + 1]);
+        for (int m = 0; m < H / 4; ++m) {
+          const float4 u = reinterpret_cast<const float4*>(rh)[m];
+          whp[q][2 * m] = make_float2(u.x, u.y);
+          whp[q][2 * m + 1] = make_float2(u.z, u.w);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < HH; ++m) whp[q][m] = make_float2(rh[2 * m], rh[2 * m + 1]);
+      }
       wxt[q] = (D & 1) ? rx[D - 1] : 0.0f;
       wht[q] = (H & 1) ? rh[H - 1] : 0.0f;
     }
