@@ -666,7 +666,17 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   const int lb = blockIdx.x % Gr;
   const int GX = max(1, a.GX);
   auto n_of = [&](int r, int q) { return a.counts ? __ldg(a.counts + (long long)r * GX + q) : a.n; };
+  // Without per-round counts every round has the same sample range and scale:
+  // computed once (the integer division by the CTA count is a serial chain).
+  const bool fixed_n = a.counts == nullptr;
+  const int fs_spc = (a.n + Gr - 1) / Gr;
+  const int fs_s0 = lb * fs_spc, fs_s1 = min(a.n, fs_s0 + fs_spc);
   auto first_sample = [&](int r, int& s, int& s1) {
+    if (fixed_n) {
+      s1 = fs_s1;
+      s = fs_s0 + warp;
+      return;
+    }
     const int n = n_of(r, rs.rank);
     const int spc = (n + Gr - 1) / Gr;
     const int s0 = lb * spc;
@@ -708,8 +718,11 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   __syncthreads();
 
   for (int r = 0; r < a.rounds; ++r) {
-    int ntot = 0;  // samples of round r over all ranks (SPEC.md:358-366 weighted mean)
-    for (int q = 0; q < GX; ++q) ntot += n_of(r, q);
+    int ntot = GX * a.n;  // samples of round r over all ranks (SPEC.md:358-366 weighted mean)
+    if (!fixed_n) {
+      ntot = 0;
+      for (int q = 0; q < GX; ++q) ntot += n_of(r, q);
+    }
     const float scale = sgd ? 1.0f / (float)ntot : a.grad_scale;
     unsigned long long* pr =
         a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
