@@ -66,6 +66,14 @@ ghc_status ghc_host_free(void* h_ptr);
 ghc_status ghc_memcpy_h2d(ghc_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);
 ghc_status ghc_memcpy_d2h(ghc_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
 ghc_status ghc_memcpy_d2d(ghc_ctx* ctx, void* d_dst, const void* d_src, size_t bytes);
+/* CUDA IPC of a ghc_malloc'd buffer (base pointer) for the async / EASGD
+ * mailboxes across processes (transport.hpp:22-44 "nvlink" backend, P2P
+ * copies): handle = GHC_IPC_HANDLE_BYTES bytes; ghc_memcpy_d2d moves data
+ * into / out of a mapped peer buffer over NVLink. */
+#define GHC_IPC_HANDLE_BYTES 64
+ghc_status ghc_ipc_handle(ghc_ctx* ctx, void* d_base, uint8_t* out_handle);
+ghc_status ghc_ipc_open(ghc_ctx* ctx, const uint8_t* handle, void** d_ptr);
+ghc_status ghc_ipc_close(ghc_ctx* ctx, void* d_ptr);
 ghc_status ghc_memset(ghc_ctx* ctx, void* d_dst, int value, size_t bytes);
 /* CUDA-event timer on the context stream: start, then stop returns ms. */
 ghc_status ghc_timer_start(ghc_ctx* ctx);
@@ -259,7 +267,6 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
 /* sgd_step — each rank holds a bit-identical master replica.            */
 /* ------------------------------------------------------------------ */
 typedef struct ghc_p2p ghc_p2p;
-#define GHC_IPC_HANDLE_BYTES 64
 /* Rank `rank` of an nranks (2..8) exchange over plan's fused kernel (the
  * same architecture, GPU model and batch size on every rank). */
 ghc_status ghc_p2p_create(ghc_plan* plan, int32_t rank, int32_t nranks, ghc_p2p** out);

@@ -68,6 +68,9 @@ SIGNATURES = [
     ("ghc_malloc", C.c_int, [_vp, _sz, _vp]),
     ("ghc_free", C.c_int, [_vp, _vp]),
     ("ghc_host_alloc", C.c_int, [_sz, _vp]),
+    ("ghc_ipc_handle", C.c_int, [_vp, _vp, _vp]),
+    ("ghc_ipc_open", C.c_int, [_vp, _vp, _vp]),
+    ("ghc_ipc_close", C.c_int, [_vp, _vp]),
     ("ghc_host_free", C.c_int, [_vp]),
     ("ghc_memcpy_h2d", C.c_int, [_vp, _vp, _vp, _sz]),
     ("ghc_memcpy_d2h", C.c_int, [_vp, _vp, _vp, _sz]),

@@ -163,6 +163,31 @@ ghc_status ghc_memcpy_d2d(ghc_ctx* c, void* d, const void* s, size_t bytes) {
   CU(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, c->stream));
   return GHC_OK;
 }
+// CUDA IPC of a ghc_malloc'd buffer (the async / EASGD mailboxes of
+// roles_dist.py: one process per GPU, data over NVLink P2P copies).
+ghc_status ghc_ipc_handle(ghc_ctx* c, void* d_base, uint8_t* out_handle) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == GHC_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CU(cudaSetDevice(c->device));
+  CU(cudaIpcGetMemHandle(&h, d_base));
+  std::memcpy(out_handle, &h, sizeof(h));
+  return GHC_OK;
+}
+ghc_status ghc_ipc_open(ghc_ctx* c, const uint8_t* handle, void** d_ptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CU(cudaSetDevice(c->device));
+  if (cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GHC_ERR_TRANSPORT, "ipc_open: cannot map the peer buffer");
+  }
+  return GHC_OK;
+}
+ghc_status ghc_ipc_close(ghc_ctx* c, void* d_ptr) {
+  CU(cudaSetDevice(c->device));
+  CU(cudaIpcCloseMemHandle(d_ptr));
+  return GHC_OK;
+}
 ghc_status ghc_memset(ghc_ctx* c, void* d, int v, size_t bytes) {
   CU(cudaMemsetAsync(d, v, bytes, c->stream));
   return GHC_OK;
