@@ -1,5 +1,6 @@
-"""Asynchronous Downpour and EASGD across processes (one per GPU): the SPEC
-roles with the exchange over NVLink P2P copies.
+"""Asynchronous Downpour, EASGD and hierarchical masters across processes
+(one per GPU): the SPEC roles with the exchange over NVLink
+P2P copies (the sync Downpour round has its own fused path, p2p.cu).
 
 BASELINE north_star: "gradient send and weight broadcast move over NVLink ...
 P2P copies in async mode".  Rank k is worker k; rank 0 also runs the master.
@@ -229,3 +230,160 @@ def run_easgd(arch: g.Architecture, spec, cfg, order, rank: int, world: int, dis
     dist.barrier()
     ipc.close()
     return out
+
+
+def run_hierarchical(arch: g.Architecture, spec, cfg, rank: int, world: int, dist):
+    """Hierarchical masters (SPEC.md:367-375, Topology::hierarchical
+    transport.cpp:520-531, oracle decision 2) across processes: cfg.groups
+    groups of world/groups workers; the sub-master of group q runs on the
+    group's first rank, the top master on rank 0.  Per round every group does
+    a sync Downpour step (workers → sub-master mailbox, sample-weighted combine
+    in rank order SPEC.md:358-366, sgd_step(lr, mu)); a group flushes after
+    flush_k updates (or when its data ends) by sending snapshot − current,
+    weighted by the samples it absorbed, to the top master, which combines the
+    flushing groups in group order, applies sgd_step(parent_lr, parent_mu) and
+    replies; the group adopts the reply as weights and snapshot.  All
+    transfers are CUDA-IPC device-to-device copies.  Returns worker_w on every
+    rank, group_w on sub-masters, top w on rank 0."""
+    ctx = arch.ctx
+    lib = ctx.lib
+    P = arch.n_params
+    G = cfg.groups
+    Wg = world // G
+    q, sub = rank // Wg, (rank // Wg) * Wg
+    wk = _Worker(arch, spec, cfg, world, rank)
+    counts = gd.round_counts(spec, world, cfg.batch_size, cfg.epochs, cfg.shuffle_seed)
+    R = counts.shape[0]
+    plan = _group_history(counts, R, G, Wg, cfg.flush_k)  # deterministic on every rank
+    ipc = _Ipc(ctx)
+    w0 = g.init_weights(arch, cfg.weight_seed).astype(np.float32)
+    if rank == sub:
+        mail = ctx.array(Wg * P)                # gradient slot of each group worker
+        stage = ctx.array(Wg * P)               # active slots, compacted in rank order
+        wg, vg, snap = ctx.upload(w0), ctx.array(P), ctx.upload(w0)
+        vg.zero()
+        comb, psd, vd = ctx.array(P), ctx.array(P), ctx.array(P)
+        st = ctx.array(1, np.int32)
+    if rank == 0:
+        tmail = ctx.array(G * P)                # pseudo-gradient slot of each group
+        tstage = ctx.array(G * P)
+        tw, tv, tcomb = ctx.upload(w0), ctx.array(P), ctx.array(P)
+        tv.zero()
+        tst = ctx.array(1, np.int32)
+    inbox_h = gd.allgather_bytes(dist, ipc.handle(wk.w))
+    mail_h = gd.allgather_bytes(dist, ipc.handle(mail) if rank == sub else b"")
+    wg_h = gd.allgather_bytes(dist, ipc.handle(wg) if rank == sub else b"")
+    tmail_h = gd.allgather_bytes(dist, ipc.handle(tmail) if rank == 0 else b"")[0]
+    if rank != sub:
+        my_slot = ipc.open(mail_h[sub]) + 4 * (rank - sub) * P
+    else:
+        inbox = {k: ipc.open(inbox_h[k]) for k in range(sub + 1, sub + Wg)}
+        top_slot = (tmail.ptr.value if rank == 0 else ipc.open(tmail_h)) + 4 * q * P
+    if rank == 0:
+        sub_wg = {qq: (wg.ptr.value if qq == 0 else ipc.open(wg_h[qq * Wg])) for qq in range(G)}
+
+    def sgd(w, v, gp, lr, mu, stat):
+        g.check(lib.ghc_sgd_apply(ctx.h, w.ptr, v.ptr, C.c_void_p(gp), P, lr, mu, stat.ptr, None),
+                "sgd_apply")
+
+    def combine(out, slots, stage_buf, weights):
+        """Σ c_i slot_i / Σ c_i over the slots with c_i > 0, in slot order."""
+        act = [i for i, c in enumerate(weights) if c > 0]
+        for n, i in enumerate(act):
+            _copy(ctx, stage_buf.ptr.value + 4 * n * P, slots.ptr.value + 4 * i * P, 4 * P)
+        wts = (C.c_double * len(act))(*[float(weights[i]) for i in act])
+        g.check(lib.ghc_weighted_mean(ctx.h, out.ptr, stage_buf.ptr, wts, len(act), P),
+                "weighted_mean")
+
+    for r in range(R + 1):  # round R: data exhausted, final flushes only
+        cnt = counts[r] if r < R else np.zeros(world, np.int32)
+        gcnt = cnt[sub:sub + Wg]
+        flushing, absorbed = plan[r]
+        # ---- worker: mean gradient of its next batch at the group weights ----
+        if cnt[rank]:
+            if rank == sub:
+                wk.grad()
+                _copy(ctx, mail.ptr.value, wk.gl.ptr.value, 4 * P)
+            else:
+                wk.grad()
+                _copy(ctx, my_slot, wk.gl.ptr.value, 4 * P)
+                ctx.sync()
+                _tok(dist, sub, send=True)
+        if rank == sub:
+            # ---- sub-master: sync combine + sgd_step (lr, mu) ----
+            if gcnt.sum() > 0:
+                for j in range(1, Wg):
+                    if gcnt[j]:
+                        _tok(dist, sub + j, send=False)
+                combine(comb, mail, stage, gcnt)
+                sgd(wg, vg, comb.ptr.value, cfg.lr, cfg.mu, st)
+            if flushing[q]:
+                # pseudo-gradient snapshot − current (oracle decision 2) → top master
+                _copy(ctx, psd.ptr.value, snap.ptr.value, 4 * P)
+                vd.zero()
+                sgd(psd, vd, wg.ptr.value, 1.0, 0.0, st)  # psd + (−1·wg): exactly snap − wg
+                _copy(ctx, top_slot, psd.ptr.value, 4 * P)
+                ctx.sync()
+                if rank != 0:
+                    _tok(dist, 0, send=True)
+        if rank == 0 and any(flushing):
+            # ---- top master: combine the flushing groups (group order), sgd_step ----
+            for qq in range(1, G):
+                if flushing[qq]:
+                    _tok(dist, qq * Wg, send=False)
+            combine(tcomb, tmail, tstage, [absorbed[qq] if flushing[qq] else 0 for qq in range(G)])
+            sgd(tw, tv, tcomb.ptr.value, cfg.parent_lr, cfg.parent_mu, tst)
+            for qq in range(G):
+                if flushing[qq]:
+                    _copy(ctx, sub_wg[qq], tw.ptr.value, 4 * P)  # reply → the group's weights
+            ctx.sync()
+            for qq in range(1, G):
+                if flushing[qq]:
+                    _tok(dist, qq * Wg, send=True)
+        if rank == sub:
+            if flushing[q]:
+                if rank != 0:
+                    _tok(dist, 0, send=False)  # the top weights landed in wg
+                _copy(ctx, snap.ptr.value, wg.ptr.value, 4 * P)
+            if r < R:  # ---- the group's weights → every worker of the group ----
+                _copy(ctx, wk.w.ptr.value, wg.ptr.value, 4 * P)
+                for p in inbox.values():
+                    _copy(ctx, p, wg.ptr.value, 4 * P)
+                ctx.sync()
+                for k in inbox:
+                    _tok(dist, k, send=True)
+        elif r < R:
+            _tok(dist, sub, send=False)  # the group weights landed in wk.w
+    ctx.sync()
+    out = {"worker_w": wk.w.numpy()}
+    if rank == sub:
+        out["group_w"] = wg.numpy()
+    if rank == 0:
+        out["w"] = tw.numpy()
+    dist.barrier()
+    ipc.close()
+    return out
+
+
+def _group_history(counts, R, G, Wg, K):
+    """Per round r ≤ R: (flushing flag of each group, samples each group
+    absorbed since its last flush) — the deterministic schedule of run_hier
+    (session.cu), identical on every rank."""
+    absorbed, since = [0] * G, [0] * G
+    hist = []
+    for r in range(R + 1):
+        cnt = counts[r] if r < R else np.zeros(G * Wg, np.int32)
+        fl, ab = [0] * G, [0] * G
+        for q in range(G):
+            c = int(cnt[q * Wg:(q + 1) * Wg].sum())
+            if c:
+                absorbed[q] += c
+                since[q] += 1
+                fl[q] = int(since[q] >= K)
+            else:
+                fl[q] = int(absorbed[q] > 0)
+            ab[q] = absorbed[q]
+            if fl[q]:
+                absorbed[q] = since[q] = 0
+        hist.append((fl, ab))
+    return hist

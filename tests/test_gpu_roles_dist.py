@@ -42,8 +42,11 @@ def _rank_main(rank, world, port, outdir, algo, order, spec_args, cfg_kw):
     arch = g.Architecture(ctx, ARCH)
     cfg = g.train_config(**cfg_kw)
     spec = g.data_spec(*spec_args)
-    fn = rd.run_async_downpour if algo == "async" else rd.run_easgd
-    out = fn(arch, spec, cfg, order, rank, world, dist)
+    if algo == "hier":
+        out = rd.run_hierarchical(arch, spec, cfg, rank, world, dist)
+    else:
+        fn = rd.run_async_downpour if algo == "async" else rd.run_easgd
+        out = fn(arch, spec, cfg, order, rank, world, dist)
     np.savez(os.path.join(outdir, f"r{rank}.npz"), **{k: np.asarray(v) for k, v in out.items()})
     dist.destroy_process_group()
 
@@ -99,3 +102,19 @@ def test_easgd_p2p_vs_oracle(tmp_path, oracle, replay):
     _close(outs[0]["center"], r.w)
     for k in range(W):
         _close(outs[k]["worker_w"], r.extra["worker_w"][k])
+
+
+@pytest.mark.parametrize("W,K", [(4, 2), (8, 2), (4, 3)])
+def test_hierarchical_p2p_vs_oracle(tmp_path, oracle, W, K):
+    """2 sub-masters × W/2 workers → top master (pass-through parent), every
+    transfer a device-to-device IPC copy; flushes every K group updates and at
+    data end."""
+    spec_args = (16, 200)
+    kw = dict(n_workers=W, batch_size=40, epochs=1, groups=2, flush_k=K)
+    outs = _spawn(tmp_path, W, "hier", None, spec_args, kw)
+    spec = oracle.data_spec(*spec_args)
+    x, y = oracle.generate(spec)
+    r = oracle.run_hier(oracle.parse_arch(ARCH), spec, x, y, oracle.train_cfg(**kw))
+    _close(outs[0]["w"], r.w)
+    for q in range(2):
+        _close(outs[q * (W // 2)]["group_w"], r.extra["group_w"][q])
