@@ -38,6 +38,7 @@ ARCH = "lstm(5,20,10),softmax(20,3)"
 FLOP_PER_SAMPLE = 102_760   # fwd 36,920 + bwd 65,840
 SGD_BYTES_PER_PARAM = 20    # read w, v, g; write w, v (fp32)
 WIDE_P = 16_881_699         # SURVEY §8 wide variant parameter count
+WIDE_ARCH = "lstm(5,20,10),dense(20,4096,relu),dense(4096,4096,relu),softmax(4096,3)"
 METRIC = "train samples/sec at 1/2/4/8 B200 (sync Downpour); % of roofline"
 UNIT = "samples/s"
 
@@ -479,30 +480,47 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
 
 
 def update_roofline(args, g, ctx):
-    """ghc_sgd_apply (optim.cpp:39-65) at the wide variant's P: HBM roofline."""
-    import ctypes as C
+    """The master's update path (optim.cpp:39-65) at the wide variant's P,
+    HBM roofline: ghc_master_apply (one pass into the other buffer,
+    sgd_db_kernel — what a Downpour master runs per combined gradient) and
+    the in-place ghc_sgd_apply (finite check + update, sgd_apply_kernel)."""
     P = WIDE_P
     rng = np.random.default_rng(0)
-    w = ctx.upload(rng.normal(size=P).astype(np.float32))
-    v = ctx.upload(np.zeros(P, np.float32))
+    w0 = rng.normal(size=P).astype(np.float32)
     gr = ctx.upload((rng.normal(size=P) * 1e-3).astype(np.float32))
-    st = ctx.array(1, np.int32)
     flush = ctx.array(64 << 20)  # 256 MB > L2: evict between launches
-    times = []
-    for it in range(23):
-        flush.zero()
-        ctx.timer_start()
-        g.gradhub.check(ctx.lib.ghc_sgd_apply(ctx.h, w.ptr, v.ptr, gr.ptr, P, 0.01, 0.9, st.ptr,
-                                              None))
-        t = ctx.timer_stop()
-        if it >= 3:
-            times.append(t)
-    t = statistics.median(times)
-    gbs = SGD_BYTES_PER_PARAM * P / (t / 1e3) / 1e9
     pk, kind = peaks()
-    return {"kernel": "sgd_apply_kernel", "P": P, "ms": t, "achieved_gbs": gbs,
-            "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"], "bytes_per_param": 20,
-            "peak_kind": kind, "l2": "256 MB flush before every launch"}
+
+    def timed(fn):
+        times = []
+        for it in range(23):
+            flush.zero()
+            ctx.timer_start()
+            fn()
+            t = ctx.timer_stop()
+            if it >= 3:
+                times.append(t)
+        return statistics.median(times)
+
+    arch = g.Architecture(ctx, WIDE_ARCH)
+    assert arch.n_params == P
+    m = g.Master(arch, w0, 0.01, 0.9)
+    t_db = timed(lambda: m.apply(gr))
+    del m
+    w = ctx.upload(w0)
+    v = ctx.upload(np.zeros(P, np.float32))
+    st = ctx.array(1, np.int32)
+    t_ip = timed(lambda: g.gradhub.check(ctx.lib.ghc_sgd_apply(ctx.h, w.ptr, v.ptr, gr.ptr, P, 0.01,
+                                                               0.9, st.ptr, None)))
+
+    def row(kernel, t):
+        gbs = SGD_BYTES_PER_PARAM * P / (t / 1e3) / 1e9
+        return {"kernel": kernel, "P": P, "ms": t, "achieved_gbs": gbs, "peak_gbs": pk["hbm_gbs"],
+                "frac": gbs / pk["hbm_gbs"], "bytes_per_param": SGD_BYTES_PER_PARAM,
+                "peak_kind": kind, "l2": "256 MB flush before every launch"}
+    out = row("sgd_db_kernel", t_db)
+    out["in_place"] = row("sgd_apply_kernel", t_ip)
+    return out
 
 
 def main():

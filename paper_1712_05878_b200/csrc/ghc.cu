@@ -672,6 +672,13 @@ ghc_status ghc_master_create(ghc_plan* p, const double* h_w0, float lr, float mu
   CU(cudaMemset(m->ms, 0, sizeof(MasterDev)));
   CU(cudaMalloc(&m->ms_apply, sizeof(MasterDev)));
   CU(cudaMemset(m->ms_apply, 0, sizeof(MasterDev)));
+  CU(cudaMalloc(&m->ms_db, sizeof(MasterDev)));
+  CU(cudaMemset(m->ms_db, 0, sizeof(MasterDev)));
+  {
+    float* h[4] = {m->w[0], m->w[1], m->v[0], m->v[1]};
+    CU(cudaMalloc(&m->bufs, sizeof(h)));
+    CU(cudaMemcpy(m->bufs, h, sizeof(h), cudaMemcpyHostToDevice));
+  }
   *out = m;
   return GHC_OK;
 }
@@ -686,6 +693,8 @@ void ghc_master_destroy(ghc_master* m) {
   }
   cudaFree(m->ms);
   cudaFree(m->ms_apply);
+  cudaFree(m->ms_db);
+  cudaFree(m->bufs);
   cudaFree(m->g_scratch);
   delete m;
 }
@@ -786,23 +795,14 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
 }
 
 ghc_status ghc_master_apply(ghc_master* m, const float* d_g) {
-  // Single-buffer apply on the current buffer (host knows cur after sync).
-  int cur = 0;
-  if (ghc_status s = master_cur(m, cur)) return s;
+  // One pass into the other buffer; the device flips `cur` (no host sync).
   ghc_ctx* c = m->plan->ctx;
-  float* w = m->w[cur];
-  float* v = m->v[cur];
-  MasterDev* ms = m->ms_apply;
-  int vec = 1;
-  long long PP = m->P;
-  float lr = m->lr, mu = m->mu;
-  int* st = &m->ms->status;
-  unsigned long long* ver = &m->ms->version;
-  unsigned long long* rj = &m->ms->rejected;
-  void* args[] = {&w, &v, &d_g, &PP, &vec, &lr, &mu, &ms, &st, &ver, &rj};
-  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
-  CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid), dim3(256),
-                                 args, 0, c->stream));
+  const int vec = aligned16(d_g);  // w[], v[] are cudaMalloc-aligned; the tail is scalar
+  const int grid = std::min<long long>(occupancy_grid(c, reinterpret_cast<const void*>(sgd_db_kernel), 256),
+                                       (m->P / 4 + 255) / 256 + 1);
+  sgd_db_kernel<<<grid, 256, 0, c->stream>>>(m->bufs, m->bufs + 2, d_g, m->P, vec, m->lr, m->mu,
+                                             m->ms, m->ms_db);
+  CU(cudaGetLastError());
   c->launches++;
   return GHC_OK;
 }

@@ -92,10 +92,12 @@ struct ghc_plan {
 struct ghc_master {
   ghc_plan* plan = nullptr;
   float* g_scratch = nullptr;  // layered archs: the round's combined gradient
+  float** bufs = nullptr;      // device copy of {w[0], w[1], v[0], v[1]} (sgd_db_kernel)
   float* w[2] = {nullptr, nullptr};
   float* v[2] = {nullptr, nullptr};
   MasterDev* ms = nullptr;
-  MasterDev* ms_apply = nullptr;  // barrier state for ghc_master_apply
+  MasterDev* ms_apply = nullptr;  // barrier state for the in-place sgd_apply_kernel
+  MasterDev* ms_db = nullptr;     // bad flag + arrival counter of sgd_db_kernel
   float lr = 0.01f, mu = 0.0f;
   int64_t P = 0;
 };

@@ -106,6 +106,73 @@ static __global__ void __launch_bounds__(256) sgd_apply_kernel(float* __restrict
   finish_rejecting(ms, rej, status, version, rejected);
 }
 
+// sgd_step for the double-buffered master (optim.cpp:39-65) in ONE pass:
+// read w, v, g of the current buffer, write the new w, v into the other one
+// (20 B/param, the algorithmic minimum); the last CTA out commits by flipping
+// ms->cur (version + 1) or rejects a non-finite gradient whole (optim.cpp:
+// 49-51 — the current buffer was never written).  No grid barrier, no
+// separate finite-check pass.  `flags` holds the cross-CTA bad flag and the
+// arrival counter.
+static __global__ void __launch_bounds__(256) sgd_db_kernel(float* const* __restrict__ wb,
+                                                     float* const* __restrict__ vb,
+                                                     const float* __restrict__ g, long long P,
+                                                     int vec, float lr, float mu, MasterDev* ms,
+                                                     MasterDev* flags) {
+  const int cur = __ldcg(&ms->cur);
+  const float* w = wb[cur];
+  const float* v = vb[cur];
+  float* w2 = wb[cur ^ 1];
+  float* v2 = vb[cur ^ 1];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long n4 = vec ? (P >> 2) : 0;
+  int bad = 0;
+  for (long long i = tid; i < n4; i += nth) {
+    const float4 gv = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    float4 vv = __ldcs(reinterpret_cast<const float4*>(v) + i);
+    float4 wv = __ldcs(reinterpret_cast<const float4*>(w) + i);
+    bad |= !finite4(gv);
+    vv.x = fmaf(mu, vv.x, -lr * gv.x);
+    vv.y = fmaf(mu, vv.y, -lr * gv.y);
+    vv.z = fmaf(mu, vv.z, -lr * gv.z);
+    vv.w = fmaf(mu, vv.w, -lr * gv.w);
+    wv.x += vv.x;
+    wv.y += vv.y;
+    wv.z += vv.z;
+    wv.w += vv.w;
+    __stcs(reinterpret_cast<float4*>(v2) + i, vv);
+    __stcs(reinterpret_cast<float4*>(w2) + i, wv);
+  }
+  for (long long i = (n4 << 2) + tid; i < P; i += nth) {
+    const float gi = g[i];
+    bad |= !isfinite(gi);
+    const float vn = fmaf(mu, v[i], -lr * gi);
+    v2[i] = vn;
+    w2[i] = w[i] + vn;
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    if (bad) atomicOr(&flags->flag[0], 1);
+    __threadfence();
+    const unsigned prev = atomicAdd(&flags->arrive, 1u);
+    if (prev == gridDim.x - 1) {  // last CTA: every write and flag of the grid is visible
+      __threadfence();
+      const int rej = atomicAdd(&flags->flag[0], 0);
+      if (rej) {
+        ms->rejected += 1ull;
+        ms->status = 2;  // GHC_ERR_NONFINITE
+      } else {
+        ms->cur = cur ^ 1;
+        ms->version += 1ull;
+        ms->status = 0;
+      }
+      flags->flag[0] = 0;
+      flags->arrive = 0;
+      __threadfence();
+    }
+  }
+}
+
 static __global__ void __launch_bounds__(256) easgd_worker_kernel(float* __restrict__ w,
                                                            const float* __restrict__ c,
                                                            const float* __restrict__ g,

@@ -8,6 +8,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 BENCH_ARCH = "lstm(5,20,10),softmax(20,3)"
+WIDE_ARCH = "lstm(5,20,10),dense(20,4096,relu),dense(4096,4096,relu),softmax(4096,3)"  # SURVEY §8 wide
 
 
 def pytest_configure(config):

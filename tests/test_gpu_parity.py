@@ -13,7 +13,7 @@ MUFU-based sigmoid/tanh while the reference computes in f64, so
 import numpy as np
 import pytest
 
-from conftest import BENCH_ARCH
+from conftest import BENCH_ARCH, WIDE_ARCH
 
 import paper_1712_05878_b200 as g
 
@@ -225,6 +225,51 @@ def test_master_rejects_nonfinite_round(ctx):
     m.sync_rounds(ctx.upload(x_bad), ctx.upload(y), ctx.upload(idx), B, B, 2, idx_offset=B)
     w, v, ver, rej = m.read()
     assert ver == 2 and rej == 1 and np.isfinite(w).all()
+
+
+@pytest.mark.parametrize("arch_text", [BENCH_ARCH, WIDE_ARCH])
+def test_master_apply_vs_oracle(ctx, oracle, arch_text):
+    """ghc_master_apply (one-pass double-buffered sgd_db_kernel, optim.cpp:
+    39-65): each accepted update flips the current buffer on device; a
+    non-finite gradient is rejected whole (optim.cpp:49-51) and leaves the
+    current buffer and version untouched; it composes with sync_rounds."""
+    arch = g.Architecture(ctx, arch_text)
+    P = arch.n_params
+    rng = np.random.default_rng(P)
+    w0 = g.init_weights(arch, 3)
+    m = g.Master(arch, w0, 0.01, 0.9)
+    w, v = w0.astype(np.float64), np.zeros(P)
+    for k in range(3):
+        gr = (rng.normal(size=P) * 0.1).astype(np.float32)
+        m.apply(ctx.upload(gr))
+        rc, w, v = oracle.sgd_step(w, v, gr.astype(np.float64), 0.01, 0.9)
+        assert rc == 0
+        wd, vd, ver, rej = m.read()
+        assert ver == k + 1 and rej == 0
+        assert np.max(np.abs(wd - w) / np.maximum(1, np.abs(w))) <= 1e-6
+        assert np.max(np.abs(vd - v) / np.maximum(1, np.abs(v))) <= 1e-6
+        w, v = wd.astype(np.float64), vd.astype(np.float64)  # continue from the f32 state
+    gbad = np.ones(P, np.float32)
+    gbad[P // 2] = np.nan
+    m.apply(ctx.upload(gbad))
+    wd, vd, ver, rej = m.read()
+    assert ver == 3 and rej == 1
+    assert np.array_equal(wd, w.astype(np.float32)) and np.array_equal(vd, v.astype(np.float32))
+    if arch_text != BENCH_ARCH:
+        return
+    # sync_rounds picks up the applied buffer, and apply picks up sync_rounds'
+    spec = g.data_spec(2, 500)
+    x, y = g.generate(spec)
+    m.sync_rounds(ctx.upload(x), ctx.upload(y), ctx.upload(np.arange(200, dtype=np.int32)), 200,
+                  200, 1)
+    w1, v1, ver, _ = m.read()
+    assert ver == 4 and not np.array_equal(w1, wd)
+    gr = (rng.normal(size=P) * 0.1).astype(np.float32)
+    m.apply(ctx.upload(gr))
+    _, wo, vo = oracle.sgd_step(w1.astype(np.float64), v1.astype(np.float64),
+                                gr.astype(np.float64), 0.01, 0.9)
+    w2, v2, ver, _ = m.read()
+    assert ver == 5 and np.max(np.abs(w2 - wo) / np.maximum(1, np.abs(wo))) <= 1e-6
 
 
 @pytest.mark.parametrize("B", [1000, 3000])
