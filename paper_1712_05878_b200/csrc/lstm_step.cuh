@@ -178,7 +178,11 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   using N = LstmNet<D, H, T, K>;
   constexpr int DP = N::DP;
   const bool act = lane < H;
-  const int j = act ? lane : 0;
+  // Lanes ≥ H shadow unit lane mod H: they compute the same values as that
+  // unit's lane, so their shared-memory stores (same address, same value)
+  // need no divergent branch in the recurrences.  Reductions and the weight
+  // gradients still mask them with `act`.
+  const int j = lane % H;
   auto put = [](float& dst, float v) {
     if constexpr (ACC) dst += v;
     else dst = v;
@@ -300,12 +304,10 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
         const float og = sigmoid_f(a0[sp][3] + a1[sp][3]);
         c[sp] = fmaf(fg, c[sp], ig * gg);
         const float tc = tanh_f(c[sp]);
-        if (act) {
-          float* ct = cs[sp] + (t * H + j) * 8;
-          reinterpret_cast<float4*>(ct)[0] = make_float4(ig, fg, gg, og);
-          reinterpret_cast<float2*>(ct)[2] = make_float2(c[sp], tc);
-          hs[sp][t * H + j] = og * tc;
-        }
+        float* ct = cs[sp] + (t * H + j) * 8;
+        reinterpret_cast<float4*>(ct)[0] = make_float4(ig, fg, gg, og);
+        reinterpret_cast<float2*>(ct)[2] = make_float2(c[sp], tc);
+        hs[sp][t * H + j] = og * tc;
       }
       __syncwarp();
     }
@@ -321,7 +323,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
         if (act && trunk_io[sp]) trunk_io[sp][j] = hs[sp][(T - 1) * H + j];
         dh[sp] = 0.0f;
       } else {
-        dh[sp] = act ? trunk_io[sp][j] * (scale[sp] != 0.0f ? 1.0f : 0.0f) : 0.0f;
+        dh[sp] = trunk_io[sp][j] * (scale[sp] != 0.0f ? 1.0f : 0.0f);
       }
     }
     if constexpr (!BWD) return;
@@ -366,7 +368,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
       const float dzk = (e[sp][k] * inv_den[sp] - (k == label[sp] ? 1.0f : 0.0f)) * scale[sp];
       gws = fmaf(dzk, hT[sp], gws);
       gbs += dzk;
-      dh[sp] = fmaf(act ? wsm[N::OFF_WS + k * H + j] : 0.0f, dzk, dh[sp]);
+      dh[sp] = fmaf(wsm[N::OFF_WS + k * H + j], dzk, dh[sp]);  // shadow lanes: = lane j's
     }
     if (act) put(wp[N::OFF_WS + k * H + j], gws);
     if (lane == 0) put(wp[N::OFF_BS + k], gbs);
@@ -397,12 +399,10 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
         dc[sp] = fmaf(dh[sp] * og, 1.0f - tc * tc, dc[sp]);
         const float di = dc[sp] * gg, dg = dc[sp] * ig, df = dc[sp] * cp;
         float* dzt = dzs[sp] + t * 4 * H;
-        if (act) {
-          dzt[0 * H + j] = di * ig * (1.0f - ig);
-          dzt[1 * H + j] = df * fg * (1.0f - fg);
-          dzt[2 * H + j] = dg * (1.0f - gg * gg);
-          dzt[3 * H + j] = dout * og * (1.0f - og);
-        }
+        dzt[0 * H + j] = di * ig * (1.0f - ig);
+        dzt[1 * H + j] = df * fg * (1.0f - fg);
+        dzt[2 * H + j] = dg * (1.0f - gg * gg);
+        dzt[3 * H + j] = dout * og * (1.0f - og);
       }
       __syncwarp();
       if (t > 0) {  // dh_{t-1} = Whᵀ dz_t (the reference also does this at t=0, unused)
