@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libghc.so")
+# GHC_LIB_PATH: load another in-tree build (A/B experiments, tools/ablate.sh)
+LIB_PATH = os.environ.get("GHC_LIB_PATH") or os.path.join(HERE, "_build", "libghc.so")
 
 
 class GradhubError(RuntimeError):
