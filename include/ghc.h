@@ -216,7 +216,11 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
                                   const int32_t* d_counts, int64_t n, int32_t n_rounds,
                                   float* d_loss_out);
 /* Apply a combined gradient produced elsewhere (NCCL reduce, virtual workers):
- * d_g[P] is the already-combined gradient. */
+ * d_g[P] is the already-combined gradient.  sgd_step (optim.cpp:39-65) in one
+ * stream-ordered pass from the current w/v buffer into the other; the device
+ * flips the current buffer and bumps the version, or — any non-finite g —
+ * leaves it untouched and counts a rejection (optim.cpp:49-51; read back with
+ * ghc_master_read).  No host synchronisation. */
 ghc_status ghc_master_apply(ghc_master* m, const float* d_g);
 
 /* ------------------------------------------------------------------ */
