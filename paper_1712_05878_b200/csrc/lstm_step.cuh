@@ -229,7 +229,114 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   // (even / odd input index) — one FFMA2 advances both with the same rounding
   // as two FFMAs, so results are bit-identical to the scalar loop at half the
   // issue slots (3-register FFMA issues once per 2 cycles per SM sub-partition).
-  {
+  //
+  // Gate rows spread over all 32 lanes (H ≤ 24, H % 4 == 0): lane ℓ computes
+  // rows ℓ, ℓ+32, ℓ+64 (< 4H) — NR = ⌈4H/32⌉ rows instead of 4 — activates
+  // them (σ or tanh by the row's gate, branch-free), and lane u collects the
+  // four gates of unit u with one SHFL per gate.  The recurrent product is
+  // bound by FFMA2 issue (≈ 6.3 warp-cycles per FFMA2 with two
+  // warps per sub-partition), so 3 rows × 10 instead of 4 × 10 FFMA2 per step
+  // at H = 20.  Same operations in the same order per row: bit-identical to
+  // the unit-per-lane loop below.
+  constexpr int NR = (4 * H + 31) / 32;
+  if constexpr (N::HV && NR < 4) {
+    constexpr int DH = D / 2, HH = H / 2;
+    float2 wxr[NR][DH > 0 ? DH : 1], whr[NR][HH];
+    float wxt[NR], br[NR], al[NR], be[NR], ga[NR];
+#pragma unroll
+    for (int sl = 0; sl < NR; ++sl) {
+      const int r = lane + 32 * sl;
+      const bool ok = r < 4 * H;
+      const int rr = ok ? r : 0;
+      const float* rx = wsm + N::OFF_WX + rr * D;
+      const float4* rh4 = reinterpret_cast<const float4*>(wsm + N::OFF_WH + rr * H);
+#pragma unroll
+      for (int m = 0; m < DH; ++m) wxr[sl][m] = ok ? make_float2(rx[2 * m], rx[2 * m + 1]) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int m = 0; m < H / 4; ++m) {
+        const float4 u = ok ? rh4[m] : make_float4(0.f, 0.f, 0.f, 0.f);
+        whr[sl][2 * m] = make_float2(u.x, u.y);
+        whr[sl][2 * m + 1] = make_float2(u.z, u.w);
+      }
+      wxt[sl] = (ok && (D & 1)) ? rx[D - 1] : 0.0f;
+      br[sl] = ok ? wsm[N::OFF_B + rr] : 0.0f;
+      // σ(z) = rcp(1 + 2^(−z·log2e));  tanh(z) = 1 − 2·rcp(2^(2z·log2e) + 1)
+      const bool tnh = (rr / H) == 2;
+      al[sl] = tnh ? 2.8853900817779268f : -1.4426950408889634f;
+      be[sl] = tnh ? -2.0f : 1.0f;
+      ga[sl] = tnh ? 1.0f : 0.0f;
+    }
+    // gate q of unit u lives in lane (qH+u) mod 32, row slot (qH+u) / 32;
+    // pick[q] = the slot this lane presents for gate q
+    // (as bit masks: a select by a runtime slot index would compile to a
+    // local-memory array access)
+    unsigned pick[4][NR];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int sl = 0; sl < NR; ++sl) {
+        const int r = lane + 32 * sl;
+        pick[q][sl] = (r < 4 * H && r / H == q) ? 0xffffffffu : 0u;
+      }
+    int src[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) src[q] = (q * H + j) & 31;
+    float c[SPW];
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) c[sp] = 0.0f;
+#pragma unroll 1
+    for (int t = 0; t < T; ++t) {
+      float2 acc[SPW][NR];
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp) {
+        float xv[DP];
+        load_x(sp, t, xv);
+#pragma unroll
+        for (int sl = 0; sl < NR; ++sl) {
+          acc[sp][sl] = make_float2(br[sl], 0.0f);
+#pragma unroll
+          for (int m = 0; m < DH; ++m)
+            acc[sp][sl] = __ffma2_rn(wxr[sl][m], make_float2(xv[2 * m], xv[2 * m + 1]), acc[sp][sl]);
+          if (D & 1) acc[sp][sl].x = fmaf(wxt[sl], xv[D - 1], acc[sp][sl].x);
+        }
+      }
+      if (t > 0) {
+#pragma unroll
+        for (int sp = 0; sp < SPW; ++sp) {
+          float hv[H];
+          load_h(sp, t - 1, hv);
+#pragma unroll
+          for (int m = 0; m < HH; ++m)
+#pragma unroll
+            for (int sl = 0; sl < NR; ++sl)
+              acc[sp][sl] = __ffma2_rn(whr[sl][m], make_float2(hv[2 * m], hv[2 * m + 1]), acc[sp][sl]);
+        }
+      }
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp) {
+        float y[NR];
+#pragma unroll
+        for (int sl = 0; sl < NR; ++sl)
+          y[sl] = fmaf(be[sl], rcp_approx(1.0f + ex2_approx(al[sl] * (acc[sp][sl].x + acc[sp][sl].y))), ga[sl]);
+        float gq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          unsigned pv = 0u;
+#pragma unroll
+          for (int sl = 0; sl < NR; ++sl) pv |= __float_as_uint(y[sl]) & pick[q][sl];
+          gq[q] = __shfl_sync(0xffffffffu, __uint_as_float(pv), src[q]);
+        }
+        const float ig = gq[0], fg = gq[1], gg = gq[2], og = gq[3];
+        c[sp] = fmaf(fg, c[sp], ig * gg);
+        const float tc = tanh_f(c[sp]);
+        float* ct = cs[sp] + (t * H + j) * 8;
+        reinterpret_cast<float4*>(ct)[0] = make_float4(ig, fg, gg, og);
+        reinterpret_cast<float2*>(ct)[2] = make_float2(c[sp], tc);
+        hs[sp][t * H + j] = og * tc;
+      }
+      __syncwarp();
+    }
+  } else {
     constexpr int DH = D / 2, HH = H / 2;
     float2 wxp[4][DH > 0 ? DH : 1], whp[4][HH > 0 ? HH : 1];
     float wxt[4], wht[4], bb[4];  // odd-length tails (into the even partial sum)
