@@ -313,8 +313,14 @@ def run_ours_dist(args, rank, world, local):
     B = args.batch
     p2p = args.exchange == "p2p"
     if p2p:
-        ex = gd.P2PExchange(arch, rank, world, dist=tdist)
-    else:
+        try:
+            ex = gd.P2PExchange(arch, rank, world, dist=tdist)
+        except gd.P2PUnavailable as e:  # raised on every rank alike
+            print(f"[bench] fused NVLink exchange unavailable ({e}); using NCCL reduce/broadcast",
+                  file=sys.stderr)
+            p2p = False
+            args.exchange = "reduce_bcast"
+    if not p2p:
         uid = gd.rendezvous(tdist, rank, gd.nccl_unique_id)
         comm = gd.Comm(ctx, uid, rank, world)
         exchange = gd.ALLREDUCE if args.exchange == "allreduce" else gd.REDUCE_BCAST

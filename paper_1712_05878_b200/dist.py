@@ -136,6 +136,22 @@ def allgather_bytes(dist, payload: bytes) -> list:
     return out
 
 
+def agree(dist, ok: bool, payload: bytes = b""):
+    """Collective success check: every rank contributes (ok, payload).
+    Returns (True, [payload of every rank, rank order]) when all ranks
+    succeeded, else (False, [(rank, payload) of the failed ranks]) — the same
+    answer on every rank, so no rank is left waiting in a later collective."""
+    allp = allgather_bytes(dist, bytes([1 if ok else 0]) + bytes(payload))
+    if all(p[0] for p in allp):
+        return True, [p[1:] for p in allp]
+    return False, [(k, p[1:].decode(errors="replace")) for k, p in enumerate(allp) if not p[0]]
+
+
+class P2PUnavailable(RuntimeError):
+    """Peer memory could not be exported/mapped on some rank (raised on every
+    rank alike)."""
+
+
 class P2PExchange:
     """ghc_p2p: fused NVLink exchange of the sync round (p2p.cu)."""
 
@@ -153,11 +169,23 @@ class P2PExchange:
             g.check(lib.ghc_p2p_create(arch.h, rank, world, C.byref(h)), "p2p_create")
         self.h = h
         if not virtual:
+            # Every rank takes part in both all-gathers even when its own step
+            # failed, so a rank that cannot export/map peer memory makes ALL
+            # ranks raise P2PUnavailable (callers fall back to NCCL) instead
+            # of leaving the others blocked in a collective.
             mine = (C.c_uint8 * self.HANDLE_BYTES)()
-            g.check(lib.ghc_p2p_export(h, mine), "p2p_export")
-            allh = allgather_bytes(dist, bytes(mine))
+            rc = lib.ghc_p2p_export(h, mine)
+            ok, allh = agree(dist, rc == 0, bytes(mine))
+            if not ok:
+                self.close()
+                raise P2PUnavailable(f"ghc_p2p_export failed: {allh}")
             buf = (C.c_uint8 * (self.HANDLE_BYTES * world)).from_buffer_copy(b"".join(allh))
-            g.check(lib.ghc_p2p_import(h, buf), "p2p_import")
+            rc = lib.ghc_p2p_import(h, buf)
+            why = b"" if rc == 0 else lib.ghc_last_error()[:200]
+            ok, bad = agree(dist, rc == 0, why)
+            if not ok:
+                self.close()
+                raise P2PUnavailable(f"ghc_p2p_import failed: {bad}")
 
     def sync_rounds(self, master: g.Master, x, y, idx, stride: int, idx_vstride: int, counts,
                     n_max: int, rounds: int, loss_out=None, idx_offset: int = 0,

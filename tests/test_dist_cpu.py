@@ -45,6 +45,12 @@ def _worker(rank, world, port, outdir):
     # P2PExchange bootstrap: every rank's 64-byte IPC handle, in rank order
     hs = gd.allgather_bytes(dist, bytes([rank + 1]) * gd.P2PExchange.HANDLE_BYTES)
     assert hs == [bytes([q + 1]) * 64 for q in range(world)]
+    # collective success check (P2PExchange's fallback to NCCL): every rank
+    # sees the same verdict, with the failing ranks' messages
+    ok, pay = gd.agree(dist, True, bytes([rank]))
+    assert ok and pay == [bytes([q]) for q in range(world)]
+    ok, bad = gd.agree(dist, rank != 1, b"no peer access" if rank == 1 else b"")
+    assert not ok and bad == [(1, "no peer access")]
 
     B, epochs, seed = 70, 1, 99
     spec = g.data_spec(6, 110)
