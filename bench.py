@@ -126,11 +126,12 @@ def run_reference(args):
     cfg = O.train_cfg(n_workers=W, batch_size=args.batch, epochs=1000)
     # each step = one sync round of W workers × B samples; bounded sample
     steps = max(1, min(args.steps, args.ref_rounds))
-    sec, n = O.ref_bench_sync(ARCH, spec, cfg, max(1, args.warmup // 10), steps)
+    warm = max(3, min(args.warmup, 10))  # W ≥ 3, bounded: each round is ~0.1 s of CPU
+    sec, n = O.ref_bench_sync(ARCH, spec, cfg, warm, steps)
     value = n / sec
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
-        "n_gpus": args.gpus, "steps": steps, "warmup": max(1, args.warmup // 10),
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm,
         "ms_per_step": 1e3 * sec / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "sync Downpour, lstm(5,20,10)+softmax(20,3), B=1000/worker",
