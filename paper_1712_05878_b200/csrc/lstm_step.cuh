@@ -11,9 +11,12 @@
 // whole-update non-finite rejection (optim.cpp:49-51) committed on device.
 //
 // Mapping (B200, 148 SMs): one warp per sample, lane j owns hidden unit j
-// (H ≤ 32) and the four gate rows {j, H+j, 2H+j, 3H+j}; its rows of Wx/Wh
-// live in registers for the forward recurrence, its column of Wh for
-// dh = Whᵀdz in the backward; h_t and the gate cache live in shared memory.
+// (H ≤ 32).  Forward: the 4H gate rows are spread over all 32 lanes (rows ℓ,
+// ℓ+32, ℓ+64 with their Wx/Wh/b in registers), activated where computed and
+// gathered per unit with one SHFL per gate (H ≤ 24, H % 4 == 0; otherwise
+// lane j computes the rows {j, H+j, 2H+j, 3H+j} itself).  Backward: lane j
+// holds column j of Wh for dh = Whᵀdz; h_t, the gate cache and dz live in
+// shared memory.
 // Samples of a round are spread over ≈ one CTA per SM so the 1000
 // transcendentals/sample run on every SM's MUFU pipe.  The recurrence is a
 // K=25 contraction per timestep — far below a tcgen05 tile — so the kernel is
