@@ -90,6 +90,7 @@ extern "C" ghc_status ghc_diag_barrier_bench(ghc_ctx* c, int32_t impl, int32_t c
   CU(cudaMalloc(&bar, bar_bytes));
   CU(cudaMemset(bar, 0, bar_bytes));
   CU(cudaMalloc(&out, sizeof(unsigned long long) * ctas));
+  CU(cudaDeviceSynchronize());  // memsets (legacy stream) before the launch on ctx->stream
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(threads);

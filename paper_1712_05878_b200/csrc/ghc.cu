@@ -259,6 +259,7 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     const size_t bar_bytes = sizeof(unsigned) * 32 * (2 + static_cast<size_t>(p->max_ctas));
     CU(cudaMalloc(&p->bar, bar_bytes));
     CU(cudaMemset(p->bar, 0, bar_bytes));
+    CU(cudaDeviceSynchronize());  // legacy-stream memsets vs the non-blocking ctx->stream
     p->use_cluster = false;
     *out = p;
     return GHC_OK;
@@ -382,6 +383,9 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
   const size_t bar_bytes = sizeof(unsigned) * 32 * (2 + static_cast<size_t>(p->max_ctas));
   CU(cudaMalloc(&p->bar, bar_bytes));
   CU(cudaMemset(p->bar, 0, bar_bytes));
+  // the legacy-stream memsets above are not ordered with ctx->stream
+  // (non-blocking): complete them before any kernel can use the plan
+  CU(cudaDeviceSynchronize());
   *out = p;
   return GHC_OK;
 }
@@ -566,7 +570,10 @@ MasterDev* ctx_scratch_ms(ghc_ctx* c) {
   MasterDev* m = nullptr;
   cudaSetDevice(c->device);
   if (cudaMalloc(&m, sizeof(MasterDev)) != cudaSuccess) return nullptr;
-  cudaMemset(m, 0, sizeof(MasterDev));
+  if (cudaMemset(m, 0, sizeof(MasterDev)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(m);
+    return nullptr;
+  }
   g_scratch.v.push_back({c, m});
   return m;
 }

@@ -57,6 +57,10 @@ ghc_status p2p_new(ghc_plan* plan, int rank, int G, bool virt, ghc_p2p** out) {
   const size_t total = p->rank_bytes * (virt ? G : 1);
   CU(cudaMalloc(&p->own, total));
   CU(cudaMemset(p->own, 0, total));
+  // complete before the handle leaves this process: peers' kernels store
+  // into these rows as soon as they launch, and cudaMemset is not ordered
+  // with respect to other processes' work
+  CU(cudaDeviceSynchronize());
   auto bind = [&](int q, char* base) {
     p->gpart[q] = reinterpret_cast<float*>(base);
     p->gcnt[q] = reinterpret_cast<unsigned*>(base + gpart_bytes(G, p->ep));
