@@ -328,7 +328,11 @@ struct ClusterRS {
       ++accepted;
       last_status = 0;
     }
-    __syncthreads();
+    // No CTA barrier here: every thread waited on the mbarrier itself (the
+    // new weights are visible to it), vsub/vnew entries are owned by one
+    // thread, and the next writes into the other weight buffer come from
+    // peers' step (d) of the next round, which needs this CTA's step (b) —
+    // after the barrier that closes the next round's samples.
   }
 
   __device__ void publish(const StepArgs& a, float* gw, float* gv, const float* wa,
