@@ -61,7 +61,7 @@ struct ClusterRS {
   float* recv;           // [2][CS][SL]
   float* vsub;           // [SL] velocity of this CTA's sub-slice
   float* vnew;           // [SL]
-  float* wnew;           // [SL] new weights of the sub-slice (staged until its flag is known)
+  float* wnew;           // [SL] spare (the new weights go straight to the tagged row)
   int* badr;             // [2][CS][4] non-finite flags pushed by the slice owners
   uint64_t* mbp;         // [2] partial rows arrived
   uint64_t* mbw;         // [2] new weights arrived
@@ -238,7 +238,6 @@ struct ClusterRS {
     //     order (bit-identical on every rank) → sgd_step
     unsigned long long* tw = a.tw + ((long long)vrank * 2 + par) * EP;
     const unsigned long long* myrows = rows + (long long)vrank * NCr * EP;
-    int bad = 0;
     for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
       float t = 0.0f;
       for (int c0 = 0; c0 < NCr; c0 += kRowBatch) {
@@ -264,21 +263,21 @@ struct ClusterRS {
       } else if (a.mode == MODE_GRAD) {
         a.g_out[e] = t;
       } else if (sgd) {
-        bad |= !is_finite_f(t);
-        // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v
+        // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v.  Each element
+        // carries its own non-finite bit in its tag (2·epoch + bit); step (d)
+        // ORs the bits of a slice and (e) the slices' flags, so one
+        // non-finite entry anywhere rejects the whole update (optim.cpp:49-51)
+        // without a CTA barrier here.
+        const unsigned bad_e = is_finite_f(t) ? 0u : 1u;
         const float vn = fmaf(a.mu, vsub[e - s0], -a.lr * t);
         vnew[e - s0] = vn;
-        wnew[e - s0] = wa[e] + vn;
+        st_tag(tw + e, wa[e] + vn, tag | bad_e);
       }
     }
     if (!sgd) {
       __syncthreads();
       return;
     }
-    // publish the sub-slice once its non-finite bit is known (tag = 2·epoch + bit)
-    bad = __syncthreads_or(bad);
-    for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x)
-      if (e != P) st_tag(tw + e, wnew[e - s0], tag | (unsigned)bad);
     // weights-row elements that no sub-slice owns (e ≥ E, e == P) get a plain tag
     if (cl == 0)
       for (int e = max(E - 1, e0) + threadIdx.x; e < e0 + SL; e += blockDim.x)
