@@ -241,12 +241,12 @@ def run_ours(args):
 
 
 # ncu --set full of one 200-round launch of lstm_round_kernel<5,20,10,3,4>
-# (profiles/r01_ncu_full_round_spread_raw.csv): dram__bytes_read.sum 63.51 MB +
-# dram__bytes_write.sum 1.74 MB → per round.  Algorithmic: the gathered batch,
+# (profiles/r01_ncu_full_round_final_r1_raw.csv): dram__bytes_read.sum 63.50 MB +
+# dram__bytes_write.sum 1.44 MB → per round.  Algorithmic: the gathered batch,
 # 1000 × (50 + 1) × 4 B = 204 KB; the excess is 32-B sector granularity on the
 # unaligned 200-B rows and 4-B labels.
-TRAFFIC_PER_ROUND = (63.512832e6 + 1.744640e6) / 200
-TRAFFIC_SOURCE = ("ncu --set full, 200-round launch (profiles/r01_ncu_full_round_spread_raw.csv): "
+TRAFFIC_PER_ROUND = (63.499776e6 + 1.436672e6) / 200
+TRAFFIC_SOURCE = ("ncu --set full, 200-round launch (profiles/r01_ncu_full_round_final_r1_raw.csv): "
                   "dram read+write / 200; traffic = per round × timed rounds")
 
 
