@@ -88,11 +88,35 @@ ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_
                        float alpha) {
   if (M < 1 || N < 1 || K < 1) return ghc_fail(GHC_ERR_SHAPE, "gemm: empty operand");
   GemmArgs g{d_a, d_b, d_c, d_bias, d_y, M, N, K, lda, ldb, ldc, ldy, act, alpha, epi};
-  const int bn = N <= 32 ? 32 : 128;
+  // N tile: one 128×BN tile per CTA, one CTA per SM (≈190 KB of stages), so a
+  // launch takes ⌈tiles / SMs⌉ waves of time ∝ BN.  Pick the BN with the
+  // least waves × BN (ties → the larger tile): M = 1000, N = 4096 → BN = 112,
+  // 296 tiles = exactly 2 waves on 148 SMs instead of 256 tiles in 2 waves of
+  // 128-wide tiles.
+  int bn = 32;
+  if (N > 32) {
+    const long long mt = (M + gemm_detail::BM - 1) / gemm_detail::BM;
+    long long best = -1;
+    for (int cand : {128, 112, 96, 64}) {
+      const long long tiles = mt * ((N + cand - 1) / cand);
+      const long long cost = (tiles + c->num_sms - 1) / c->num_sms * cand;
+      if (best < 0 || cost < best) {
+        best = cost;
+        bn = cand;
+      }
+    }
+  }
   CUtensorMap ta, tb;
   if (tma_allowed() && make_map(&ta, d_a, M, K, lda, gemm_detail::BM) &&
-      make_map(&tb, d_b, N, K, ldb, bn))
-    return bn == 32 ? launch_gemm_tma<32>(c, g, ta, tb) : launch_gemm_tma<128>(c, g, ta, tb);
+      make_map(&tb, d_b, N, K, ldb, bn)) {
+    switch (bn) {
+      case 32: return launch_gemm_tma<32>(c, g, ta, tb);
+      case 64: return launch_gemm_tma<64>(c, g, ta, tb);
+      case 96: return launch_gemm_tma<96>(c, g, ta, tb);
+      case 112: return launch_gemm_tma<112>(c, g, ta, tb);
+      default: return launch_gemm_tma<128>(c, g, ta, tb);
+    }
+  }
   if (N <= 32) return launch_gemm<32>(c, g);
   return launch_gemm<128>(c, g);
 }

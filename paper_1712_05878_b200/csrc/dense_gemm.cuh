@@ -18,6 +18,8 @@
 //   activation-derivative / scale → st.global.
 #pragma once
 
+#include <type_traits>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -316,19 +318,48 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
 
 }  // namespace gemm_detail
 
+// tcgen05.ld of W ∈ {16, 32} consecutive 32-bit TMEM columns (32 lanes × W)
+template <int W>
+__device__ __forceinline__ void tmem_ld(uint32_t (&v)[W], uint32_t taddr) {
+  static_assert(W == 16 || W == 32, "chunk");
+  if constexpr (W == 32) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+  } else {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+}
+
 template <int BN>
 __global__ void __launch_bounds__(192, 1)
     tcgen05_gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                             const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using namespace gemm_detail;
-  static_assert(BN == 32 || BN == 64 || BN == 128, "N tile");
+  // BN: any multiple of 16 up to 128 (kind::tf32, M = 128 needs N % 16 == 0);
+  // the host picks it so the tile count fills whole waves of the SMs.
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 128, "N tile");
   constexpr int S = kTmaStages;
   constexpr int A_BYTES = BM * BK * 4;
   constexpr int B_BYTES = BN * BK * 4;
   constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi | A_lo | B_hi | B_lo
   constexpr int NACC = 4;                           // rotating accumulators (accuracy)
-  constexpr int TCOLS = NACC * BN < 32 ? 32 : NACC * BN;
-  static_assert(TCOLS <= 512, "TMEM columns");
+  constexpr int TCOLS = NACC * BN <= 32 ? 32 : NACC * BN <= 64 ? 64 : NACC * BN <= 128 ? 128
+                       : NACC * BN <= 256 ? 256 : 512;  // power of two
+  static_assert(NACC * BN <= 512, "TMEM columns");
   extern __shared__ __align__(1024) uint8_t gsm[];
   __shared__ uint64_t full[S], split[S], empty[S], done;
   __shared__ uint32_t tmem_base_s;
@@ -433,31 +464,22 @@ __global__ void __launch_bounds__(192, 1)
     const int row = m0 + q * 32 + lane;
     const bool vec = (g.N % 4 == 0) && (g.ldc % 4 == 0) &&
                      ((reinterpret_cast<uintptr_t>(g.C) & 15u) == 0);
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float acc[32];
+    // 32-column chunks (+ one 16-column tail when BN % 32 == 16)
+    auto chunk = [&](auto width, int c0) {
+      constexpr int W = decltype(width)::value;
+      float acc[W];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      for (int i = 0; i < W; ++i) acc[i] = 0.f;
       for (int a = 0; a < NACC && a < nkb; ++a) {
-        uint32_t v[32];
+        uint32_t v[W];
         const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + a * BN + c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-              "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        tmem_ld<W>(v, taddr);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(v[i]);
+        for (int i = 0; i < W; ++i) acc[i] += __uint_as_float(v[i]);
       }
       if (row < g.M) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < W; ++i) {
           const int col = n0 + c0 + i;
           float o = acc[i];
           if (col < g.N) {
@@ -468,17 +490,20 @@ __global__ void __launch_bounds__(192, 1)
           acc[i] = o;
         }
         float* crow = g.C + (long long)row * g.ldc + n0 + c0;
-        if (vec && n0 + c0 + 32 <= g.N) {
+        if (vec && n0 + c0 + W <= g.N) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
+          for (int i = 0; i < W; i += 4)
             reinterpret_cast<float4*>(crow)[i / 4] = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
+          for (int i = 0; i < W; ++i)
             if (n0 + c0 + i < g.N) crow[i] = acc[i];
         }
       }
-    }
+    };
+#pragma unroll 1
+    for (int c0 = 0; c0 + 32 <= BN; c0 += 32) chunk(std::integral_constant<int, 32>{}, c0);
+    if constexpr (BN % 32 == 16) chunk(std::integral_constant<int, 16>{}, BN - 16);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
