@@ -1,6 +1,7 @@
 // dense.cu — C ABI for the dense-layer GEMM (tcgen05, 3×TF32) and transpose.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -72,8 +73,40 @@ ghc_status launch_gemm_tma(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta,
                             static_cast<int>(smem)));
     attr_set = true;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + gemm_detail::BM - 1) / gemm_detail::BM);
+  const int nz = g.kchunk > 0 ? (g.K + g.kchunk - 1) / g.kchunk : 1;
+  dim3 grid((g.N + BN - 1) / BN, (g.M + gemm_detail::BM - 1) / gemm_detail::BM, nz);
   tcgen05_gemm_tma_kernel<BN><<<grid, 192, smem, c->stream>>>(ta, tb, g);
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
+// Narrow outputs with a long K (dX of the N = 20 input layer, K = 4096: only
+// ⌈M/128⌉ = 8 tiles for 148 SMs): split K over ≈ one wave of CTAs into
+// per-split partials, then one deterministic combine + epilogue pass.
+ghc_status launch_gemm_splitk(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta,
+                              const CUtensorMap& tb, int nsplit) {
+  int kchunk = (g.K + nsplit - 1) / nsplit;
+  kchunk = (kchunk + gemm_detail::BK - 1) / gemm_detail::BK * gemm_detail::BK;
+  const int nz = (g.K + kchunk - 1) / kchunk;
+  const size_t need = sizeof(float) * static_cast<size_t>(nz) * g.M * g.N;
+  if (need > c->splitk_bytes) {
+    cudaFree(c->splitk_ws);  // synchronising: no launch still uses the old buffer
+    c->splitk_ws = nullptr;
+    c->splitk_bytes = 0;
+    CU(cudaMalloc(&c->splitk_ws, need));
+    c->splitk_bytes = need;
+  }
+  GemmArgs p = g;  // partials: raw sums, [nz][M][N]
+  p.C = c->splitk_ws;
+  p.ldc = g.N;
+  p.epi = EPI_STORE;
+  p.alpha = 1.0f;
+  p.kchunk = kchunk;
+  if (ghc_status st = launch_gemm_tma<32>(c, p, ta, tb)) return st;
+  const long long n = static_cast<long long>(g.M) * g.N;
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * c->num_sms));
+  splitk_reduce_kernel<<<blocks, 256, 0, c->stream>>>(c->splitk_ws, nz, g);
   CU(cudaGetLastError());
   c->launches++;
   return GHC_OK;
@@ -109,6 +142,12 @@ ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_
   CUtensorMap ta, tb;
   if (tma_allowed() && make_map(&ta, d_a, M, K, lda, gemm_detail::BM) &&
       make_map(&tb, d_b, N, K, ldb, bn)) {
+    const long long tiles = static_cast<long long>((M + gemm_detail::BM - 1) / gemm_detail::BM) *
+                            ((N + bn - 1) / bn);
+    if (bn == 32 && tiles * 4 <= c->num_sms && K >= 8 * gemm_detail::BK) {
+      const int nsplit = static_cast<int>(std::min<long long>(c->num_sms / tiles, K / (4 * gemm_detail::BK)));
+      if (nsplit >= 2) return launch_gemm_splitk(c, g, ta, tb, nsplit);
+    }
     switch (bn) {
       case 32: return launch_gemm_tma<32>(c, g, ta, tb);
       case 64: return launch_gemm_tma<64>(c, g, ta, tb);

@@ -44,6 +44,7 @@ struct GemmArgs {
   int act;      // 0 tanh, 1 relu, 2 identity (arch.hpp:10)
   float alpha;
   int epi;
+  int kchunk = 0;  // split-K: CTA z covers K range [z·kchunk, (z+1)·kchunk) (multiple of BK)
 };
 
 namespace gemm_detail {
@@ -366,7 +367,11 @@ __global__ void __launch_bounds__(192, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nkb = (g.K + BK - 1) / BK;
+  // split-K (g.kchunk > 0): this CTA's K range and its own partial-C slice
+  const int kbase = g.kchunk > 0 ? static_cast<int>(blockIdx.z) * g.kchunk : 0;
+  const int klen = g.kchunk > 0 ? min(g.kchunk, g.K - kbase) : g.K;
+  const int nkb = (klen + BK - 1) / BK;
+  if (g.kchunk > 0) g.C += static_cast<long long>(blockIdx.z) * g.M * g.ldc;
 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -400,8 +405,8 @@ __global__ void __launch_bounds__(192, 1)
         mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
 #pragma unroll
         for (int c = 0; c < BK / 4; ++c) {
-          tma_load_2d(st + c * BM * 16, &tmA, kb * BK + 4 * c, m0, &full[s]);
-          tma_load_2d(st + 2 * A_BYTES + c * BN * 16, &tmB, kb * BK + 4 * c, n0, &full[s]);
+          tma_load_2d(st + c * BM * 16, &tmA, kbase + kb * BK + 4 * c, m0, &full[s]);
+          tma_load_2d(st + 2 * A_BYTES + c * BN * 16, &tmB, kbase + kb * BK + 4 * c, n0, &full[s]);
         }
       }
     }
@@ -509,6 +514,22 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+}
+
+// Split-K combine: C = epilogue(Σ_z part[z]) in z order (deterministic),
+// with the same epilogues as the GEMM kernels.
+static __global__ void splitk_reduce_kernel(const float* __restrict__ part, int nz, GemmArgs g) {
+  using namespace gemm_detail;
+  const long long n = static_cast<long long>(g.M) * g.N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(i / g.N), col = static_cast<int>(i % g.N);
+    float o = 0.f;
+    for (int z = 0; z < nz; ++z) o += part[(static_cast<long long>(z) * g.M + row) * g.N + col];
+    if (g.epi == EPI_BIAS_ACT) o = act_f(o + __ldg(g.bias + col), g.act);
+    else if (g.epi == EPI_DACT) o *= dact_from_y(__ldg(g.Y + (long long)row * g.ldy + col), g.act);
+    else o *= g.alpha;
+    g.C[(long long)row * g.ldc + col] = o;
+  }
 }
 
 // Out-of-place transpose: out[c][r] = in[r][c] (32×32 smem tiles).

@@ -123,6 +123,7 @@ void ghc_ctx_destroy(ghc_ctx* c) {
   cudaEventDestroy(c->ev0);
   cudaEventDestroy(c->ev1);
   cudaStreamDestroy(c->stream);
+  cudaFree(c->splitk_ws);
   delete c;
 }
 

@@ -60,6 +60,8 @@ struct ghc_ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::atomic<uint64_t> launches{0};
+  float* splitk_ws = nullptr;  // split-K GEMM partials (dense.cu), grown on demand
+  size_t splitk_bytes = 0;
 };
 
 struct LayeredWorkspace;

@@ -25,7 +25,9 @@ def gemm(ctx, A, B, epi=0, act=2, bias=None, Y=None, alpha=1.0):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (128, 32, 8), (1000, 4096, 20), (250, 300, 77),
-                                   (1000, 4096, 4096), (4096, 20, 1000), (20, 64, 1000)])
+                                   (1000, 4096, 4096), (4096, 20, 1000), (20, 64, 1000),
+                                   # narrow N, long K → split-K (partials + ordered combine)
+                                   (1000, 20, 4096), (130, 3, 2048), (1000, 20, 300), (1, 7, 999)])
 def test_gemm_nt_vs_f64(ctx, M, N, K):
     rng = np.random.default_rng(M * 7 + N + K)
     A = rng.normal(size=(M, K)).astype(np.float32)
@@ -48,6 +50,26 @@ def test_gemm_epilogues(ctx, act):
     assert np.max(np.abs(gemm(ctx, A, B, epi=1, act=act, bias=bias) - ref)) <= 1e-5
     Y = ref.astype(np.float32)
     D = A.astype(np.float64) @ B.astype(np.float64).T
+    d = (1 - Y.astype(np.float64) ** 2) if act == 0 else ((Y > 0) * 1.0 if act == 1 else 1.0)
+    assert np.max(np.abs(gemm(ctx, A, B, epi=2, act=act, Y=Y) - D * d)) <= 1e-5
+    assert np.max(np.abs(gemm(ctx, A, B, alpha=0.25) - 0.25 * D)) <= 1e-5
+
+
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_gemm_splitk_epilogues(ctx, act):
+    """The split-K path applies the same epilogues after the ordered combine,
+    and is deterministic (repeat → same bits)."""
+    rng = np.random.default_rng(10 + act)
+    A = rng.normal(size=(300, 2048)).astype(np.float32) * 0.05
+    B = rng.normal(size=(20, 2048)).astype(np.float32) * 0.05
+    bias = rng.normal(size=20)
+    D = A.astype(np.float64) @ B.astype(np.float64).T
+    Z = D + bias
+    ref = np.tanh(Z) if act == 0 else (np.maximum(Z, 0) if act == 1 else Z)
+    out = gemm(ctx, A, B, epi=1, act=act, bias=bias)
+    assert np.max(np.abs(out - ref)) <= 1e-5
+    assert np.array_equal(out, gemm(ctx, A, B, epi=1, act=act, bias=bias))
+    Y = ref.astype(np.float32)
     d = (1 - Y.astype(np.float64) ** 2) if act == 0 else ((Y > 0) * 1.0 if act == 1 else 1.0)
     assert np.max(np.abs(gemm(ctx, A, B, epi=2, act=act, Y=Y) - D * d)) <= 1e-5
     assert np.max(np.abs(gemm(ctx, A, B, alpha=0.25) - 0.25 * D)) <= 1e-5
