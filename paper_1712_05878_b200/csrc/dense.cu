@@ -99,6 +99,7 @@ ghc_status launch_gemm_splitk(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& 
   }
   GemmArgs p = g;  // partials: raw sums, [nz][M][N]
   p.C = c->splitk_ws;
+  p.CT = nullptr;
   p.ldc = g.N;
   p.epi = EPI_STORE;
   p.alpha = 1.0f;
@@ -113,14 +114,15 @@ ghc_status launch_gemm_splitk(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& 
 }
 }  // namespace
 
-extern "C" {
-
-ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c, int32_t M,
-                       int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc, int32_t epi,
-                       int32_t act, const float* d_bias, const float* d_y, int32_t ldy,
-                       float alpha) {
+namespace ghc {
+ghc_status gemm_nt_ct(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c, int32_t M,
+                      int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc, int32_t epi,
+                      int32_t act, const float* d_bias, const float* d_y, int32_t ldy, float alpha,
+                      float* d_ct, int32_t ldct) {
   if (M < 1 || N < 1 || K < 1) return ghc_fail(GHC_ERR_SHAPE, "gemm: empty operand");
   GemmArgs g{d_a, d_b, d_c, d_bias, d_y, M, N, K, lda, ldb, ldc, ldy, act, alpha, epi};
+  g.CT = d_ct;
+  g.ldct = ldct;
   // N tile: one 128×BN tile per CTA, one CTA per SM (≈190 KB of stages), so a
   // launch takes ⌈tiles / SMs⌉ waves of time ∝ BN.  Pick the BN with the
   // least waves × BN (ties → the larger tile): M = 1000, N = 4096 → BN = 112,
@@ -156,8 +158,22 @@ ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_
       default: return launch_gemm_tma<128>(c, g, ta, tb);
     }
   }
-  if (N <= 32) return launch_gemm<32>(c, g);
-  return launch_gemm<128>(c, g);
+  // register-staged fallback (GHC_GEMM=legacy / unaligned operands): no CT
+  // epilogue there, so transpose the result afterwards
+  if (ghc_status st = N <= 32 ? launch_gemm<32>(c, g) : launch_gemm<128>(c, g)) return st;
+  if (d_ct) return ghc_transpose(c, d_ct, d_c, M, N, ldc, ldct);
+  return GHC_OK;
+}
+}  // namespace ghc
+
+extern "C" {
+
+ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c, int32_t M,
+                       int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc, int32_t epi,
+                       int32_t act, const float* d_bias, const float* d_y, int32_t ldy,
+                       float alpha) {
+  return gemm_nt_ct(c, d_a, d_b, d_c, M, N, K, lda, ldb, ldc, epi, act, d_bias, d_y, ldy, alpha,
+                    nullptr, 0);
 }
 
 ghc_status ghc_transpose(ghc_ctx* c, float* d_out, const float* d_in, int32_t rows, int32_t cols,

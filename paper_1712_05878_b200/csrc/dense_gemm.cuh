@@ -45,6 +45,9 @@ struct GemmArgs {
   float alpha;
   int epi;
   int kchunk = 0;  // split-K: CTA z covers K range [z·kchunk, (z+1)·kchunk) (multiple of BK)
+  float* CT = nullptr;  // optional transposed copy: CT[n][m] (row stride ldct) — the
+  int ldct = 0;         // K-major operand of the next weight-gradient GEMM, written
+                        // coalesced by the epilogue instead of a separate transpose
 };
 
 namespace gemm_detail {
@@ -504,6 +507,11 @@ __global__ void __launch_bounds__(192, 1)
           for (int i = 0; i < W; ++i)
             if (n0 + c0 + i < g.N) crow[i] = acc[i];
         }
+        if (g.CT) {  // lanes = consecutive rows → each store is one coalesced 128-B line
+#pragma unroll
+          for (int i = 0; i < W; ++i)
+            if (n0 + c0 + i < g.N) g.CT[(long long)(n0 + c0 + i) * g.ldct + row] = acc[i];
+        }
       }
     };
 #pragma unroll 1
@@ -529,6 +537,7 @@ static __global__ void splitk_reduce_kernel(const float* __restrict__ part, int 
     else if (g.epi == EPI_DACT) o *= dact_from_y(__ldg(g.Y + (long long)row * g.ldy + col), g.act);
     else o *= g.alpha;
     g.C[(long long)row * g.ldc + col] = o;
+    if (g.CT) g.CT[(long long)col * g.ldct + row] = o;
   }
 }
 

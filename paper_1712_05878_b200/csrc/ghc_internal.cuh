@@ -66,6 +66,15 @@ struct ghc_ctx {
 
 struct LayeredWorkspace;
 
+namespace ghc {
+// ghc_gemm_nt with an optional transposed copy of C (CT[n][m], stride ldct)
+// written by the GEMM epilogue (dense.cu).
+ghc_status gemm_nt_ct(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c, int32_t M,
+                      int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc, int32_t epi,
+                      int32_t act, const float* d_bias, const float* d_y, int32_t ldy, float alpha,
+                      float* d_ct, int32_t ldct);
+}  // namespace ghc
+
 struct ghc_plan {
   ghc_ctx* ctx = nullptr;
   bool layered = false;                 // dense layers: layered.cu path

@@ -158,8 +158,10 @@ struct Buf {
 
 struct LayeredWorkspace {
   Buf xg, yg, h, dh, logits, loss, part, zT, aT, wT;
-  std::vector<Buf> act;  // Y_l per dense layer
+  std::vector<Buf> act;   // Y_l per dense layer
+  std::vector<Buf> actT;  // Y_lᵀ [width][n] (written by the forward GEMM's epilogue)
   Buf dz[2];
+  Buf dzT[2];             // dZᵀ written by the dA GEMM's epilogue
 };
 
 namespace {
@@ -211,6 +213,8 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
   const bool has_lstm = L.front().kind == LayerKind::lstm;
   const int nd = static_cast<int>(L.size()) - 1 - (has_lstm ? 1 : 0);  // dense layers
   ws.act.resize(static_cast<size_t>(nd));
+  ws.actT.resize(static_cast<size_t>(nd));
+  const bool want_grad = g_out != nullptr;
   // 2. LSTM trunk forward → h_T [n × H]
   const float* a = X;
   int a_w = width;
@@ -244,8 +248,16 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
     ti_l[static_cast<size_t>(l)] = ti;
     const float* W = w + m.tensors[static_cast<size_t>(ti)].offset;
     const float* b = w + m.tensors[static_cast<size_t>(ti + 1)].offset;
-    if (ghc_status s = ghc_gemm_nt(c, a, W, ws.act[static_cast<size_t>(l)].p, n, d.b, d.a, a_w, d.a,
-                                   d.b, GHC_EPI_BIAS_ACT, static_cast<int>(d.act), b, nullptr, 0, 1.0f))
+    // Y_l feeds layer l+1's weight gradient as the K-major Y_lᵀ: the epilogue
+    // writes it (coalesced) instead of a separate transpose pass
+    float* yT = nullptr;
+    if (want_grad && l + 1 < nd) {
+      if (ghc_status s = ws.actT[static_cast<size_t>(l)].ensure(static_cast<size_t>(n) * d.b)) return s;
+      yT = ws.actT[static_cast<size_t>(l)].p;
+    }
+    if (ghc_status s = gemm_nt_ct(c, a, W, ws.act[static_cast<size_t>(l)].p, n, d.b, d.a, a_w, d.a,
+                                  d.b, GHC_EPI_BIAS_ACT, static_cast<int>(d.act), b, nullptr, 0, 1.0f,
+                                  yT, n))
       return s;
     a = ws.act[static_cast<size_t>(l)].p;
     a_w = d.b;
@@ -301,11 +313,21 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
                               out, nullptr, 1, n, out))
       return s;
     // dW_l = dZᵀ·A (nn.cpp:327-329): C[out×in] = dZᵀ[out×n] · (Aᵀ[in×n])ᵀ
-    if (ghc_status s = ws.zT.ensure(static_cast<size_t>(out) * n)) return s;
-    if (ghc_status s = ws.aT.ensure(static_cast<size_t>(in) * n)) return s;
-    if (ghc_status s = transpose(c, ws.zT.p, dZ, n, out)) return s;
-    if (ghc_status s = transpose(c, ws.aT.p, A_in[static_cast<size_t>(l)], n, in)) return s;
-    if (ghc_status s = ghc_gemm_nt(c, ws.zT.p, ws.aT.p, g_out + m.tensors[static_cast<size_t>(tw)].offset,
+    // K-major operands: dZᵀ from the previous dA GEMM's epilogue (the head's dZ
+    // is transposed here), Aᵀ from the forward epilogue (the trunk's h here)
+    const float* zT = ws.dzT[cur].p;
+    if (l == nd - 1) {
+      if (ghc_status s = ws.zT.ensure(static_cast<size_t>(out) * n)) return s;
+      if (ghc_status s = transpose(c, ws.zT.p, dZ, n, out)) return s;
+      zT = ws.zT.p;
+    }
+    const float* aT = l > 0 ? ws.actT[static_cast<size_t>(l - 1)].p : nullptr;
+    if (l == 0) {
+      if (ghc_status s = ws.aT.ensure(static_cast<size_t>(in) * n)) return s;
+      if (ghc_status s = transpose(c, ws.aT.p, A_in[static_cast<size_t>(l)], n, in)) return s;
+      aT = ws.aT.p;
+    }
+    if (ghc_status s = ghc_gemm_nt(c, zT, aT, g_out + m.tensors[static_cast<size_t>(tw)].offset,
                                    out, in, n, n, n, in, GHC_EPI_STORE, 2, nullptr, nullptr, 0, 1.0f))
       return s;
     // dA_{l-1} = dZ·W (nn.cpp:330) [n×in] = dZ[n×out] · (Wᵀ[in×out])ᵀ, act' fused
@@ -314,11 +336,14 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
       if (ghc_status s = transpose(c, ws.wT.p, w + m.tensors[static_cast<size_t>(tw)].offset, out, in))
         return s;
       float* dst;
+      float* dstT = nullptr;
       int epi, act_prev;
       const float* Yprev = nullptr;
       if (l > 0) {
         if (ghc_status s = ws.dz[cur ^ 1].ensure(static_cast<size_t>(n) * in)) return s;
+        if (ghc_status s = ws.dzT[cur ^ 1].ensure(static_cast<size_t>(n) * in)) return s;
         dst = ws.dz[cur ^ 1].p;
+        dstT = ws.dzT[cur ^ 1].p;
         epi = GHC_EPI_DACT;
         act_prev = static_cast<int>(L[static_cast<size_t>(l - 1 + (has_lstm ? 1 : 0))].act);
         Yprev = ws.act[static_cast<size_t>(l - 1)].p;
@@ -328,8 +353,8 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
         epi = GHC_EPI_STORE;
         act_prev = 2;
       }
-      if (ghc_status s = ghc_gemm_nt(c, dZ, ws.wT.p, dst, n, in, out, out, out, in, epi, act_prev,
-                                     nullptr, Yprev, in, 1.0f))
+      if (ghc_status s = gemm_nt_ct(c, dZ, ws.wT.p, dst, n, in, out, out, out, in, epi, act_prev,
+                                    nullptr, Yprev, in, 1.0f, dstT, n))
         return s;
       cur ^= 1;
     }
@@ -356,8 +381,9 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
 void layered_free(LayeredWorkspace* ws) {
   if (!ws) return;
   Buf* all[] = {&ws->xg, &ws->yg, &ws->h, &ws->dh, &ws->logits, &ws->loss, &ws->part,
-                &ws->zT, &ws->aT, &ws->wT, &ws->dz[0], &ws->dz[1]};
+                &ws->zT, &ws->aT, &ws->wT, &ws->dz[0], &ws->dz[1], &ws->dzT[0], &ws->dzT[1]};
   for (Buf* b : all) cudaFree(b->p);
   for (Buf& b : ws->act) cudaFree(b.p);
+  for (Buf& b : ws->actT) cudaFree(b.p);
   delete ws;
 }
