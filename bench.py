@@ -256,7 +256,7 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
     B = args.batch
     steps_s = ms / 1e3
     value = world * B * args.steps / steps_s
-    flops_per_round = B * FLOP_PER_SAMPLE
+    flops_per_round = B * FLOP_PER_SAMPLE  # per rank (GPU): one kernel launch each
     achieved_tflops = flops_per_round * args.steps / steps_s / 1e12
     tensor_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) / 2.0  # TF32 ≈ ½ bf16
     fp32_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
@@ -274,17 +274,18 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
                                 else f"NCCL {args.exchange} over NVLink"),
                    "l2": "inputs larger than L2: 182 MB shard/GPU > 126 MB L2, fresh "
                          "shuffled batch gathered every round"},
-        "roofline": {"bound": "tensor", "achieved": achieved_tflops / world * world,
-                     "peak": tensor_peak * world, "unit": "TFLOP/s",
-                     "frac": achieved_tflops / (tensor_peak * world),
+        # per GPU = per launch of the dominant kernel (each rank runs one)
+        "roofline": {"bound": "tensor", "achieved": achieved_tflops,
+                     "peak": tensor_peak, "unit": "TFLOP/s",
+                     "frac": achieved_tflops / tensor_peak,
                      "traffic": args.traffic * args.steps if args.traffic else None,
                      "traffic_per_round_bytes": args.traffic,
                      "algorithmic_bytes_per_round": B * (10 * 5 + 1) * 4,
                      "traffic_source": TRAFFIC_SOURCE,
                      "kernel": kernel + " (fused fwd+bwd+reduce+SGD)",
                      "peak_kind": f"{pk_kind} bf16 sustained / 2 (TF32) per GPU",
-                     "fp32_core": {"peak": fp32_peak * world,
-                                   "frac": achieved_tflops / (fp32_peak * world),
+                     "fp32_core": {"peak": fp32_peak,
+                                   "frac": achieved_tflops / fp32_peak,
                                    "note": "the kernel is FFMA/MUFU/sync-bound by design "
                                            "(DESIGN.md §4)"},
                      "one_round_launch_ms": one_round_ms},

@@ -1,0 +1,45 @@
+"""CPU: the bench.py JSON contract (keys, types, per-GPU roofline) for the
+N = 1 and N > 1 lines, and the reference arm's argument handling — no GPU
+needed (result_line only formats measured numbers)."""
+import argparse
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+REQUIRED = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+            "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+            "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"}
+
+
+def _args(**kw):
+    a = argparse.Namespace(batch=1000, steps=1000, warmup=50, exchange="p2p",
+                           traffic=bench.TRAFFIC_PER_ROUND)
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_result_line_contract(world):
+    ms = 12.5  # 1000 rounds × 12.5 µs
+    e2e = {"value": 7.9e7, "unit": bench.UNIT, "h2d_bytes_per_step": 204000,
+           "d2h_bytes_per_step": 4}
+    line = bench.result_line(_args(), world, ms, None, 1000, e2e, None, 1,
+                             {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": []},
+                             1000, 0, [1.0, 0.1], 0.5, "lstm_round", None)
+    assert REQUIRED <= set(line)
+    assert line["n_gpus"] == world and line["scaling"] == "weak" and line["warmup"] >= 3
+    assert line["value"] == pytest.approx(world * 1000 * 1000 / (ms / 1e3))
+    assert line["config"]["workload"] and "model" not in line["config"]
+    r = line["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and r["unit"] == "TFLOP/s"
+    # per-GPU (per launch) achieved rate; the fraction is the same at any N
+    assert r["achieved"] == pytest.approx(bench.FLOP_PER_SAMPLE * 1000 * 1000 / (ms / 1e3) / 1e12)
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    assert r["traffic"] == pytest.approx(bench.TRAFFIC_PER_ROUND * 1000)
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["gpu_launches"] >= 1
