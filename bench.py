@@ -54,7 +54,12 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled over the clock window: a
+    busy pre-roll of the same kernel (so the GPU is at its load clocks when
+    the timed region starts — an idle GPU drops to 120 MHz within ~1 s) plus
+    the timed region itself.  nvidia-smi's 20 ms period is longer than a
+    20-round timed region (~0.3 ms), so `bracket` adds NVML reads taken
+    immediately before and after the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -63,6 +68,14 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.bracket = []
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self.nvml = None
 
     def __enter__(self):
         try:
@@ -72,17 +85,28 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            t0 = time.time()  # nvidia-smi needs ~0.1-1 s before its first row
-            while not self.rows and time.time() - t0 < 5.0:
-                time.sleep(0.02)
-            self.rows.clear()  # keep only rows sampled during the timed region
         except Exception:
             self.proc = None
         return self
 
+    def started(self):
+        """nvidia-smi delivered its first row (it needs ~0.1-1 s)."""
+        return self.proc is None or bool(self.rows)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([s.strip() for s in line.split(",")])
+
+    def mark(self, tag):
+        """NVML clock read (bracket of the timed region)."""
+        if self.nvml is None:
+            return
+        try:
+            nv, h = self.nvml
+            self.bracket.append({"at": tag, "sm_mhz": nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                 "reasons": int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))})
+        except Exception:
+            pass
 
     def __exit__(self, *a):
         if self.proc:
@@ -102,9 +126,27 @@ class ClockSampler:
                 for nm, v in zip(names, r[3:7]):
                     if v.strip().lower() == "active":
                         reasons.add(nm)
+        # NVML reason bits: 0x8 hw_slowdown, 0x20 sw_thermal, 0x40 hw_thermal, 0x4 sw_power_cap
+        for b in self.bracket:
+            for bit, nm in ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"),
+                            (0x20, "sw_thermal_slowdown"), (0x4, "sw_power_cap")):
+                if b["reasons"] & bit:
+                    reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "busy pre-roll of the same kernel + timed region",
+                "bracket": self.bracket}
+
+
+def preroll(run_chunk, ctx, clk, min_s=0.25):
+    """Keep the GPU busy with the bench's own kernel (untimed) until the
+    clock sampler runs and the clocks are at their load level."""
+    t0 = time.time()
+    while time.time() - t0 < min_s or not clk.started():
+        run_chunk()
+        ctx.sync()
+        if time.time() - t0 > 10.0:
+            break
 
 
 def dist_env():
@@ -121,7 +163,7 @@ def run_reference(args):
         return 0
     from oracle import oracle as O
     ncores = os.cpu_count() or 1
-    W = max(1, min(ncores - 1, 96))
+    W = args.ref_workers if args.ref_workers > 0 else max(1, min(ncores - 1, 96))
     spec = O.data_spec(96, 9500)
     cfg = O.train_cfg(n_workers=W, batch_size=args.batch, epochs=1000)
     # each step = one sync round of W workers × B samples; bounded sample
@@ -203,9 +245,12 @@ def run_ours(args):
     # ---- timed: K rounds, device-resident roles loop (one persistent launch
     # per `chunk` rounds) ----
     chunk = args.chunk if args.chunk > 0 else args.steps
-    launches0 = ctx.launches
+    mpre = g.Master(arch, w0, 0.01, 0.9)  # pre-roll on its own master: the timed one is untouched
     with ClockSampler(local) as clk:
+        preroll(lambda: mpre.sync_rounds(dx, dy, di, B, B, min(2000, total_rounds)), ctx, clk)
+        launches0 = ctx.launches
         ctx.sync()
+        clk.mark("start")
         ctx.timer_start()
         done = 0
         while done < args.steps:
@@ -215,7 +260,9 @@ def run_ours(args):
             done += r
         ms = ctx.timer_stop()
         ctx.sync()
-    launches = ctx.launches - launches0
+        clk.mark("stop")
+        launches = ctx.launches - launches0
+    del mpre
     _, _, version, rejected = m.read()
     losses = loss.numpy() / B
 
@@ -340,8 +387,10 @@ def run_ours_dist(args, rank, world, local):
     setup_s = time.time() - t0
     m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
     loss = ctx.array(total_rounds)
+    state = {"m": m}
 
     def rounds(r0, n, loss_offset):
+        m = state["m"]
         if p2p:
             ex.sync_rounds(m, dx, dy, di, B, 0, dc, B, n, loss_out=loss, idx_offset=r0 * B,
                            counts_offset=r0 * world, loss_offset=loss_offset)
@@ -352,14 +401,24 @@ def run_ours_dist(args, rank, world, local):
     rounds(0, args.warmup, 0)
     ctx.sync()
     tdist.barrier()
-    launches0 = ctx.launches
     with ClockSampler(local) as clk:
+        # busy pre-roll (untimed, same number of calls on every rank: the
+        # fused exchange pairs the ranks' rounds) on a scratch master
+        state["m"] = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+        for _ in range(args.preroll_calls):
+            rounds(0, min(total_rounds, 2000), 0)
+        ctx.sync()
+        state["m"] = m
+        launches0 = ctx.launches
+        tdist.barrier()
         ctx.sync()
         tdist.barrier()
+        clk.mark("start")
         ctx.timer_start()
         rounds(args.warmup, args.steps, args.warmup)
         ms_local = ctx.timer_stop()
         ctx.sync()
+        clk.mark("stop")
         tdist.barrier()
     t = torch.tensor([ms_local], dtype=torch.float64)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -418,73 +477,102 @@ def run_e2e_dist(args, g, gd, tdist, ctx, arch, ex, x, y, plan, dc, rank, world)
 
 
 def run_e2e(args, g, ctx, arch, x, y, idx):
-    """Same metric through the public API with HOST batches, two ways:
+    """Same metric through the public API with the data on the HOST:
 
-    * streaming (the headline ``e2e``): the K steps' batches sit in pinned
-      host memory (HostArray) and ONE ghc_master_sync_rounds call trains on
-      them — every round the persistent kernel prefetches its next batch rows
+    * host_dataset (the headline ``e2e``): the worker's whole 182 MB shard,
+      its labels and the shuffled index stream live in pinned host memory
+      (HostArray), like the reference's in-memory dataset; ONE
+      ghc_master_sync_rounds call trains K rounds and every round the
+      persistent kernel gathers its freshly shuffled batch rows straight
       from host memory over PCIe (cp.async, one round ahead) and stores the
-      round's loss into pinned host memory.  All K·204 KB of inputs cross
-      host→device and all K losses cross device→host inside the timed region.
-    * per_call: one ghc_memcpy_h2d(batch) + ghc_master_sync_rounds(1 round) +
-      ghc_memcpy_d2h(loss) per step on one stream (the reference's
-      one-batch-per-call usage, launch and copy latencies exposed)."""
-    import ctypes as C
-    from paper_1712_05878_b200 import _lib
-    lib = _lib.load()
+      round's loss to host memory.  The batch assembly the reference arm does
+      per round (oracle/ref_roles.cpp:139-143) is inside the timed region.
+    * pregathered: the K batches already gathered contiguously in pinned
+      host memory (the gather done before timing), one call.
+    * per_call: one batch per API call (zero-copy from pinned host memory,
+      loss stored to host memory), queued, and `per_call_sync` with a host
+      synchronisation after every call (the loss read back each step)."""
     B = args.batch
     K = min(args.steps, args.e2e_steps)
     width = x.shape[1]
-    xb_bytes = B * width * 4
-    yb_bytes = B * 4
+    w0 = g.init_weights(arch, 7)
+
+    # ---- host_dataset ----
+    hX = ctx.host_array(x.shape)
+    hY = ctx.host_array(y.shape, np.int32)
+    hI = ctx.host_array(K * B, np.int32)
+    hl = ctx.host_array(K)
+    hX.np[:] = x
+    hY.np[:] = y
+    hI.np[:] = idx[: K * B]
+    hl.np[:] = np.nan
+    m = g.Master(arch, w0, 0.01, 0.9)
+    m.sync_rounds(hX, hY, hI, B, B, min(3, K), loss_out=hl)  # warm-up
+    ctx.sync()
+    m = g.Master(arch, w0, 0.01, 0.9)
+    hl.np[:] = np.nan
+    ctx.sync()
+    ctx.timer_start()
+    m.sync_rounds(hX, hY, hI, B, B, K, loss_out=hl)
+    ms = ctx.timer_stop()
+    ctx.sync()
+    out = {"value": B * K / (ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": B * (width * 4 + 4 + 4), "d2h_bytes_per_step": 4,
+           "steps": K, "ms_per_step": ms / K, "losses_finite": bool(np.isfinite(hl.np).all()),
+           "path": "ghc_master_sync_rounds with the dataset (182 MB), labels and shuffled index "
+                   "stream in pinned host memory: each round's batch is gathered by the kernel "
+                   "from host memory over PCIe (one round ahead), its loss stored to host memory"}
+    for a in (hX, hY, hI):
+        a.free()
+
+    # ---- pregathered ----
     hx = ctx.host_array((K * B, width))
     hy = ctx.host_array(K * B, np.int32)
-    hl = ctx.host_array(K)
     sel = idx[: K * B]
     hx.np[:] = x[sel]
     hy.np[:] = y[sel]
-    hl.np[:] = np.nan
-    w0 = g.init_weights(arch, 7)
     m = g.Master(arch, w0, 0.01, 0.9)
-    m.sync_rounds(hx, hy, None, B, B, 3, loss_out=hl)  # warm-up (first 3 batches)
+    m.sync_rounds(hx, hy, None, B, B, min(3, K), loss_out=hl)
     ctx.sync()
     m = g.Master(arch, w0, 0.01, 0.9)
     hl.np[:] = np.nan
     ctx.sync()
     ctx.timer_start()
     m.sync_rounds(hx, hy, None, B, B, K, loss_out=hl)
-    ms = ctx.timer_stop()
+    msp = ctx.timer_stop()
     ctx.sync()
-    ok = bool(np.isfinite(hl.np).all())
-    streaming = {"value": B * K / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": xb_bytes + yb_bytes,
-                 "d2h_bytes_per_step": 4, "steps": K, "ms_per_step": ms / K, "losses_finite": ok,
-                 "path": "ghc_master_sync_rounds over K host batches (pinned HostArray, zero-copy): the "
-                         "persistent round kernel prefetches each round's rows from host memory one "
-                         "round ahead and stores each round's loss to host memory"}
+    out["pregathered"] = {"value": B * K / (msp / 1e3), "steps": K, "ms_per_step": msp / K,
+                          "losses_finite": bool(np.isfinite(hl.np).all()),
+                          "path": "K batches pre-gathered contiguously in pinned host memory (gather "
+                                  "outside the timed region); one call streams them zero-copy"}
 
-    # per_call: one batch per API call
+    # ---- per_call: one batch per API call ----
     Kc = min(K, 200)
-    dxb = ctx.array((B, width))
-    dyb = ctx.array(B, np.int32)
-    dl = ctx.array(1)
     for k in range(3):  # warm-up
-        m.sync_rounds(dxb, dyb, None, 0, B, 1, loss_out=dl)
+        m.sync_rounds(hx, hy, None, 0, B, 1, loss_out=hl, idx_offset=0)
     ctx.sync()
+    hl.np[:] = np.nan
     ctx.timer_start()
     for k in range(Kc):
-        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dxb.ptr, hx.offset(k * B * width), xb_bytes))
-        _lib.check(lib.ghc_memcpy_h2d(ctx.h, dyb.ptr, hy.offset(k * B), yb_bytes))
-        m.sync_rounds(dxb, dyb, None, 0, B, 1, loss_out=dl)
-        _lib.check(lib.ghc_memcpy_d2h(ctx.h, hl.offset(k), dl.ptr, 4))
+        m.sync_rounds(hx.sub(k * B), hy.sub(k * B), None, 0, B, 1, loss_out=hl.sub(k))
     msc = ctx.timer_stop()
     ctx.sync()
-    streaming["per_call"] = {"value": B * Kc / (msc / 1e3), "steps": Kc, "ms_per_step": msc / Kc,
-                             "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
-                             "path": "ghc_memcpy_h2d(batch) + ghc_master_sync_rounds(1 round) + "
-                                     "ghc_memcpy_d2h(loss) per step, pinned host buffers, one stream"}
+    out["per_call"] = {"value": B * Kc / (msc / 1e3), "steps": Kc, "ms_per_step": msc / Kc,
+                       "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
+                       "path": "one ghc_master_sync_rounds(1 round) per batch, the batch read "
+                               "zero-copy from pinned host memory and the loss stored to host "
+                               "memory; calls queued on one stream"}
+    t0 = time.perf_counter()
+    for k in range(Kc):
+        m.sync_rounds(hx.sub(k * B), hy.sub(k * B), None, 0, B, 1, loss_out=hl.sub(k))
+        ctx.sync()
+    dt = time.perf_counter() - t0
+    out["per_call_sync"] = {"value": B * Kc / dt, "steps": Kc, "ms_per_step": 1e3 * dt / Kc,
+                            "clock": "host wall clock (perf_counter) — the call returns with its "
+                                     "loss in host memory"}
     for a in (hx, hy, hl):
         a.free()
-    return streaming
+    return out
 
 
 def update_roofline(args, g, ctx):
@@ -542,16 +630,39 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--cpu-rounds", type=int, default=120)
     ap.add_argument("--ref-rounds", type=int, default=40)
+    ap.add_argument("--ref-workers", type=int, default=0,
+                    help="reference arm worker threads (0: one per host core, minus the master)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--preroll-calls", type=int, default=20,
+                    help="N>1: untimed busy calls before the timed region (same on every rank)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "reduce_bcast", "allreduce"])
     ap.add_argument("--traffic", type=float, default=TRAFFIC_PER_ROUND,
                     help="dram bytes per round of the fused kernel from an ncu --set full capture")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args.gpus)
+    _, world, _ = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def spawn(n):
+    """`bench.py --gpus N` without a launcher: run this same command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

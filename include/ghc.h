@@ -103,6 +103,11 @@ ghc_status ghc_plan_set_probe(ghc_plan* plan, uint64_t* d_probe);
  * 3 hardware cluster barrier of 8 CTAs) over `ctas` co-resident CTAs. */
 ghc_status ghc_diag_barrier_bench(ghc_ctx* ctx, int32_t impl, int32_t ctas, int32_t threads,
                                   int32_t iters, double* ns_per);
+/* Synchronise the context's stream and report (then clear) the plan's
+ * device error bit: GHC_ERR_SHAPE "loss: label out of range [0,K)" if any
+ * launch of this plan since the last check met a label outside [0,K)
+ * (nn.cpp:241-244); GHC_OK otherwise. */
+ghc_status ghc_plan_check_error(ghc_plan* plan);
 /* Name of the fused kernel the plan dispatches to (diagnostics). */
 const char* ghc_plan_kernel_name(const ghc_plan* plan);
 /* Cluster variant geometry: co-resident clusters and cluster size (0 = flat). */
@@ -128,9 +133,12 @@ ghc_status ghc_init_weights(const ghc_plan* plan, uint64_t seed, double* h_w);
  *                                        reference's batch mean, nn.cpp:283-297)
  * d_loss_sum[0] = Σ_s ℓ_s                 (loss() = d_loss_sum / n)
  * Samples: rows d_x[s] / d_y[s] for s < n when d_idx == NULL, otherwise the
- * rows d_idx[s] of a device-resident dataset (d_x, d_y).  Labels outside
- * [0,K) → GHC_ERR_SHAPE (nn.cpp:241-244, checked on the host copy only when
- * validate_labels != 0, since that costs a device→host read).
+ * rows d_idx[s] of a device-resident dataset (d_x, d_y).  A label outside
+ * [0,K) (nn.cpp:241-244 throws ShapeError) sets the plan's device error bit
+ * without a host round trip; the launch itself stays asynchronous and the
+ * bit is reported as GHC_ERR_SHAPE by the next synchronising call on the
+ * plan — ghc_plan_check_error, ghc_master_read, ghc_validate,
+ * ghc_session_run — which also clears it.
  * Deterministic: fixed reduction order, bit-identical across repeats. */
 ghc_status ghc_worker_grad(ghc_plan* plan, const float* d_w, const float* d_x,
                            const int32_t* d_y, const int32_t* d_idx, int64_t n,
@@ -291,6 +299,14 @@ ghc_status ghc_p2p_sync_rounds(ghc_master* m, ghc_p2p* p, const float* d_x, cons
                                const int32_t* d_idx, int64_t stride, int64_t idx_vstride,
                                const int32_t* d_counts, int64_t n_max, int32_t n_rounds,
                                float* d_loss_out);
+/* Diagnostics of the cross-process hop (no co-resident round kernels): push
+ * n tagged elements into row `rank` of rank `dst`'s receive rows (system-
+ * scope stores through the IPC mapping, then a stream sync), and check on the
+ * owner that row `src` holds them with tag `tag` (*h_bad = mismatches). */
+ghc_status ghc_p2p_diag_push(ghc_p2p* p, int32_t dst, uint32_t tag, int32_t n);
+ghc_status ghc_p2p_diag_check(ghc_p2p* p, int32_t src, uint32_t tag, int32_t n, int32_t* h_bad);
+/* Elements per receive row (the fused kernel's padded gradient row, EP). */
+int32_t ghc_p2p_row_elems(const ghc_p2p* p);
 
 /* ------------------------------------------------------------------ */
 /* Data layer, host side, bit-identical to the oracle */
@@ -392,6 +408,13 @@ ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_ord
  * stats = {version, rejected, samples absorbed, rounds/steps}. */
 ghc_status ghc_session_read(ghc_session* s, float* h_w, float* h_v, float* h_worker_w,
                             float* h_group_w, uint64_t* stats);
+/* Replace the session's dataset rows (generated from the spec at create)
+ * with caller data of the same shape: h_x[rows][seq_len*input_dim],
+ * h_y[rows], rows = n_files*samples_per_file (SPEC.md:421-448 files hold
+ * f32).  Shards, index streams and batches are unchanged.  Used to feed the
+ * reference's own data (or a poisoned row: non-finite parity tests). */
+ghc_status ghc_session_load_data(ghc_session* s, const float* h_x, const int32_t* h_y,
+                                 int64_t rows);
 /* Held-out set of the master's serial validation:
  * validate every `every` master updates (0 = only at the end) and once at
  * the end of every ghc_session_run (no duplicate if the cadence already

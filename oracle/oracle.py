@@ -308,7 +308,8 @@ def run_sync(arch: Arch, spec: DataSpec, x, y, cfg: TrainCfg, max_trace=100000) 
     return RunOut(w, v, st, trace[:n], {})
 
 
-def run_replay(arch: Arch, spec: DataSpec, x, y, cfg: TrainCfg, order) -> RunOut:
+def run_replay(arch: Arch, spec: DataSpec, x, y, cfg: TrainCfg, order,
+               allow_error=False) -> RunOut:
     P = n_params(arch)
     order = np.ascontiguousarray(order, np.int32)
     w = np.zeros(P); v = np.zeros(P)
@@ -320,9 +321,9 @@ def run_replay(arch: Arch, spec: DataSpec, x, y, cfg: TrainCfg, order) -> RunOut
                               C.byref(cfg), _p(order, C.c_int32), C.c_int64(len(order)),
                               _p(w), _p(v), _p(ww), _p(stale, C.c_int64), _p(trace),
                               C.byref(st))
-    if rc != OK:
+    if rc != OK and not allow_error:
         raise RuntimeError(f"gho_run_replay status {rc}")
-    return RunOut(w, v, st, trace, {"worker_w": ww, "staleness": stale})
+    return RunOut(w, v, st, trace, {"worker_w": ww, "staleness": stale, "rc": rc})
 
 
 def run_hier(arch: Arch, spec: DataSpec, x, y, cfg: TrainCfg, max_trace=100000) -> RunOut:

@@ -86,6 +86,7 @@ SIGNATURES = [
     ("ghc_plan_n_classes", _i32, [_vp]),
     ("ghc_plan_tensors", C.c_int, [_vp, _vp, _vp, _vp, C.c_int, _vp]),
     ("ghc_plan_kernel_name", _cp, [_vp]),
+    ("ghc_plan_check_error", C.c_int, [_vp]),
     ("ghc_plan_set_probe", C.c_int, [_vp, _vp]),
     ("ghc_plan_max_clusters", _i32, [_vp]),
     ("ghc_plan_cluster_size", _i32, [_vp]),
@@ -124,11 +125,15 @@ SIGNATURES = [
     ("ghc_p2p_export", C.c_int, [_vp, _vp]),
     ("ghc_p2p_import", C.c_int, [_vp, _vp]),
     ("ghc_p2p_destroy", None, [_vp]),
+    ("ghc_p2p_diag_push", C.c_int, [_vp, _i32, C.c_uint32, _i32]),
+    ("ghc_p2p_diag_check", C.c_int, [_vp, _i32, C.c_uint32, _i32, _vp]),
+    ("ghc_p2p_row_elems", _i32, [_vp]),
     ("ghc_p2p_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
     ("ghc_session_create", C.c_int, [_vp, _vp, _vp, _vp]),
     ("ghc_session_destroy", None, [_vp]),
     ("ghc_session_run", C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64]),
     ("ghc_session_set_validation", C.c_int, [_vp, _vp, _vp, _i64, _i32]),
+    ("ghc_session_load_data", C.c_int, [_vp, _vp, _vp, _i64]),
     ("ghc_session_validations", C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
     ("ghc_validate", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     ("ghc_frame_size", C.c_int, [_vp, _i32, _i32, _vp]),

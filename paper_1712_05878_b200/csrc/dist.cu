@@ -107,6 +107,14 @@ ghc_status ensure_buffers(ghc_comm* c, int64_t n) {
 
 __global__ void copy_scalar_kernel(float* dst, const float* src) { *dst = *src; }
 
+// Non-root ranks of the reduce/broadcast exchange: the root's sgd_step status
+// arrived by broadcast into ms->status; keep the same version / rejected
+// counters as the root (optim.cpp:49-51, 63).
+__global__ void account_kernel(MasterDev* ms) {
+  if (ms->status == 0) ms->version += 1ull;
+  else ms->rejected += 1ull;
+}
+
 }  // namespace
 
 extern "C" {
@@ -205,13 +213,8 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
   ghc_ctx* ctx = p->ctx;
   const int64_t P = m->P;
   if (ghc_status s = ensure_buffers(comm, P + 1)) return s;
-  int cur = 0;
-  {
-    MasterDev h;
-    CU(cudaMemcpyAsync(&h, m->ms, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    cur = h.cur;
-  }
+  int cur = 0;  // the in-place update below never flips it: cached after one read
+  if (ghc_status s = ghc_master_current(m, &cur)) return s;
   float* w = m->w[cur];
   float* v = m->v[cur];
   const bool master_here = exchange == GHC_EXCHANGE_ALLREDUCE || comm->rank == 0;
@@ -257,8 +260,17 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
         ctx->launches++;
       }
     }
-    if (exchange == GHC_EXCHANGE_REDUCE_BCAST)
+    if (exchange == GHC_EXCHANGE_REDUCE_BCAST) {
       NC(nccl().broadcast(w, w, static_cast<size_t>(P), ncclFloat32, 0, comm->nccl, ctx->stream));
+      // the root's accept/reject decision, so every rank's master reports
+      // the same version / rejected counters
+      NC(nccl().broadcast(&m->ms->status, &m->ms->status, 1, ncclInt32, 0, comm->nccl, ctx->stream));
+      if (!master_here) {
+        account_kernel<<<1, 1, 0, ctx->stream>>>(m->ms);
+        CU(cudaGetLastError());
+        ctx->launches++;
+      }
+    }
   }
   return GHC_OK;
 }

@@ -11,62 +11,39 @@
 
 namespace {
 thread_local std::string g_err;
-
-template <int D, int H, int T, int K, int CS, bool TC>
-constexpr void (*tc_fn())(StepArgs) {
-  if constexpr (TC) return &lstm_round_tc_kernel<D, H, T, K, CS>;
-  else return nullptr;
-}
-
-template <int D, int H, int T, int K, bool TC = true>
-LstmEntry make_entry(const char* name) {
-  using N = LstmNet<D, H, T, K>;
-  using R4 = RoundLayout<D, H, T, K, 4>;
-  using R8 = RoundLayout<D, H, T, K, 8>;
-  using C4 = TcLayout<D, H, T, K, 4>;
-  using C8 = TcLayout<D, H, T, K, 8>;
-  static_assert(C4::EP == R4::EP && C8::EP == R8::EP, "same partial-row layout");
-  return LstmEntry{D,
-                   H,
-                   T,
-                   K,
-                   &lstm_softmax_step_kernel<D, H, T, K>,
-                   {&lstm_round_kernel<D, H, T, K, 4>, &lstm_round_kernel<D, H, T, K, 8>},
-                   {tc_fn<D, H, T, K, 4, TC>(), tc_fn<D, H, T, K, 8, TC>()},
-                   N::P,
-                   N::PPAD,
-                   {R4::EP, R8::EP},
-                   &N::smem_bytes,
-                   {&R4::smem_bytes, &R8::smem_bytes},
-                   {&C4::smem_bytes, &C8::smem_bytes},
-                   name};
-}
-
 }  // namespace
+
+// The instantiated fused-kernel shapes: one translation unit per shape
+// (inst_*.cu, see inst.cuh) so the kernels compile in parallel.
+#define GHC_DECL(D, H, T, K) LstmEntry ghc_entry_##D##_##H##_##T##_##K();
+#define GHC_DECL_TRUNK(D, H, T) LstmEntry ghc_trunk_##D##_##H##_##T();
+GHC_DECL(5, 20, 10, 3)
+GHC_DECL(5, 8, 10, 3)
+GHC_DECL(3, 4, 5, 3)
+GHC_DECL(2, 16, 3, 4)
+GHC_DECL(5, 32, 10, 3)
+GHC_DECL(4, 12, 6, 5)
+GHC_DECL_TRUNK(5, 20, 10)
+GHC_DECL_TRUNK(5, 8, 10)
+GHC_DECL_TRUNK(3, 4, 5)
 
 const std::vector<LstmEntry>& lstm_table() {
   static const std::vector<LstmEntry> t = {
-      make_entry<5, 20, 10, 3>("lstm_round<D5,H20,T10,K3>"),  // SPEC.md:109 bench net
-      make_entry<5, 8, 10, 3>("lstm_round<D5,H8,T10,K3>"),
-      make_entry<3, 4, 5, 3>("lstm_round<D3,H4,T5,K3>"),
-      make_entry<2, 16, 3, 4>("lstm_round<D2,H16,T3,K4>"),
-      make_entry<5, 32, 10, 3>("lstm_round<D5,H32,T10,K3>"),
-      make_entry<4, 12, 6, 5>("lstm_round<D4,H12,T6,K5>"),
+      ghc_entry_5_20_10_3(),  // SPEC.md:109 bench net
+      ghc_entry_5_8_10_3(),  ghc_entry_3_4_5_3(), ghc_entry_2_16_3_4(),
+      ghc_entry_5_32_10_3(), ghc_entry_4_12_6_5(),
   };
   return t;
 }
 
 const std::vector<LstmEntry>& trunk_table() {
   static const std::vector<LstmEntry> t = {
-      make_entry<5, 20, 10, 1, false>("lstm_trunk<D5,H20,T10>"),  // wide variant
-      make_entry<5, 8, 10, 1, false>("lstm_trunk<D5,H8,T10>"),
-      make_entry<3, 4, 5, 1, false>("lstm_trunk<D3,H4,T5>"),
+      ghc_trunk_5_20_10(),  // wide variant
+      ghc_trunk_5_8_10(),
+      ghc_trunk_3_4_5(),
   };
   return t;
 }
-
-
-namespace {}  // namespace
 
 ghc_status ghc_fail(ghc_status s, const std::string& msg) {
   g_err = msg;
@@ -124,6 +101,7 @@ void ghc_ctx_destroy(ghc_ctx* c) {
   cudaEventDestroy(c->ev1);
   cudaStreamDestroy(c->stream);
   cudaFree(c->splitk_ws);
+  cudaFree(c->scratch_ms);
   delete c;
 }
 
@@ -409,6 +387,19 @@ void ghc_plan_destroy(ghc_plan* p) {
   delete p;
 }
 
+ghc_status ghc_plan_check_error(ghc_plan* p) {
+  if (!p) return fail(GHC_ERR_CONFIG, "null plan");
+  int err = 0;
+  CU(cudaMemcpyAsync(&err, p->err, sizeof(int), cudaMemcpyDeviceToHost, p->ctx->stream));
+  CU(cudaStreamSynchronize(p->ctx->stream));
+  if (err) {
+    CU(cudaMemsetAsync(p->err, 0, sizeof(int), p->ctx->stream));
+    CU(cudaStreamSynchronize(p->ctx->stream));
+    return fail(GHC_ERR_SHAPE, "loss: label out of range [0," + std::to_string(p->model.n_classes) + ")");
+  }
+  return GHC_OK;
+}
+
 int64_t ghc_plan_n_params(const ghc_plan* p) { return p->model.n_params; }
 int64_t ghc_plan_input_width(const ghc_plan* p) { return p->model.input_width; }
 int32_t ghc_plan_n_classes(const ghc_plan* p) { return p->model.n_classes; }
@@ -540,6 +531,7 @@ ghc_status ghc_validate(ghc_plan* p, const float* d_w, const float* d_x, const i
     CU(cudaMemcpyAsync(&lsum, loss, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaMemcpyAsync(&ok, cnt, sizeof(ok), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
+    st = ghc_plan_check_error(p);
     if (h_correct) *h_correct = static_cast<int64_t>(ok);
     if (h_loss_mean) *h_loss_mean = static_cast<double>(lsum) / static_cast<double>(n);
   }
@@ -559,15 +551,11 @@ static ghc_status validate_alpha(float alpha) {  // optim.cpp:31-37
 }
 
 namespace {
-struct ScratchMs {
-  std::mutex mu;
-  std::vector<std::pair<ghc_ctx*, MasterDev*>> v;
-};
-ScratchMs g_scratch;
+// Barrier state of the cooperative context-level kernels (sgd_apply,
+// easgd_worker): owned by the context, allocated on first use, freed in
+// ghc_ctx_destroy.
 MasterDev* ctx_scratch_ms(ghc_ctx* c) {
-  std::lock_guard<std::mutex> lk(g_scratch.mu);
-  for (auto& e : g_scratch.v)
-    if (e.first == c) return e.second;
+  if (c->scratch_ms) return c->scratch_ms;
   MasterDev* m = nullptr;
   cudaSetDevice(c->device);
   if (cudaMalloc(&m, sizeof(MasterDev)) != cudaSuccess) return nullptr;
@@ -575,7 +563,7 @@ MasterDev* ctx_scratch_ms(ghc_ctx* c) {
     cudaFree(m);
     return nullptr;
   }
-  g_scratch.v.push_back({c, m});
+  c->scratch_ms = m;
   return m;
 }
 }  // namespace
@@ -707,13 +695,18 @@ void ghc_master_destroy(ghc_master* m) {
   delete m;
 }
 
-static ghc_status master_cur(ghc_master* m, int& cur) {
-  MasterDev h;
-  CU(cudaMemcpyAsync(&h, m->ms, sizeof(h), cudaMemcpyDeviceToHost, m->plan->ctx->stream));
-  CU(cudaStreamSynchronize(m->plan->ctx->stream));
-  cur = h.cur;
+ghc_status ghc_master_current(ghc_master* m, int* cur) {
+  if (!m->host_cur_known) {
+    MasterDev h;
+    CU(cudaMemcpyAsync(&h, m->ms, sizeof(h), cudaMemcpyDeviceToHost, m->plan->ctx->stream));
+    CU(cudaStreamSynchronize(m->plan->ctx->stream));
+    m->host_cur = h.cur;
+    m->host_cur_known = true;
+  }
+  *cur = m->host_cur;
   return GHC_OK;
 }
+static ghc_status master_cur(ghc_master* m, int& cur) { return ghc_master_current(m, &cur); }
 
 ghc_status ghc_master_weights(ghc_master* m, float** d_w, float** d_v) {
   int cur = 0;
@@ -734,7 +727,7 @@ ghc_status ghc_master_read(ghc_master* m, float* h_w, float* h_v, uint64_t* vers
   CU(cudaStreamSynchronize(s));
   if (version) *version = h.version;
   if (rejected) *rejected = h.rejected;
-  return GHC_OK;
+  return ghc_plan_check_error(m->plan);
 }
 
 ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t* d_y,
@@ -799,6 +792,7 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
   a.ms = m->ms;
   a.loss_out = d_loss_out;
   a.mode = MODE_SGD;
+  m->host_cur_known = false;  // the round kernel flips the buffers on device
   return launch_step(m->plan, a, n);
 }
 
@@ -808,6 +802,7 @@ ghc_status ghc_master_apply(ghc_master* m, const float* d_g) {
   const int vec = aligned16(d_g);  // w[], v[] are cudaMalloc-aligned; the tail is scalar
   const int grid = std::min<long long>(occupancy_grid(c, reinterpret_cast<const void*>(sgd_db_kernel), 256),
                                        (m->P / 4 + 255) / 256 + 1);
+  m->host_cur_known = false;  // the last CTA flips ms->cur (or rejects)
   sgd_db_kernel<<<grid, 256, 0, c->stream>>>(m->bufs, m->bufs + 2, d_g, m->P, vec, m->lr, m->mu,
                                              m->ms, m->ms_db);
   CU(cudaGetLastError());

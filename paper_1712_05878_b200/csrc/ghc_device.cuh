@@ -23,6 +23,7 @@ struct MasterDev {
   int flag[2];                 // per-round non-finite flags (parity round & 1)
   unsigned arrive;             // last-CTA-done counter (single-barrier kernels)
   int pad_;
+  unsigned long long samples;  // samples of the accepted rounds (run stats)
 };
 
 // Sense-free generation barrier across all CTAs of a cooperative launch.

@@ -25,8 +25,6 @@ using namespace ghc;
 ghc_status ghc_fail(ghc_status s, const std::string& msg);
 #define fail ghc_fail
 
-namespace {
-
 #define CU(expr)                                                                        \
   do {                                                                                  \
     cudaError_t e_ = (expr);                                                            \
@@ -47,8 +45,6 @@ struct LstmEntry {
   const char* name;
 };
 
-}  // namespace
-
 // The instantiated fused-kernel shapes (defined in ghc.cu only).
 const std::vector<LstmEntry>& lstm_table();
 // LSTM trunk shapes for layered archs (K unused; defined in ghc.cu).
@@ -62,6 +58,7 @@ struct ghc_ctx {
   std::atomic<uint64_t> launches{0};
   float* splitk_ws = nullptr;  // split-K GEMM partials (dense.cu), grown on demand
   size_t splitk_bytes = 0;
+  MasterDev* scratch_ms = nullptr;  // barrier state of the context-level cooperative kernels
 };
 
 struct LayeredWorkspace;
@@ -111,7 +108,14 @@ struct ghc_master {
   MasterDev* ms_db = nullptr;     // bad flag + arrival counter of sgd_db_kernel
   float lr = 0.01f, mu = 0.0f;
   int64_t P = 0;
+  // host copy of ms->cur: valid until a launch that may flip the buffers
+  // (the fused rounds, ghc_master_apply) — saves a blocking D2H per call
+  int host_cur = 0;
+  bool host_cur_known = true;
 };
+
+// Current buffer index of the master (cached; one D2H read when unknown).
+extern "C" ghc_status ghc_master_current(ghc_master* m, int* cur);
 
 namespace {
 

@@ -69,7 +69,7 @@ struct ClusterRS {
   int GX, NCr, vrank, rank, cl;  // ranks; clusters per rank; this CTA's (virtual) rank, cluster in rank
   unsigned epoch;   // this plan's round counter: tags of the rank-local rows
   unsigned xepoch;  // the cross-rank exchange's counter (kept with its buffers, equal on all ranks)
-  unsigned long long accepted, rejected;
+  unsigned long long accepted, rejected, acc_samples;
   int last_status;
   bool sgd;
 
@@ -133,7 +133,7 @@ struct ClusterRS {
     s1 = min(min(e0 + SL, E), s0 + SS);
     epoch = __ldcg(a.bar);
     xepoch = GX > 1 ? __ldcg(a.gcnt[rank] + CS * kFlagStride) : 0u;
-    accepted = rejected = 0;
+    accepted = rejected = acc_samples = 0;
     last_status = 0;
     sgd = a.mode == MODE_SGD;
     if (threadIdx.x == 0) {
@@ -188,7 +188,7 @@ struct ClusterRS {
   // wparts: nw warp partials [nw][pstride] (P gradient entries + loss slot);
   // their sum (warp order) is the CTA partial, formed while pushing.
   __device__ void exchange(const StepArgs& a, int r, const float* wparts, int nw, int pstride,
-                           float*& wa, float*& wb, unsigned long long* pr) {
+                           float*& wa, float*& wb, unsigned long long* pr, int ntot) {
     ++epoch;
     ++xepoch;
     const int par = epoch & 1;                 // L2 rows: epoch parity (survives launches)
@@ -325,6 +325,7 @@ struct ClusterRS {
       wa = wb;
       wb = t;
       ++accepted;
+      acc_samples += (unsigned long long)ntot;
       last_status = 0;
     }
     // No CTA barrier here: every thread waited on the mbarrier itself (the
@@ -348,6 +349,7 @@ struct ClusterRS {
       if (sgd) {
         a.ms->version += accepted;
         a.ms->rejected += rejected;
+        a.ms->samples += acc_samples;
         a.ms->round = round0 + (unsigned long long)a.rounds;
         a.ms->status = last_status;
       }
@@ -390,7 +392,7 @@ struct ClusterXchg {
   int crank, cid, NC, e0, e1;
   int NCr, vrank, rank, cl;  // clusters per rank, this CTA's virtual/global rank, cluster in rank
   unsigned epoch, xepoch;
-  unsigned long long accepted, rejected;
+  unsigned long long accepted, rejected, acc_samples;
   int last_status;
   bool sgd;
 
@@ -410,7 +412,7 @@ struct ClusterXchg {
     epoch = __ldcg(a.bar);
     // cross-rank exchange epoch: kept next to this rank's arrival counters
     xepoch = a.GX > 1 ? __ldcg(a.gcnt[rank] + CS * kFlagStride) : 0u;
-    accepted = rejected = 0;
+    accepted = rejected = acc_samples = 0;
     last_status = 0;
     sgd = a.mode == MODE_SGD;
   }
@@ -511,7 +513,7 @@ struct ClusterXchg {
   }
 
   __device__ void exchange(const StepArgs& a, cg::cluster_group& cluster, int r, float* cpart,
-                           float*& wa, float*& wb, unsigned long long* pr) {
+                           float*& wa, float*& wb, unsigned long long* pr, int ntot) {
     const int par = r & 1;
     // ---- (2) slice j over the cluster via DSMEM → cluster partial in HBM ----
     float* grow = a.part + ((long long)par * NC + cid) * EP;
@@ -596,6 +598,7 @@ struct ClusterXchg {
         wa = wb;
         wb = t;
         ++accepted;
+        acc_samples += (unsigned long long)ntot;
         last_status = 0;
       }
       __syncthreads();
@@ -618,6 +621,7 @@ struct ClusterXchg {
       if (sgd) {
         a.ms->version += accepted;
         a.ms->rejected += rejected;
+        a.ms->samples += acc_samples;
         a.ms->round = round0 + (unsigned long long)a.rounds;
         a.ms->status = last_status;
       }
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
 
     // (the CTA partial — Σ warp partials, warp order — is formed by ClusterRS (a))
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
-    rs.exchange(a, r, wpart, NW, N::PPAD, wa, wb, pr);
+    rs.exchange(a, r, wpart, NW, N::PPAD, wa, wb, pr, ntot);
   }
 
   rs.publish(a, gw, gv, wa, round0);

@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
 
   int cur = 0;
   unsigned long long round0 = 0;
-  unsigned long long accepted = 0, rejected = 0;
+  unsigned long long accepted = 0, rejected = 0, acc_samples = 0;
   int last_status = 0;
   if (a.mode == MODE_SGD) {
     cur = __ldcg(&a.ms->cur);
@@ -866,6 +866,7 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
       } else {
         cur ^= 1;
         ++accepted;
+        acc_samples += (unsigned long long)n;
         last_status = 0;
       }
     }
@@ -876,6 +877,7 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
       a.ms->cur = cur;
       a.ms->version += accepted;
       a.ms->rejected += rejected;
+      a.ms->samples += acc_samples;
       a.ms->round = round0 + (unsigned long long)a.rounds;
       a.ms->status = last_status;
     }

@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_tc_kernel(StepArgs a) {
     if (pr && threadIdx.x == 0) pr[2] = pr[3] = globaltimer();
     cluster.sync();  // CTA partials of the whole cluster complete
     if (pr && threadIdx.x == 0) pr[4] = globaltimer();
-    xc.exchange(a, cluster, r, cpart, wa, wb, pr);
+    xc.exchange(a, cluster, r, cpart, wa, wb, pr, n);
   }
   xc.publish(a, gw, gv, wa, round0);
 }

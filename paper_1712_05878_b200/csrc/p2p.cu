@@ -159,5 +159,66 @@ ghc_status ghc_p2p_sync_rounds(ghc_master* m, ghc_p2p* p, const float* d_x, cons
     a.gpart[q] = p->gpart[q];
     a.gcnt[q] = p->gcnt[q];
   }
+  m->host_cur_known = false;  // the round kernel flips the buffers on device
   return launch_step(m->plan, a, n_max, p->virt ? p->G : 1);
 }
+
+// ---------------------------------------------------------------- diagnostics
+// The cross-process half of the fused exchange without co-resident round
+// kernels (a 2-process single-GPU test must not run ranks whose kernels
+// wait on each other): rank `rank` stores n (value, epoch-tag) 64-bit
+// elements into row `rank` of rank `dst`'s IPC-mapped receive rows with the
+// same system-scope relaxed stores the round kernel uses (ClusterRS::
+// cross_rank_sum), and the owner later reads them back with the kernel's
+// system-scope loads and checks value and tag.
+namespace {
+__device__ __forceinline__ float diag_value(int rank, int e) { return (float)(rank * 4096 + e) + 0.25f; }
+
+__global__ void p2p_diag_push_kernel(uint2* rows, int G, int rank, int ep, int par, unsigned tag, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n && e < ep; e += gridDim.x * blockDim.x) {
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(diag_value(rank, e));
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(rows) + ((long long)par * G + rank) * ep + e;
+    asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+  }
+}
+
+__global__ void p2p_diag_check_kernel(const uint2* rows, int G, int src, int ep, int par, unsigned tag,
+                                      int n, int* bad) {
+  int b = 0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n && e < ep; e += gridDim.x * blockDim.x) {
+    const unsigned long long* p =
+        reinterpret_cast<const unsigned long long*>(rows) + ((long long)par * G + src) * ep + e;
+    unsigned long long w;
+    asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    b += ((unsigned)(w >> 32) != tag) || (__uint_as_float((unsigned)w) != diag_value(src, e));
+  }
+  if (b) atomicAdd(bad, b);
+}
+}  // namespace
+
+extern "C" ghc_status ghc_p2p_diag_push(ghc_p2p* p, int32_t dst, uint32_t tag, int32_t n) {
+  if (!p || dst < 0 || dst >= p->G || !p->gpart[dst]) return fail(GHC_ERR_CONFIG, "p2p_diag_push: bad rank");
+  p2p_diag_push_kernel<<<8, 256, 0, p->plan->ctx->stream>>>(reinterpret_cast<uint2*>(p->gpart[dst]), p->G,
+                                                          p->rank, p->ep, tag & 1u, tag, n);
+  CU(cudaGetLastError());
+  p->plan->ctx->launches++;
+  CU(cudaStreamSynchronize(p->plan->ctx->stream));
+  return GHC_OK;
+}
+
+extern "C" ghc_status ghc_p2p_diag_check(ghc_p2p* p, int32_t src, uint32_t tag, int32_t n, int32_t* h_bad) {
+  if (!p || src < 0 || src >= p->G || !h_bad) return fail(GHC_ERR_CONFIG, "p2p_diag_check: bad argument");
+  int* d_bad = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(int), p->plan->ctx->stream));
+  CU(cudaMemsetAsync(d_bad, 0, sizeof(int), p->plan->ctx->stream));
+  p2p_diag_check_kernel<<<8, 256, 0, p->plan->ctx->stream>>>(reinterpret_cast<const uint2*>(p->gpart[p->rank]),
+                                                           p->G, src, p->ep, tag & 1u, tag, n, d_bad);
+  CU(cudaGetLastError());
+  p->plan->ctx->launches++;
+  CU(cudaMemcpyAsync(h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, p->plan->ctx->stream));
+  CU(cudaFreeAsync(d_bad, p->plan->ctx->stream));
+  CU(cudaStreamSynchronize(p->plan->ctx->stream));
+  return GHC_OK;
+}
+
+extern "C" int32_t ghc_p2p_row_elems(const ghc_p2p* p) { return p ? p->ep : 0; }

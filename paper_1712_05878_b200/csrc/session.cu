@@ -33,6 +33,11 @@ __global__ void __launch_bounds__(256) easgd_exchange_kernel(float* __restrict__
                                                              long long P, float lr, float alpha,
                                                              int exchange, MasterDev* ms,
                                                              int* err, unsigned long long* cver) {
+  // An earlier step already met a non-finite gradient: the reference worker
+  // aborted there (optim.cpp:90-92, oracle gho_run_replay), so nothing after
+  // it may change the center or any worker (err is stream-ordered: every CTA
+  // reads the same value and returns before the grid barrier).
+  if (__ldcg(err) & 2) return;
   const int rej = check_finite_all(g, P, 0, ms);
   if (!rej) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -60,6 +65,21 @@ __global__ void sub_kernel(float* __restrict__ out, const float* __restrict__ a,
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
        i += (long long)gridDim.x * blockDim.x)
     out[i] = a[i] - b[i];
+}
+
+// Async Downpour replay bookkeeping on the device (oracle
+// gho_run_replay): staleness = accepted master updates since the sender's
+// basis, taken before the apply; after it the sender's basis is the current
+// version and its samples count only if the update was accepted — a rejected
+// (non-finite) gradient advances neither (optim.cpp:49-51).
+__global__ void replay_pre_kernel(const MasterDev* ms, const unsigned long long* basis, int k,
+                                  long long* stale_out) {
+  *stale_out = (long long)(ms->version - basis[k]);
+}
+__global__ void replay_post_kernel(const MasterDev* ms, unsigned long long* basis, int k,
+                                   unsigned long long* samples, int n) {
+  basis[k] = ms->version;
+  if (ms->status == 0) *samples += (unsigned long long)n;
 }
 
 struct Batch {
@@ -92,12 +112,15 @@ struct ghc_session {
   float* pseudo = nullptr;                   // [G][P]
   float* comb = nullptr;                     // [P]
   unsigned long long* cver = nullptr;        // EASGD center version
+  unsigned long long* d_basis = nullptr;     // [W] async Downpour: sender basis versions
+  unsigned long long* d_samples = nullptr;   // accepted samples (async Downpour replay)
   MasterDev* ms = nullptr;                   // barrier scratch for cooperative kernels
   int* err = nullptr;
   std::vector<int64_t> basis;                // per worker basis version (host mirror)
   std::vector<uint64_t> bidx;                // per worker batch counter (EASGD)
   // accounting
   int64_t updates = 0, samples = 0, rounds = 0;
+  uint64_t rejected_groups = 0;  // hierarchical: rejected group-master updates
   int64_t trace_cap = 0;  // entries of the caller's loss / staleness buffers
   // the master's serial validation
   float* Xv = nullptr;
@@ -248,7 +271,6 @@ ghc_status run_sync(ghc_session* s, float* h_loss) {
       break;
     }
     counts.push_back(cnt);
-    s->samples += cnt;
   }
   const int R = static_cast<int>(counts.size());
   if (R == 0) return GHC_OK;
@@ -259,6 +281,10 @@ ghc_status run_sync(ghc_session* s, float* h_loss) {
   CU(cudaMalloc(&d_loss, sizeof(float) * counts.size()));
   CU(cudaMemcpy(d_table, table.data(), sizeof(int32_t) * table.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_counts, counts.data(), sizeof(int32_t) * counts.size(), cudaMemcpyHostToDevice));
+  // samples of the ACCEPTED rounds only (oracle gho_run_sync): the round
+  // kernel counts them on the device next to version / rejected
+  MasterDev before{};
+  CU(cudaMemcpy(&before, s->master->ms, sizeof(before), cudaMemcpyDeviceToHost));
   // one persistent launch for all rounds, or chunks of V rounds with the
   // master's serial validation in between (split launches are bit-identical)
   ghc_status st = GHC_OK;
@@ -278,6 +304,9 @@ ghc_status run_sync(ghc_session* s, float* h_loss) {
       h_loss[r] = lo[static_cast<size_t>(r)] / static_cast<float>(counts[static_cast<size_t>(r)]);
   }
   cudaStreamSynchronize(s->plan->ctx->stream);
+  MasterDev after{};
+  CU(cudaMemcpy(&after, s->master->ms, sizeof(after), cudaMemcpyDeviceToHost));
+  s->samples += static_cast<int64_t>(after.samples - before.samples);
   cudaFree(d_table);
   cudaFree(d_counts);
   cudaFree(d_loss);
@@ -293,7 +322,14 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
   float* d_loss = nullptr;
   CU(cudaMalloc(&d_loss, sizeof(float) * (n_order > 0 ? n_order : 1)));
   std::vector<int32_t> counts;
-  int64_t version = 0;
+  int64_t version = 0;  // EASGD: center exchanges (host mirror of cver)
+  const bool downpour = s->cfg.algo == GHC_ALGO_DOWNPOUR;
+  long long* d_stale = nullptr;
+  unsigned long long samples0 = 0;
+  if (downpour) {
+    CU(cudaMalloc(&d_stale, sizeof(long long) * (n_order > 0 ? n_order : 1)));
+    CU(cudaMemcpy(&samples0, s->d_samples, sizeof(samples0), cudaMemcpyDeviceToHost));
+  }
   for (int64_t step = 0; step < n_order; ++step) {
     const int k = order[step];
     if (k < 0 || k >= s->W) return fail(GHC_ERR_PROTOCOL, "replay order names an unknown worker");
@@ -302,21 +338,29 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
     if (ghc_status st = worker_step(s, k, wk, n)) return st;
     if (n == 0) return fail(GHC_ERR_PROTOCOL, "replay order uses a worker that already sent DONE");
     counts.push_back(n);
-    s->samples += n;
     CU(cudaMemcpyAsync(d_loss + step, s->scratch_g + P, sizeof(float), cudaMemcpyDeviceToDevice,
                        c->stream));
-    if (s->cfg.algo == GHC_ALGO_DOWNPOUR) {
-      // sgd_step at the master, reply to the sender only
-      if (h_stale && step < s->trace_cap) h_stale[step] = version - s->basis[static_cast<size_t>(k)];
+    if (downpour) {
+      // sgd_step at the master, reply to the sender only;
+      // staleness / basis / samples follow the device's accepted count
+      replay_pre_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, d_stale + step);
       if (ghc_status st = apply_master(s, s->master, s->scratch_g, s->cfg.lr, s->cfg.mu))
         return st;
-      ++version;  // host mirror (a rejected update is corrected from the device counter)
+      replay_post_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, s->d_samples, n);
+      c->launches += 2;
+      CU(cudaGetLastError());
       CU(cudaMemcpyAsync(wk, s->master->w[0], sizeof(float) * P, cudaMemcpyDeviceToDevice,
                          c->stream));
-      s->basis[static_cast<size_t>(k)] = version;
-      if (s->v_every > 0 && version % s->v_every == 0)
-        if (ghc_status st = validate_now(s)) return st;
+      if (s->v_every > 0) {  // the cadence needs the accepted count (serial)
+        uint64_t ver = 0;
+        CU(cudaMemcpyAsync(&ver, &s->master->ms->version, sizeof(ver), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        if (ver % static_cast<uint64_t>(s->v_every) == 0)
+          if (ghc_status st = validate_now(s)) return st;
+      }
     } else {
+      s->samples += n;
       const uint64_t bi = s->bidx[static_cast<size_t>(k)]++;
       int exch = (bi % static_cast<uint64_t>(s->cfg.tau)) == 0;
       if (h_stale && step < s->trace_cap)
@@ -348,6 +392,16 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
       h_loss[i] = lo[static_cast<size_t>(i)] / counts[static_cast<size_t>(i)];
   }
   CU(cudaStreamSynchronize(c->stream));
+  if (downpour) {
+    if (h_stale && n_order > 0) {
+      const int64_t nt = std::min(n_order, s->trace_cap);
+      CU(cudaMemcpy(h_stale, d_stale, sizeof(long long) * nt, cudaMemcpyDeviceToHost));
+    }
+    unsigned long long samples1 = 0;
+    CU(cudaMemcpy(&samples1, s->d_samples, sizeof(samples1), cudaMemcpyDeviceToHost));
+    s->samples += static_cast<int64_t>(samples1 - samples0);
+    cudaFree(d_stale);
+  }
   cudaFree(d_loss);
   s->rounds += n_order;
   return GHC_OK;
@@ -373,6 +427,7 @@ ghc_status run_hier(ghc_session* s, float* h_loss) {
   CU(cudaMemcpy(hs.data(), s->streams, sizeof(int32_t) * all, cudaMemcpyDeviceToHost));
   std::vector<int32_t> tab(static_cast<size_t>(stride * G));
   std::vector<float> lsum(static_cast<size_t>(G));
+  std::vector<int> gstat(static_cast<size_t>(G), 0);
   for (int64_t r = 0;; ++r) {
     if (s->cfg.max_updates > 0 && r >= s->cfg.max_updates) break;
     bool any_group = false;
@@ -403,12 +458,23 @@ ghc_status run_hier(ghc_session* s, float* h_loss) {
                                                  d_idx + q * stride, stride, nullptr,
                                                  cnt[static_cast<size_t>(q)], 1, d_lsum + q))
         return st;
-      absorbed[static_cast<size_t>(q)] += cnt[static_cast<size_t>(q)];
-      since[static_cast<size_t>(q)] += 1;
-      if (since[static_cast<size_t>(q)] >= s->cfg.flush_k) flushing[static_cast<size_t>(q)] = 1;
+      CU(cudaMemcpyAsync(&gstat[static_cast<size_t>(q)], &s->group[static_cast<size_t>(q)]->ms->status,
+                         sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     }
     CU(cudaMemcpyAsync(lsum.data(), d_lsum, sizeof(float) * G, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
+    // a group update counts toward absorbed / the flush cadence only if the
+    // group master accepted it (oracle gho_run_hier; optim.cpp:49-51)
+    for (int q = 0; q < G; ++q) {
+      if (cnt[static_cast<size_t>(q)] == 0) continue;
+      if (gstat[static_cast<size_t>(q)] == 0) {
+        absorbed[static_cast<size_t>(q)] += cnt[static_cast<size_t>(q)];
+        since[static_cast<size_t>(q)] += 1;
+      } else {
+        ++s->rejected_groups;
+      }
+      if (since[static_cast<size_t>(q)] >= s->cfg.flush_k) flushing[static_cast<size_t>(q)] = 1;
+    }
     for (int q = 0; q < G; ++q)
       if (cnt[static_cast<size_t>(q)] > 0) {
         rl += lsum[static_cast<size_t>(q)];
@@ -431,11 +497,16 @@ ghc_status run_hier(ghc_session* s, float* h_loss) {
     }
     if (nfl > 0) {
       if (ghc_status st = ghc_weighted_mean(c, s->comb, s->pseudo, wts.data(), nfl, P)) return st;
-      for (double v : wts) s->samples += static_cast<int64_t>(v);
       float* tw = nullptr;
       if (ghc_status st = ghc_master_weights(s->master, &tw, nullptr)) return st;
       if (ghc_status st = apply_master(s, s->master, s->comb, s->cfg.parent_lr, s->cfg.parent_mu))
         return st;
+      int tstat = 0;  // the top master's samples count only an accepted update
+      CU(cudaMemcpyAsync(&tstat, &s->master->ms->status, sizeof(int), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      if (tstat == 0)
+        for (double v : wts) s->samples += static_cast<int64_t>(v);
       for (int q = 0; q < G; ++q) {
         if (!flushing[static_cast<size_t>(q)]) continue;
         float* gw = nullptr;
@@ -499,6 +570,10 @@ ghc_status ghc_session_create(ghc_plan* p, const ghc_train_config* cfg, const gh
   CU(cudaMemset(s->err, 0, sizeof(int)));
   CU(cudaMalloc(&s->cver, sizeof(unsigned long long)));
   CU(cudaMemset(s->cver, 0, sizeof(unsigned long long)));
+  CU(cudaMalloc(&s->d_basis, sizeof(unsigned long long) * static_cast<size_t>(s->W)));
+  CU(cudaMemset(s->d_basis, 0, sizeof(unsigned long long) * static_cast<size_t>(s->W)));
+  CU(cudaMalloc(&s->d_samples, sizeof(unsigned long long)));
+  CU(cudaMemset(s->d_samples, 0, sizeof(unsigned long long)));
   std::vector<float> w32(static_cast<size_t>(s->P));
   for (int64_t i = 0; i < s->P; ++i) w32[static_cast<size_t>(i)] = static_cast<float>(w0[static_cast<size_t>(i)]);
   // every worker starts from the initial WEIGHTS message (f32 wire)
@@ -546,6 +621,8 @@ void ghc_session_destroy(ghc_session* s) {
   cudaFree(s->pseudo);
   cudaFree(s->comb);
   cudaFree(s->cver);
+  cudaFree(s->d_basis);
+  cudaFree(s->d_samples);
   cudaFree(s->ms);
   cudaFree(s->err);
   cudaFree(s->Xv);
@@ -588,6 +665,17 @@ ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_ord
   CU(cudaMemcpy(&err, s->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err & 2) return fail(GHC_ERR_NONFINITE, "easgd_worker_step: gradient has NaN/Inf entries");
   return validate_now(s);  // "and once at end"
+}
+
+ghc_status ghc_session_load_data(ghc_session* s, const float* h_x, const int32_t* h_y,
+                                 int64_t rows) {
+  if (!s || !h_x || !h_y) return fail(GHC_ERR_CONFIG, "session: null argument");
+  const int64_t want = static_cast<int64_t>(s->spec.n_files) * s->spec.samples_per_file;
+  if (rows != want) return fail(GHC_ERR_SHAPE, "session_load_data: rows != n_files*samples_per_file");
+  const int64_t width = s->plan->model.input_width;
+  CU(cudaMemcpy(s->X, h_x, sizeof(float) * rows * width, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(s->Y, h_y, sizeof(int32_t) * rows, cudaMemcpyHostToDevice));
+  return GHC_OK;
 }
 
 ghc_status ghc_session_set_validation(ghc_session* s, const float* h_x, const int32_t* h_y,
@@ -641,7 +729,7 @@ ghc_status ghc_session_read(ghc_session* s, float* h_w, float* h_v, float* h_wor
         return st;
   if (stats) {
     stats[0] = ver;
-    stats[1] = rej;
+    stats[1] = rej + s->rejected_groups;
     stats[2] = static_cast<uint64_t>(s->samples);
     stats[3] = static_cast<uint64_t>(s->rounds);
   }

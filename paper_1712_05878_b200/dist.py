@@ -163,16 +163,23 @@ class P2PExchange:
         self.world = world
         lib = self.ctx.lib
         h = C.c_void_p()
+        self.h = None
         if virtual:
             g.check(lib.ghc_p2p_create_virtual(arch.h, world, C.byref(h)), "p2p_create_virtual")
+            self.h = h
         else:
-            g.check(lib.ghc_p2p_create(arch.h, rank, world, C.byref(h)), "p2p_create")
-        self.h = h
-        if not virtual:
-            # Every rank takes part in both all-gathers even when its own step
-            # failed, so a rank that cannot export/map peer memory makes ALL
-            # ranks raise P2PUnavailable (callers fall back to NCCL) instead
-            # of leaving the others blocked in a collective.
+            # Every rank takes part in every agreement even when its own step
+            # failed, so a rank that cannot create, export or map the peer
+            # memory makes ALL ranks raise P2PUnavailable (callers fall back to
+            # NCCL) instead of leaving the others blocked in a collective.
+            rc = lib.ghc_p2p_create(arch.h, rank, world, C.byref(h))
+            why = b"" if rc == 0 else lib.ghc_last_error()[:200]
+            if rc == 0:
+                self.h = h
+            ok, bad = agree(dist, rc == 0, why)
+            if not ok:
+                self.close()
+                raise P2PUnavailable(f"ghc_p2p_create failed: {bad}")
             mine = (C.c_uint8 * self.HANDLE_BYTES)()
             rc = lib.ghc_p2p_export(h, mine)
             ok, allh = agree(dist, rc == 0, bytes(mine))

@@ -162,6 +162,23 @@ class HostArray:
     def offset(self, elements: int) -> C.c_void_p:
         return C.c_void_p(self.ptr.value + elements * self.dtype.itemsize)
 
+    def sub(self, row: int) -> "_View":
+        """View starting at `row` (first-axis index): pass to the C ABI like
+        the array itself (e.g. one batch of a pinned host batch stream)."""
+        step = int(np.prod(self.shape[1:])) if len(self.shape) > 1 else 1
+        return _View(self.offset(row * step))
+
+
+class _View:
+    """A raw pointer that stands in for an array in the C-ABI wrappers."""
+
+    def __init__(self, ptr: C.c_void_p):
+        self.ptr = ptr
+
+    def offset(self, elements: int) -> C.c_void_p:
+        assert elements == 0, "offset into a view"
+        return self.ptr
+
 
 class Architecture:
     """Architecture (arch.hpp:36-57) compiled to a device plan (ghc_plan)."""
@@ -192,6 +209,11 @@ class Architecture:
     @property
     def n_classes(self) -> int:
         return int(self.ctx.lib.ghc_plan_n_classes(self.h))
+
+    def check_error(self):
+        """ghc_plan_check_error: raise ShapeError if a launch of this plan met a
+        label outside [0,K) since the last check (nn.cpp:241-244)."""
+        check(self.ctx.lib.ghc_plan_check_error(self.h), "loss")
 
     @property
     def kernel_name(self) -> str:
@@ -255,6 +277,7 @@ def forward_backward(w: np.ndarray, arch: Architecture, x: np.ndarray, y: np.nda
     g = ctx.array(arch.n_params)
     ls = ctx.array(1)
     worker_grad_device(arch, dw, dx, dy, n, g, ls)
+    arch.check_error()
     return g.numpy(), float(ls.numpy()[0]) / n
 
 
@@ -271,6 +294,7 @@ def forward(w: np.ndarray, arch: Architecture, x: np.ndarray, y: np.ndarray):
     ls = ctx.array(1)
     check(ctx.lib.ghc_forward(arch.h, dw.ptr, dx.ptr, dy.ptr, None, n, probs.ptr, ls.ptr),
           "forward")
+    arch.check_error()
     return probs.numpy(), float(ls.numpy()[0]) / n
 
 
@@ -519,6 +543,12 @@ class Session:
         check(self.ctx.lib.ghc_session_run(self.h, None if o is None else _vp(o), n, _vp(loss),
                                            _vp(stale), cap), "session_run")
         return loss, stale[:n]
+
+    def load_data(self, x: np.ndarray, y: np.ndarray):
+        """Replace the session's dataset rows (same shape as the spec's)."""
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.ascontiguousarray(y, np.int32)
+        check(self.ctx.lib.ghc_session_load_data(self.h, _vp(x), _vp(y), len(y)), "load_data")
 
     def set_validation(self, x: np.ndarray, y: np.ndarray, every: int = 0):
         """Held-out set of the master's serial validation:

@@ -96,13 +96,15 @@ class _Worker:
         self.j += 1
 
 
-def _tok(dist, peer: int, send: bool):
+def _tok(dist, peer: int, send: bool, payload=(0,)):
+    """Control token (gloo); returns the received payload (int64 values)."""
     import torch
-    t = torch.zeros(1, dtype=torch.int32)
+    t = torch.tensor(list(payload), dtype=torch.int64)
     if send:
         dist.send(t, dst=peer)
     else:
         dist.recv(t, src=peer)
+    return t.tolist()
 
 
 def run_async_downpour(arch: g.Architecture, spec, cfg, order, rank: int, world: int, dist):
@@ -136,7 +138,9 @@ def run_async_downpour(arch: g.Architecture, spec, cfg, order, rank: int, world:
             stale.append(version - basis[k])
             g.check(ctx.lib.ghc_sgd_apply(ctx.h, mw.ptr, mv.ptr, C.c_void_p(dst), P, cfg.lr,
                                           cfg.mu, st.ptr, None), "sgd_apply")
-            version += 1
+            # only an accepted update advances the version (optim.cpp:49-51,
+            # oracle gho_run_replay): the rejecting kernel leaves its status
+            version += int(st.numpy()[0]) == 0
             if k == 0:
                 _copy(ctx, wk.w.ptr.value, mw.ptr.value, 4 * P)
             else:
@@ -254,7 +258,10 @@ def run_hierarchical(arch: g.Architecture, spec, cfg, rank: int, world: int, dis
     wk = _Worker(arch, spec, cfg, world, rank)
     counts = gd.round_counts(spec, world, cfg.batch_size, cfg.epochs, cfg.shuffle_seed)
     R = counts.shape[0]
-    plan = _group_history(counts, R, G, Wg, cfg.flush_k)  # deterministic on every rank
+    # flush schedule: kept by each sub-master from its group's ACCEPTED
+    # updates (a rejected group step absorbs nothing, oracle gho_run_hier) and
+    # reported to the top master with one token per round
+    absorbed_q, since_q = 0, 0
     ipc = _Ipc(ctx)
     w0 = g.init_weights(arch, cfg.weight_seed).astype(np.float32)
     if rank == sub:
@@ -298,7 +305,7 @@ def run_hierarchical(arch: g.Architecture, spec, cfg, rank: int, world: int, dis
     for r in range(R + 1):  # round R: data exhausted, final flushes only
         cnt = counts[r] if r < R else np.zeros(world, np.int32)
         gcnt = cnt[sub:sub + Wg]
-        flushing, absorbed = plan[r]
+        flushing, absorbed = [0] * G, [0] * G
         # ---- worker: mean gradient of its next batch at the group weights ----
         if cnt[rank]:
             if rank == sub:
@@ -317,6 +324,20 @@ def run_hierarchical(arch: g.Architecture, spec, cfg, rank: int, world: int, dis
                         _tok(dist, sub + j, send=False)
                 combine(comb, mail, stage, gcnt)
                 sgd(wg, vg, comb.ptr.value, cfg.lr, cfg.mu, st)
+                if int(st.numpy()[0]) == 0:  # accepted
+                    absorbed_q += int(gcnt.sum())
+                    since_q += 1
+                flushing[q] = int(since_q >= cfg.flush_k)
+            else:
+                flushing[q] = int(absorbed_q > 0)  # final flush of a finished group
+            absorbed[q] = absorbed_q
+            if flushing[q]:
+                absorbed_q = since_q = 0
+            if rank != 0:
+                _tok(dist, 0, send=True, payload=(flushing[q], absorbed[q]))
+            else:
+                for qq in range(1, G):
+                    flushing[qq], absorbed[qq] = _tok(dist, qq * Wg, send=False, payload=(0, 0))
             if flushing[q]:
                 # pseudo-gradient snapshot − current (oracle decision 2) → top master
                 _copy(ctx, psd.ptr.value, snap.ptr.value, 4 * P)
@@ -363,27 +384,3 @@ def run_hierarchical(arch: g.Architecture, spec, cfg, rank: int, world: int, dis
     dist.barrier()
     ipc.close()
     return out
-
-
-def _group_history(counts, R, G, Wg, K):
-    """Per round r ≤ R: (flushing flag of each group, samples each group
-    absorbed since its last flush) — the deterministic schedule of run_hier
-    (session.cu), identical on every rank."""
-    absorbed, since = [0] * G, [0] * G
-    hist = []
-    for r in range(R + 1):
-        cnt = counts[r] if r < R else np.zeros(G * Wg, np.int32)
-        fl, ab = [0] * G, [0] * G
-        for q in range(G):
-            c = int(cnt[q * Wg:(q + 1) * Wg].sum())
-            if c:
-                absorbed[q] += c
-                since[q] += 1
-                fl[q] = int(since[q] >= K)
-            else:
-                fl[q] = int(absorbed[q] > 0)
-            ab[q] = absorbed[q]
-            if fl[q]:
-                absorbed[q] = since[q] = 0
-        hist.append((fl, ab))
-    return hist
