@@ -75,6 +75,23 @@ ghc_status ghc_ipc_handle(ghc_ctx* ctx, void* d_base, uint8_t* out_handle);
 ghc_status ghc_ipc_open(ghc_ctx* ctx, const uint8_t* handle, void** d_ptr);
 ghc_status ghc_ipc_close(ghc_ctx* ctx, void* d_ptr);
 ghc_status ghc_memset(ghc_ctx* ctx, void* d_dst, int value, size_t bytes);
+/* Peer copy between GPUs of one process (cudaMemcpyPeerAsync: NVLink on a
+ * B200 box) on ctx's stream — the payload hop of the in-process "nvlink"
+ * Endpoint (adapter/gradhub_cuda.cpp; replaces transport.cpp:25-177's
+ * mailbox copy). */
+ghc_status ghc_memcpy_peer(ghc_ctx* ctx, void* d_dst, int32_t dst_device, const void* d_src,
+                           int32_t src_device, size_t bytes);
+/* WeightSet upload for the drop-in adapter: d_w32[i] = (float)d_w64[i] (the
+ * f32 wire, proto.cpp) and *d_hash = order-independent 64-bit hash of every
+ * (index, f64 bits) — the device-side stale-cache token that replaces
+ * weights_checksum (nn.cpp:66-81) in forward/backward's guard (nn.cpp:
+ * 116-119, 253-260).  d_w32 and d_hash are nullable. */
+ghc_status ghc_weights_import_f64(ghc_ctx* ctx, float* d_w32, const double* d_w64, int64_t p,
+                                  uint64_t* d_hash);
+/* loss (nn.cpp:234-248): *h_sum = Σ_s −log d_probs[s][d_y[s]] (f64, fixed
+ * order); GHC_ERR_SHAPE if a label is outside [0,K).  Synchronising. */
+ghc_status ghc_nll_sum(ghc_ctx* ctx, const double* d_probs, const int32_t* d_y, int64_t n,
+                       int32_t k, double* h_sum);
 /* CUDA-event timer on the context stream: start, then stop returns ms. */
 ghc_status ghc_timer_start(ghc_ctx* ctx);
 ghc_status ghc_timer_stop(ghc_ctx* ctx, float* ms);

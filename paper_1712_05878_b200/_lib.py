@@ -77,6 +77,9 @@ SIGNATURES = [
     ("ghc_memcpy_d2h", C.c_int, [_vp, _vp, _vp, _sz]),
     ("ghc_memcpy_d2d", C.c_int, [_vp, _vp, _vp, _sz]),
     ("ghc_memset", C.c_int, [_vp, _vp, C.c_int, _sz]),
+    ("ghc_memcpy_peer", C.c_int, [_vp, _vp, _i32, _vp, _i32, _sz]),
+    ("ghc_weights_import_f64", C.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    ("ghc_nll_sum", C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
     ("ghc_timer_start", C.c_int, [_vp]),
     ("ghc_timer_stop", C.c_int, [_vp, _vp]),
     ("ghc_plan_create", C.c_int, [_vp, _cp, _vp]),

@@ -71,6 +71,29 @@ int main() {
     thrown = true;
   }
   expect(thrown, "stale cache -> CacheMismatchError", 0);
+  // a value change below f32 resolution with the same version: the device
+  // token hashes the f64 bits, like the reference's FNV checksum (nn.cpp:66-81)
+  thrown = false;
+  try {
+    WeightSet w3 = w32;
+    w3.tensors[2].values[5] = std::nextafter(w3.tensors[2].values[5], 1.0);
+    cuda::backward(w3, arch, fc.cache, b.labels);
+  } catch (const CacheMismatchError&) {
+    thrown = true;
+  }
+  expect(thrown, "f64 value change -> CacheMismatchError", 0);
+  // batch_loss: the fused forward's device loss sum (nn.hpp:68-69)
+  const double bl = batch_loss(w32, arch, b), blc = cuda::batch_loss(w32, arch, b);
+  expect(std::fabs(bl - blc) / bl <= 1e-5, "batch_loss rel", std::fabs(bl - blc) / bl);
+  thrown = false;
+  try {
+    std::vector<int> bad_labels = b.labels;
+    bad_labels[7] = 3;
+    cuda::loss(fc.probs, bad_labels);
+  } catch (const ShapeError&) {
+    thrown = true;
+  }
+  expect(thrown, "loss label out of range -> ShapeError", 0);
 
   // sgd_step + serial training loop (optim.cpp:39-65)
   OptimState s = OptimState::for_weights(w32, 0.05, 0.9);

@@ -22,7 +22,7 @@ OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libghc.so")
 
 CU_SOURCES = ["ghc.cu", "dist.cu", "p2p.cu", "codec.cu", "session.cu", "dense.cu", "layered.cu",
-              "diag_barrier.cu", "resident.cu", "generic.cu"]
+              "diag_barrier.cu", "adapter_support.cu", "resident.cu", "generic.cu"]
 CXX_SOURCES = ["host_model.cpp"]
 
 NVCC_FLAGS = [

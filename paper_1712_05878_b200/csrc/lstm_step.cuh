@@ -455,7 +455,11 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     for (int k = 0; k < K; ++k) {
       e[sp][k] = expf(z[k] - zmax);
       den += e[sp][k];
-      if (k == label[sp]) zy = z[k];
+      // z[label] as a branch-free select: `if (k == label) zy = z[k]` lets the
+      // compiler fold the unrolled loop into z[label] — a dynamically
+      // indexed array in local memory (STL/LDL in the round kernel)
+      zy = __uint_as_float((__float_as_uint(z[k]) & (k == label[sp] ? 0xffffffffu : 0u)) |
+                           __float_as_uint(zy));
     }
     inv_den[sp] = 1.0f / den;
     loss[sp] = logf(den) - (zy - zmax);
@@ -650,6 +654,7 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
     round0 = __ldcg(&a.ms->round);
   }
   unsigned epoch = __ldcg(a.bar);
+  const bool trunk = a.mode == MODE_TRUNK_FWD || a.mode == MODE_TRUNK_GRAD;
 
   // Sample s of round r handled by this warp: CTA b owns [b*spc, (b+1)*spc).
   auto first_sample = [&](int r, int& s, int& s1) {
@@ -722,7 +727,8 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
         else cp_async_wait<0>();       // no newer group on the last round
         __syncwarp();
         int label = lbuf[r & 1];
-        if (label < 0 || label >= K) {
+        // the trunk of a deeper net has no labels here (the head kernel checks them)
+        if (!trunk && (label < 0 || label >= K)) {
           if (lane == 0) atomicOr(a.err, 1);
           label = 0;
         }
@@ -756,10 +762,11 @@ __global__ void __launch_bounds__(256, 1) lstm_softmax_step_kernel(StepArgs a) {
         for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(a.x + (long long)row * N::XW + i);
         int label = __ldg(a.y + row);
         __syncwarp();
-        if (label < 0 || label >= K) {
+        if (!trunk && (label < 0 || label >= K)) {
           if (lane == 0) atomicOr(a.err, 1);
           label = 0;
         }
+        if (trunk) label = 0;
         if (a.mode == MODE_FWD) {
           lsum += lstm_sample<D, H, T, K, false>(
               wsm, ws, wp, xs, label, scale, lane,

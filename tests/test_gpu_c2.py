@@ -137,11 +137,11 @@ def _p2p_rank(rank, world, port, outdir):
     res = []
     for tag in (1, 2, 3):  # both parities, epochs advancing
         for dst in range(world):
-            gg.check(lib.ghc_p2p_diag_push(ex.h, dst, tag, n), "diag_push")
+            gg.gradhub.check(lib.ghc_p2p_diag_push(ex.h, dst, tag, n), "diag_push")
         dist.barrier()  # every rank's stores done (each push ends with a stream sync)
         for src in range(world):
             bad = C.c_int32(-1)
-            gg.check(lib.ghc_p2p_diag_check(ex.h, src, tag, n, C.byref(bad)), "diag_check")
+            gg.gradhub.check(lib.ghc_p2p_diag_check(ex.h, src, tag, n, C.byref(bad)), "diag_check")
             res.append(bad.value)
         dist.barrier()
     np.save(os.path.join(outdir, f"p2p{rank}.npy"), np.array(res + [n]))
