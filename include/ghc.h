@@ -166,6 +166,14 @@ ghc_status ghc_forward(ghc_plan* plan, const float* d_w, const float* d_x,
                        const int32_t* d_y, const int32_t* d_idx, int64_t n,
                        float* d_probs, float* d_loss_sum);
 
+/* The LSTM layer's LayerCache (nn.hpp:15-23) for a batch: gates [n×T×4H]
+ * (i,f,g,o after the nonlinearity), cell c_t, tanh(c_t), hidden h_t
+ * [n×T×H], each nullable.  Computed by the generic GEMM-based LSTM
+ * (generic.cu: per-timestep tcgen05 GEMMs + cell kernels) — the fused round
+ * kernels never materialise them.  The first layer must be an LSTM. */
+ghc_status ghc_forward_cache(ghc_plan* plan, const float* d_w, const float* d_x, int64_t n,
+                             float* d_gates, float* d_cell, float* d_tanh, float* d_hidden);
+
 /* ------------------------------------------------------------------ */
 /* Dense layers (nn.cpp:129-145, 312-334) on tcgen05 tensor cores       */
 /* ------------------------------------------------------------------ */

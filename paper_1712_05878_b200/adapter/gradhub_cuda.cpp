@@ -179,6 +179,27 @@ ForwardResult forward(const WeightSet& w, const Architecture& arch, const Batch&
   out.cache.arch_signature = format_architecture(arch);
   out.cache.layers.resize(arch.layers.size());
   out.cache.layers[0].x = batch.inputs;
+  out.cache.layers.back().probs = out.probs.p;
+  if (const auto* l0 = std::get_if<LstmSpec>(&arch.layers[0])) {
+    // the LSTM LayerCache (nn.hpp:15-23) from the generic GEMM-based forward
+    const size_t T = l0->seq_len, H = l0->hidden_dim, nT = n * T;
+    Dev dg(nT * 4 * H * 4), dc(nT * H * 4), dt(nT * H * 4), dh(nT * H * 4);
+    check(ghc_forward_cache(p, dw.w32.as<float>(), dx.as<float>(), static_cast<int64_t>(n), dg.as<float>(),
+                            dc.as<float>(), dt.as<float>(), dh.as<float>()),
+          "forward cache");
+    LayerCache& lc = out.cache.layers[0];
+    auto fill = [](std::vector<double>& dst, const std::vector<float>& src) { dst.assign(src.begin(), src.end()); };
+    fill(lc.gates, download(dg, nT * 4 * H));
+    fill(lc.cell, download(dc, nT * H));
+    fill(lc.tanh_c, download(dt, nT * H));
+    fill(lc.hidden, download(dh, nT * H));
+    if (arch.layers.size() == 2) {  // the softmax layer's input is h_T
+      LayerCache& sc = out.cache.layers[1];
+      sc.x.resize(n * H);
+      for (size_t s = 0; s < n; ++s)
+        for (size_t u = 0; u < H; ++u) sc.x[s * H + u] = lc.hidden[(s * T + T - 1) * H + u];
+    }
+  }
   return out;
 }
 

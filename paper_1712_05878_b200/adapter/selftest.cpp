@@ -54,6 +54,23 @@ int main() {
   double pd = 0;
   for (size_t i = 0; i < fr.probs.p.size(); ++i) pd = std::fmax(pd, std::fabs(fr.probs.p[i] - fc.probs.p[i]));
   expect(pd <= 2e-6, "forward probs max|dp|", pd);
+  {  // the LSTM LayerCache (nn.hpp:15-23): gates, cell, tanh_c, hidden
+    const LayerCache &a = fr.cache.layers[0], &c = fc.cache.layers[0];
+    double m = 0;
+    bool sized = a.gates.size() == c.gates.size() && a.cell.size() == c.cell.size() &&
+                 a.tanh_c.size() == c.tanh_c.size() && a.hidden.size() == c.hidden.size();
+    if (sized) {
+      for (size_t i = 0; i < a.gates.size(); ++i) m = std::fmax(m, std::fabs(a.gates[i] - c.gates[i]));
+      for (size_t i = 0; i < a.cell.size(); ++i) m = std::fmax(m, std::fabs(a.cell[i] - c.cell[i]));
+      for (size_t i = 0; i < a.tanh_c.size(); ++i) m = std::fmax(m, std::fabs(a.tanh_c[i] - c.tanh_c[i]));
+      for (size_t i = 0; i < a.hidden.size(); ++i) m = std::fmax(m, std::fabs(a.hidden[i] - c.hidden[i]));
+    }
+    expect(sized && m <= 2e-6, "forward LayerCache (gates/cell/tanh/hidden) max|d|", sized ? m : -1.0);
+    const LayerCache &as = fr.cache.layers[1], &cs = fc.cache.layers[1];
+    double ms = 0;
+    for (size_t i = 0; i < as.x.size() && i < cs.x.size(); ++i) ms = std::fmax(ms, std::fabs(as.x[i] - cs.x[i]));
+    expect(as.x.size() == cs.x.size() && ms <= 2e-6, "softmax layer input h_T max|d|", ms);
+  }
   const double lr_ = loss(fr.probs, b.labels), lc = cuda::loss(fc.probs, b.labels);
   expect(std::fabs(lr_ - lc) / lr_ <= 1e-5, "loss rel", std::fabs(lr_ - lc) / lr_);
 

@@ -164,6 +164,36 @@ ghc_status gemm_nt_ct(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c
   if (d_ct) return ghc_transpose(c, d_ct, d_c, M, N, ldc, ldct);
   return GHC_OK;
 }
+// Long-K weight-gradient GEMMs (K = n·T of the generic LSTM path): always
+// split K over ≈ one wave into ordered partials — each partial accumulates a
+// short K range in TMEM (3×TF32 error grows with the accumulated K), and the
+// combine adds them in split order (deterministic).
+ghc_status gemm_nt_splitk(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c, int32_t M,
+                          int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc) {
+  if (M < 1 || N < 1 || K < 1) return ghc_fail(GHC_ERR_SHAPE, "gemm: empty operand");
+  GemmArgs g{d_a, d_b, d_c, nullptr, nullptr, M, N, K, lda, ldb, ldc, 0, 2, 1.0f, GHC_EPI_STORE};
+  g.CT = nullptr;
+  g.ldct = 0;
+  CUtensorMap ta, tb;
+  if (tma_allowed() && N <= 32 && make_map(&ta, d_a, M, K, lda, gemm_detail::BM) &&
+      make_map(&tb, d_b, N, K, ldb, 32)) {
+    const long long tiles = (M + gemm_detail::BM - 1) / gemm_detail::BM;
+    const int nsplit = static_cast<int>(
+        std::max<long long>(1, std::min<long long>(c->num_sms / tiles, K / (4 * gemm_detail::BK))));
+    if (nsplit >= 2) return launch_gemm_splitk(c, g, ta, tb, nsplit);
+  }
+  if (N > 32) {  // column blocks of 32: each block takes the split-K path
+    for (int n0 = 0; n0 < N; n0 += 32) {
+      const int nb = std::min(32, N - n0);
+      if (ghc_status st = gemm_nt_splitk(c, d_a, d_b + static_cast<long long>(n0) * ldb, d_c + n0, M, nb, K,
+                                         lda, ldb, ldc))
+        return st;
+    }
+    return GHC_OK;
+  }
+  return gemm_nt_ct(c, d_a, d_b, d_c, M, N, K, lda, ldb, ldc, GHC_EPI_STORE, 2, nullptr, nullptr, 0,
+                    1.0f, nullptr, 0);
+}
 }  // namespace ghc
 
 extern "C" {

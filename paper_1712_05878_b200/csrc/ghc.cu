@@ -194,31 +194,31 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     return fail(GHC_ERR_CONFIG, e.what());
   }
   const auto& L = p->model.layers;
+  if (L.back().b > 32) {
+    const std::string txt = arch_text;
+    delete p;
+    return fail(GHC_ERR_CONFIG, "softmax head: at most 32 classes on the device path ('" + txt + "')");
+  }
   if (L.size() == 2 && L[0].kind == LayerKind::lstm && L[1].kind == LayerKind::softmax) {
     for (const LstmEntry& e : lstm_table())
       if (e.D == L[0].a && e.H == L[0].b && e.T == L[0].c && e.K == L[1].b) p->lstm = &e;
-    if (!p->lstm) {
-      const std::string txt = arch_text;
-      delete p;
-      return fail(GHC_ERR_CONFIG, "no sm_100a kernel instantiated for architecture '" + txt +
-                                      "' (see DESIGN.md §Kernels for the supported shapes)");
-    }
-  } else {
-    // dense layers: LSTM trunk kernel (if any) + tcgen05 GEMMs (layered.cu)
+  }
+  if (!p->lstm) {
+    // dense layers, or an LSTM shape outside the fused table: LSTM trunk
+    // kernel (table shapes) or the generic GEMM-based LSTM (generic.cu) +
+    // tcgen05 GEMMs (layered.cu)
     p->layered = true;
     if (L[0].kind == LayerKind::lstm) {
       for (const LstmEntry& e : trunk_table())
         if (e.D == L[0].a && e.H == L[0].b && e.T == L[0].c) p->trunk = &e;
-      if (!p->trunk) {
-        const std::string txt = arch_text;
-        delete p;
-        return fail(GHC_ERR_CONFIG, "no LSTM trunk kernel instantiated for '" + txt + "'");
-      }
+      p->generic_lstm = p->trunk == nullptr;
     }
   }
   if (p->layered) {
-    p->kname = p->trunk ? std::string(p->trunk->name) + " + tcgen05 3xTF32 dense GEMMs"
-                        : std::string("tcgen05 3xTF32 dense GEMMs");
+    p->kname = p->trunk          ? std::string(p->trunk->name) + " + tcgen05 3xTF32 dense GEMMs"
+               : p->generic_lstm ? std::string("lstm_gemm (per-timestep tcgen05 GEMMs + cell kernels) + "
+                                               "tcgen05 3xTF32 dense GEMMs")
+                                 : std::string("tcgen05 3xTF32 dense GEMMs");
     CU(cudaSetDevice(c->device));
     p->max_ctas = c->num_sms;
     if (p->trunk) {
@@ -384,6 +384,7 @@ void ghc_plan_destroy(ghc_plan* p) {
   cudaFree(p->err);
   cudaFree(p->bar);
   layered_free(p->ws);
+  generic_lstm_free(p->gws);
   delete p;
 }
 
@@ -730,6 +731,12 @@ ghc_status ghc_master_read(ghc_master* m, float* h_w, float* h_v, uint64_t* vers
   return ghc_plan_check_error(m->plan);
 }
 
+// Layered rounds: the round's samples count only for an accepted update
+// (the fused round kernels do this in their publish step).
+static __global__ void count_accepted_kernel(MasterDev* ms, int n) {
+  if (ms->status == 0) ms->samples += static_cast<unsigned long long>(n);
+}
+
 ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t* d_y,
                                   const int32_t* d_idx, int64_t stride, const int32_t* d_counts,
                                   int64_t n, int32_t n_rounds, float* d_loss_out) {
@@ -771,7 +778,9 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
       const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
       CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid),
                                      dim3(256), args, 0, c->stream));
-      c->launches++;
+      count_accepted_kernel<<<1, 1, 0, c->stream>>>(m->ms, nr);
+      CU(cudaGetLastError());
+      c->launches += 2;
     }
     return GHC_OK;
   }

@@ -62,6 +62,7 @@ struct ghc_ctx {
 };
 
 struct LayeredWorkspace;
+struct GenericLstmWorkspace;
 
 namespace ghc {
 // ghc_gemm_nt with an optional transposed copy of C (CT[n][m], stride ldct)
@@ -70,6 +71,10 @@ ghc_status gemm_nt_ct(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c
                       int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc, int32_t epi,
                       int32_t act, const float* d_bias, const float* d_y, int32_t ldy, float alpha,
                       float* d_ct, int32_t ldct);
+// C[M×N] = A·Bᵀ with K split over ≈ one wave (ordered partials; long-K
+// weight gradients of the generic LSTM path, dense.cu).
+ghc_status gemm_nt_splitk(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c, int32_t M,
+                          int32_t N, int32_t K, int32_t lda, int32_t ldb, int32_t ldc);
 }  // namespace ghc
 
 struct ghc_plan {
@@ -77,6 +82,8 @@ struct ghc_plan {
   bool layered = false;                 // dense layers: layered.cu path
   const LstmEntry* trunk = nullptr;     // LSTM trunk kernel of a layered arch
   LayeredWorkspace* ws = nullptr;
+  bool generic_lstm = false;            // LSTM layer outside the kernel tables: generic.cu
+  GenericLstmWorkspace* gws = nullptr;
   int max_warps = 8;      // warps/CTA that fit the fused kernel's smem
   unsigned long long* probe = nullptr;  // phase-timing probe (diagnostics)
   unsigned* bar = nullptr;  // flag barrier: (2 + max_ctas) 128-B lines
@@ -224,6 +231,14 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
                         const int32_t* idx, int64_t n, float scale, float* g_out,
                         float* loss_out, float* probs);
 void layered_free(LayeredWorkspace* ws);
+
+// generic.cu — LSTM layer of any shape as per-timestep tcgen05 GEMMs + cell kernels.
+ghc_status generic_lstm_fwd(ghc_plan* p, const float* w, const float* X, int n, float* hT_out);
+ghc_status generic_lstm_bwd(ghc_plan* p, const float* w, const float* X, int n, const float* dhT,
+                            float* g_out);
+ghc_status generic_lstm_cache(ghc_plan* p, int n, float* d_gates, float* d_cell, float* d_tanh,
+                              float* d_hidden);
+void generic_lstm_free(GenericLstmWorkspace* ws);
 
 // LSTM trunk (flat kernel of p->trunk, modes MODE_TRUNK_*), cooperative.
 inline ghc_status launch_trunk(ghc_plan* p, StepArgs& a, int64_t n) {

@@ -102,18 +102,24 @@ __global__ void colsum_partial_kernel(float* __restrict__ part, const float* __r
                                       int cols, int chunk) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int ch = blockIdx.y;
+  const int k0 = 4 * blockIdx.z;  // coefficient columns k0..k0+3 (kc up to the head's K)
   if (c >= cols) return;
   const int s0 = ch * chunk, s1 = min(n, s0 + chunk);
+  const int nk = min(4, kc - k0);
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int s = s0; s < s1; ++s) {
     const float xv = X[(long long)s * ldx + c];
     if (coef) {
-      for (int k = 0; k < kc; ++k) acc[k] = fmaf(coef[(long long)s * kc + k], xv, acc[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < nk) acc[k] = fmaf(coef[(long long)s * kc + k0 + k], xv, acc[k]);
     } else {
       acc[0] += xv;
     }
   }
-  for (int k = 0; k < kc; ++k) part[((long long)ch * kc + k) * cols + c] = acc[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < nk) part[((long long)ch * kc + k0 + k) * cols + c] = acc[k];
 }
 
 // Stage 2: out[k*ldo + c] = Σ_chunk part[chunk][k][c] (chunk order).
@@ -171,7 +177,7 @@ ghc_status colsum(ghc_ctx* c, LayeredWorkspace& ws, float* out, int ldo, const f
   const int nch = n < 32 ? n : 32;
   const int chunk = (n + nch - 1) / nch;
   if (ghc_status s = ws.part.ensure(static_cast<size_t>(nch) * kc * cols)) return s;
-  colsum_partial_kernel<<<dim3((cols + 127) / 128, nch), 128, 0, c->stream>>>(
+  colsum_partial_kernel<<<dim3((cols + 127) / 128, nch, (kc + 3) / 4), 128, 0, c->stream>>>(
       ws.part.p, X, ldx, coef, kc, n, cols, chunk);
   colsum_final_kernel<<<dim3((cols + 127) / 128, kc), 128, 0, c->stream>>>(out, ldo, ws.part.p,
                                                                           kc, cols, nch);
@@ -222,17 +228,21 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
   if (has_lstm) {
     const int H = L[0].b;
     if (ghc_status s = ws.h.ensure(static_cast<size_t>(n) * H)) return s;
-    StepArgs sa{};
-    sa.x = X;
-    sa.y = Y;
-    sa.n = n;
-    sa.rounds = 1;
-    sa.grad_scale = 1.0f;
-    sa.w_in = w;
-    sa.ms = p->ms;
-    sa.hio = ws.h.p;
-    sa.mode = MODE_TRUNK_FWD;
-    if (ghc_status s = launch_trunk(p, sa, n)) return s;
+    if (p->generic_lstm) {
+      if (ghc_status s = generic_lstm_fwd(p, w, X, n, ws.h.p)) return s;
+    } else {
+      StepArgs sa{};
+      sa.x = X;
+      sa.y = Y;
+      sa.n = n;
+      sa.rounds = 1;
+      sa.grad_scale = 1.0f;
+      sa.w_in = w;
+      sa.ms = p->ms;
+      sa.hio = ws.h.p;
+      sa.mode = MODE_TRUNK_FWD;
+      if (ghc_status s = launch_trunk(p, sa, n)) return s;
+    }
     a = ws.h.p;
     a_w = H;
     ti = 3;
@@ -360,6 +370,10 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
     }
   }
   // 7. LSTM trunk backward from dh_T (nn.cpp:335-396)
+  if (has_lstm && p->generic_lstm) {
+    const float* dH = nd > 0 ? ws.dh.p : ws.dz[0].p;
+    return generic_lstm_bwd(p, w, X, n, dH, g_out);
+  }
   if (has_lstm) {
     const float* dH = nd > 0 ? ws.dh.p : ws.dz[0].p;
     StepArgs sa{};

@@ -109,11 +109,14 @@ def test_label_out_of_range(ctx):
         g.forward_backward(np.zeros(arch.n_params, np.float32), arch, x, y)
 
 
-def test_unsupported_arch_is_config_error(ctx):
-    with pytest.raises(g.ConfigError):
-        g.Architecture(ctx, "lstm(5,40,10),softmax(40,3)")
+def test_invalid_arch_is_config_error(ctx):
+    """ConfigError only where the reference rejects too (arch.cpp:26-73);
+    shapes outside the fused table run on the generic path (test_gpu_generic)."""
     with pytest.raises(g.ConfigError):
         g.Architecture(ctx, "softmax(3,3),dense(3,3,tanh)")
+    with pytest.raises(g.ConfigError):
+        g.Architecture(ctx, "lstm(5,20,10),softmax(21,3)")
+    assert "lstm_gemm" in g.Architecture(ctx, "lstm(5,40,10),softmax(40,3)").kernel_name
 
 
 @pytest.mark.parametrize("P", [1, 2143, 4097, 16_881_699])
