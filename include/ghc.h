@@ -92,6 +92,13 @@ ghc_status ghc_weights_import_f64(ghc_ctx* ctx, float* d_w32, const double* d_w6
  * order); GHC_ERR_SHAPE if a label is outside [0,K).  Synchronising. */
 ghc_status ghc_nll_sum(ghc_ctx* ctx, const double* d_probs, const int32_t* d_y, int64_t n,
                        int32_t k, double* h_sum);
+/* Device timing without host launch overhead (nvbench's blocking kernel):
+ * ghc_stream_hold queues a 1-thread kernel that spins on a pinned flag, the
+ * caller queues timer_start + the timed work, then ghc_stream_release lets
+ * it all run back to back; ghc_timer_stop as usual.  The gate times out
+ * after 5 s. */
+ghc_status ghc_stream_hold(ghc_ctx* ctx);
+ghc_status ghc_stream_release(ghc_ctx* ctx);
 /* CUDA-event timer on the context stream: start, then stop returns ms. */
 ghc_status ghc_timer_start(ghc_ctx* ctx);
 ghc_status ghc_timer_stop(ghc_ctx* ctx, float* ms);
@@ -125,6 +132,12 @@ ghc_status ghc_diag_barrier_bench(ghc_ctx* ctx, int32_t impl, int32_t ctas, int3
  * launch of this plan since the last check met a label outside [0,K)
  * (nn.cpp:241-244); GHC_OK otherwise. */
 ghc_status ghc_plan_check_error(ghc_plan* plan);
+/* Diagnostics: device-side cost of launching an empty kernel with the round
+ * kernel's launch configuration piece by piece (variant bit 0 cooperative,
+ * bit 1 clusters of 4, bit 2 `smem` bytes of dynamic shared memory): one
+ * gated launch (median) and per launch over 200 back to back, in µs. */
+ghc_status ghc_diag_launch_bench(ghc_ctx* ctx, int32_t variant, int32_t ctas, int32_t threads,
+                                 int32_t smem, double* us_single, double* us_b2b);
 /* Name of the fused kernel the plan dispatches to (diagnostics). */
 const char* ghc_plan_kernel_name(const ghc_plan* plan);
 /* Cluster variant geometry: co-resident clusters and cluster size (0 = flat). */

@@ -80,6 +80,8 @@ SIGNATURES = [
     ("ghc_memcpy_peer", C.c_int, [_vp, _vp, _i32, _vp, _i32, _sz]),
     ("ghc_weights_import_f64", C.c_int, [_vp, _vp, _vp, _i64, _vp]),
     ("ghc_nll_sum", C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    ("ghc_stream_hold", C.c_int, [_vp]),
+    ("ghc_stream_release", C.c_int, [_vp]),
     ("ghc_timer_start", C.c_int, [_vp]),
     ("ghc_timer_stop", C.c_int, [_vp, _vp]),
     ("ghc_plan_create", C.c_int, [_vp, _cp, _vp]),
@@ -94,6 +96,7 @@ SIGNATURES = [
     ("ghc_plan_max_clusters", _i32, [_vp]),
     ("ghc_plan_cluster_size", _i32, [_vp]),
     ("ghc_diag_barrier_bench", C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp]),
+    ("ghc_diag_launch_bench", C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     ("ghc_arch_info", C.c_int, [_cp, _vp, _vp, _vp]),
     ("ghc_init_weights_text", C.c_int, [_cp, _u64, _vp]),
     ("ghc_init_weights", C.c_int, [_vp, _u64, _vp]),

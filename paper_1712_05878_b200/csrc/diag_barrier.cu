@@ -4,6 +4,8 @@
 //   impl 1: gather/broadcast flags (flag_barrier, lstm_step.cuh)
 //   impl 2: all-poll-all: every CTA polls every CTA's padded flag (relaxed)
 //   impl 3: cluster barrier only (barrier.cluster; cluster of 8) — lower bound
+#include <algorithm>
+
 #include "ghc_internal.cuh"
 
 using namespace ghc;
@@ -120,5 +122,75 @@ extern "C" ghc_status ghc_diag_barrier_bench(ghc_ctx* c, int32_t impl, int32_t c
   cudaFree(ms);
   cudaFree(bar);
   cudaFree(out);
+  return GHC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Launch cost of the round kernel's launch configuration, piece by piece
+// (diagnostics for the fixed per-call cost): an empty kernel
+// of `ctas` × `threads` with the flags of `variant` — bit 0: cooperative,
+// bit 1: clusters of 4, bit 2: `smem` bytes of dynamic shared memory.
+// us_single: median CUDA-event time of one launch queued behind a gate
+// (device-side launch + teardown only); us_b2b: per launch over 200
+// back-to-back launches.
+namespace {
+__global__ void empty_kernel(int* sink) {
+  if (sink && threadIdx.x == 0 && blockIdx.x == 0) *sink = 1;
+}
+}  // namespace
+
+extern "C" ghc_status ghc_diag_launch_bench(ghc_ctx* c, int32_t variant, int32_t ctas, int32_t threads,
+                                            int32_t smem, double* us_single, double* us_b2b) {
+  CU(cudaSetDevice(c->device));
+  if (variant & 4)
+    CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(empty_kernel),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = (variant & 4) ? smem : 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (variant & 1) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  if (variant & 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 4;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  int* sink = nullptr;
+  CU(cudaLaunchKernelEx(&cfg, empty_kernel, sink));  // warm-up
+  CU(cudaStreamSynchronize(c->stream));
+  std::vector<float> t;
+  for (int i = 0; i < 21; ++i) {
+    if (ghc_status s = ghc_stream_hold(c)) return s;
+    CU(cudaEventRecord(c->ev0, c->stream));
+    CU(cudaLaunchKernelEx(&cfg, empty_kernel, sink));
+    CU(cudaEventRecord(c->ev1, c->stream));
+    if (ghc_status s = ghc_stream_release(c)) return s;
+    CU(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    t.push_back(ms);
+  }
+  std::sort(t.begin(), t.end());
+  *us_single = 1e3 * t[t.size() / 2];
+  if (ghc_status s = ghc_stream_hold(c)) return s;
+  CU(cudaEventRecord(c->ev0, c->stream));
+  for (int i = 0; i < 200; ++i) CU(cudaLaunchKernelEx(&cfg, empty_kernel, sink));
+  CU(cudaEventRecord(c->ev1, c->stream));
+  if (ghc_status s = ghc_stream_release(c)) return s;
+  CU(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  *us_b2b = 1e3 * ms / 200;
   return GHC_OK;
 }

@@ -113,6 +113,7 @@ __global__ void copy_scalar_kernel(float* dst, const float* src) { *dst = *src; 
 __global__ void account_kernel(MasterDev* ms) {
   if (ms->status == 0) ms->version += 1ull;
   else ms->rejected += 1ull;
+  ms->cur ^= 1;  // the broadcast weights landed in the other buffer, as on the root
 }
 
 }  // namespace
@@ -215,8 +216,6 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
   if (ghc_status s = ensure_buffers(comm, P + 1)) return s;
   int cur = 0;  // the in-place update below never flips it: cached after one read
   if (ghc_status s = ghc_master_current(m, &cur)) return s;
-  float* w = m->w[cur];
-  float* v = m->v[cur];
   const bool master_here = exchange == GHC_EXCHANGE_ALLREDUCE || comm->rank == 0;
   for (int r = 0; r < n_rounds; ++r) {
     const int32_t* cnt = h_counts + static_cast<int64_t>(r) * comm->size;
@@ -224,6 +223,7 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
     for (int k = 0; k < comm->size; ++k) total += cnt[k];
     if (total == 0) break;  // every worker has sent DONE
     const int32_t mine = cnt[comm->rank];
+    float* w = m->w[cur];  // this round's weights (the update flips the double buffer)
     if (mine > 0) {
       if (ghc_status s = ghc_worker_grad(p, w, d_x, d_y,
                                          d_idx ? d_idx + static_cast<int64_t>(r) * stride : nullptr,
@@ -241,25 +241,18 @@ ghc_status ghc_dist_sync_rounds(ghc_master* m, ghc_comm* comm, int32_t exchange,
                        comm->nccl, ctx->stream));
     }
     if (master_here) {
-      // sgd_step with whole-update rejection (optim.cpp:39-65), in place.
-      MasterDev* ms = m->ms_apply;
-      int vec = 1;
-      long long PP = P;
-      float lr = m->lr, mu = m->mu;
-      int* st = &m->ms->status;
-      unsigned long long* ver = &m->ms->version;
-      const float* g = comm->gsum;
-      unsigned long long* rj = &m->ms->rejected;
-      void* args[] = {&w, &v, &g, &PP, &vec, &lr, &mu, &ms, &st, &ver, &rj};
-      const int grid = occupancy_grid(ctx, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
-      CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid),
-                                     dim3(256), args, 0, ctx->stream));
-      ctx->launches++;
+      // sgd_step with whole-update rejection (optim.cpp:39-65): one pass into
+      // the other buffer (sgd_db det mode; a rejection copies the old state)
+      if (ghc_status s = master_apply_det(m, comm->gsum, m->lr, m->mu)) return s;
       if (d_loss_out) {
         copy_scalar_kernel<<<1, 1, 0, ctx->stream>>>(d_loss_out + r, comm->gsum + P);
         ctx->launches++;
       }
+    } else {
+      m->host_cur = cur ^ 1;  // the broadcast lands in the other buffer, as on the root
     }
+    cur ^= 1;
+    w = m->w[cur];
     if (exchange == GHC_EXCHANGE_REDUCE_BCAST) {
       NC(nccl().broadcast(w, w, static_cast<size_t>(P), ncclFloat32, 0, comm->nccl, ctx->stream));
       // the root's accept/reject decision, so every rank's master reports

@@ -102,6 +102,7 @@ void ghc_ctx_destroy(ghc_ctx* c) {
   cudaStreamDestroy(c->stream);
   cudaFree(c->splitk_ws);
   cudaFree(c->scratch_ms);
+  if (c->gate_h) cudaFreeHost(c->gate_h);
   delete c;
 }
 
@@ -173,6 +174,40 @@ ghc_status ghc_memset(ghc_ctx* c, void* d, int v, size_t bytes) {
 }
 ghc_status ghc_timer_start(ghc_ctx* c) {
   CU(cudaEventRecord(c->ev0, c->stream));
+  return GHC_OK;
+}
+// Launch-overhead-free device timing (the "blocking kernel" of nvbench):
+// ghc_stream_hold queues a 1-thread kernel that spins on a pinned host flag,
+// so everything the host queues behind it (the start event, the timed
+// launches, the stop event) reaches the GPU before any of it runs;
+// ghc_stream_release sets the flag.  The events then time the device work
+// only, not the host's launch calls.  The gate gives up after 5 s (never
+// hangs the stream).
+static __global__ void stream_gate_kernel(const volatile int* flag) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    if (*flag) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 5000000000ull) return;
+    __nanosleep(200);
+  }
+}
+ghc_status ghc_stream_hold(ghc_ctx* c) {
+  if (!c->gate_h) {
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&c->gate_h), sizeof(int), cudaHostAllocMapped));
+    CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->gate_d), c->gate_h, 0));
+  }
+  *c->gate_h = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  stream_gate_kernel<<<1, 1, 0, c->stream>>>(c->gate_d);
+  CU(cudaGetLastError());
+  return GHC_OK;
+}
+ghc_status ghc_stream_release(ghc_ctx* c) {
+  if (!c->gate_h) return fail(GHC_ERR_CONFIG, "stream_release without stream_hold");
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *reinterpret_cast<volatile int*>(c->gate_h) = 1;
   return GHC_OK;
 }
 ghc_status ghc_timer_stop(ghc_ctx* c, float* ms) {
@@ -764,23 +799,12 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
                                       1.0f / static_cast<float>(nr), m->g_scratch,
                                       d_loss_out ? d_loss_out + r : nullptr, nullptr))
         return s;
-      float* w = m->w[cur];
-      float* v = m->v[cur];
-      const float* g = m->g_scratch;
-      MasterDev* ms = m->ms_apply;
-      int vec = 1;
-      long long PP = m->P;
-      float lr = m->lr, mu = m->mu;
-      int* st = &m->ms->status;
-      unsigned long long* ver = &m->ms->version;
-      unsigned long long* rj = &m->ms->rejected;
-      void* args[] = {&w, &v, &g, &PP, &vec, &lr, &mu, &ms, &st, &ver, &rj};
-      const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_apply_kernel), 256);
-      CU(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sgd_apply_kernel), dim3(grid),
-                                     dim3(256), args, 0, c->stream));
+      // one-pass double-buffered sgd_step (optim.cpp:39-65); the buffers flip
+      if (ghc_status s = master_apply_det(m, m->g_scratch, m->lr, m->mu)) return s;
+      cur ^= 1;
       count_accepted_kernel<<<1, 1, 0, c->stream>>>(m->ms, nr);
       CU(cudaGetLastError());
-      c->launches += 2;
+      c->launches += 1;
     }
     return GHC_OK;
   }
@@ -803,6 +827,23 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
   a.mode = MODE_SGD;
   m->host_cur_known = false;  // the round kernel flips the buffers on device
   return launch_step(m->plan, a, n);
+}
+
+ghc_status master_apply_det(ghc_master* m, const float* d_g, float lr, float mu) {
+  ghc_ctx* c = m->plan->ctx;
+  int cur = 0;
+  if (ghc_status s = ghc_master_current(m, &cur)) return s;
+  const int vec = aligned16(d_g);
+  const int grid = std::min<long long>(occupancy_grid(c, reinterpret_cast<const void*>(sgd_db_kernel), 256),
+                                       (m->P / 4 + 255) / 256 + 1);
+  sgd_db_kernel<<<grid, 256, 0, c->stream>>>(m->bufs, m->bufs + 2, d_g, m->P, vec, lr, mu, m->ms, m->ms_db, 1);
+  CU(cudaGetLastError());
+  db_fixup_kernel<<<grid, 256, 0, c->stream>>>(m->bufs, m->bufs + 2, m->P, m->ms, m->ms_db);
+  CU(cudaGetLastError());
+  c->launches += 2;
+  m->host_cur = cur ^ 1;  // flips on every call (det mode)
+  m->host_cur_known = true;
+  return GHC_OK;
 }
 
 ghc_status ghc_master_apply(ghc_master* m, const float* d_g) {

@@ -59,6 +59,8 @@ struct ghc_ctx {
   float* splitk_ws = nullptr;  // split-K GEMM partials (dense.cu), grown on demand
   size_t splitk_bytes = 0;
   MasterDev* scratch_ms = nullptr;  // barrier state of the context-level cooperative kernels
+  int* gate_h = nullptr;            // ghc_stream_hold: pinned flag (host view)
+  int* gate_d = nullptr;            //                  (device view)
 };
 
 struct LayeredWorkspace;
@@ -123,6 +125,11 @@ struct ghc_master {
 
 // Current buffer index of the master (cached; one D2H read when unknown).
 extern "C" ghc_status ghc_master_current(ghc_master* m, int* cur);
+// sgd_step on the master's double buffers in ONE pass (sgd_db_kernel, det
+// mode + db_fixup_kernel): the buffers flip on every call, so the host keeps
+// knowing the current index; lr / mu as given (the top master of a
+// hierarchy uses its parent settings).
+extern "C" ghc_status master_apply_det(ghc_master* m, const float* d_g, float lr, float mu);
 
 namespace {
 

@@ -145,10 +145,36 @@ struct ClusterRS {
     }
   }
 
+  // Prologue: the current weights into shared memory (all loads of a
+  // thread in flight before its stores — the loop with interleaved smem
+  // stores serialised one L2 round trip per element) and the velocity of
+  // this CTA's sub-slice.
   __device__ void load_state(const float* gw, const float* gv, float* wbuf) {
-    for (int p = threadIdx.x; p < P; p += blockDim.x) wbuf[p] = __ldcg(gw + p);
-    if (sgd)
-      for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) vsub[e - s0] = e < P ? __ldcg(gv + e) : 0.f;
+    const float vs = (sgd && s0 + (int)threadIdx.x < s1 && s0 + (int)threadIdx.x < P) ? __ldcg(gv + s0 + threadIdx.x) : 0.f;
+    if ((reinterpret_cast<uintptr_t>(gw) & 15u) == 0) {
+      constexpr int P4 = P / 4;
+      const float4* g4 = reinterpret_cast<const float4*>(gw);
+      for (int base = threadIdx.x; base < P4; base += 4 * blockDim.x) {
+        float4 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = base + i * blockDim.x;
+          v[i] = q < P4 ? __ldcg(g4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = base + i * blockDim.x;
+          if (q < P4) reinterpret_cast<float4*>(wbuf)[q] = v[i];
+        }
+      }
+      for (int p = 4 * P4 + threadIdx.x; p < P; p += blockDim.x) wbuf[p] = __ldcg(gw + p);
+    } else {
+      for (int p = threadIdx.x; p < P; p += blockDim.x) wbuf[p] = __ldcg(gw + p);
+    }
+    if (sgd) {
+      if (s0 + (int)threadIdx.x < s1) vsub[threadIdx.x] = vs;
+      for (int e = s0 + blockDim.x + threadIdx.x; e < s1; e += blockDim.x) vsub[e - s0] = e < P ? __ldcg(gv + e) : 0.f;
+    }
   }
 
   // Push this rank's sum of element e into row `rank` of every rank's receive
@@ -637,6 +663,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   constexpr int SPW = RL::SPW;
   cg::cluster_group cluster = cg::this_cluster();
   const int G = gridDim.x;
+  const unsigned long long t_entry = a.probe ? globaltimer() : 0ull;
 
   extern __shared__ __align__(16) float smem[];
   const int NW = blockDim.x >> 5;
@@ -835,6 +862,10 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   }
 
   rs.publish(a, gw, gv, wa, round0);
+  if (a.probe && threadIdx.x == 0 && a.rounds > 0) {  // kernel entry / exit (launch anatomy)
+    a.probe[(long long)blockIdx.x * 16 + 14] = t_entry;
+    a.probe[((long long)(a.rounds - 1) * G + blockIdx.x) * 16 + 15] = globaltimer();
+  }
   cluster.sync();  // no CTA leaves while a peer may still address its shared memory
 }
 

@@ -197,17 +197,16 @@ ghc_status worker_step(ghc_session* s, int k, const float* w, int32_t& n_out) {
 }
 
 ghc_status apply_master(ghc_session* s, ghc_master* m, const float* g, float lr, float mu) {
-  ghc_ctx* c = s->plan->ctx;
-  float* w = m->w[0];
-  float* v = m->v[0];
-  MasterDev* ms = s->ms;
-  int vec = 1;
-  long long PP = s->P;
-  int* st = &m->ms->status;
-  unsigned long long* ver = &m->ms->version;
-  unsigned long long* rj = &m->ms->rejected;
-  void* args[] = {&w, &v, &g, &PP, &vec, &lr, &mu, &ms, &st, &ver, &rj};
-  return coop(c, reinterpret_cast<const void*>(sgd_apply_kernel), args);
+  (void)s;
+  // one pass over the master's double buffers (sgd_db det mode, ghc.cu)
+  return master_apply_det(m, g, lr, mu);
+}
+
+// The master's current weights (the double buffer flips on every apply).
+float* master_w(ghc_master* m) {
+  int cur = 0;
+  ghc_master_current(m, &cur);  // known on the host: never a device read here
+  return m->w[cur];
 }
 
 // VALIDATE_RESULT of the current master weights (EASGD: the center), appended
@@ -349,7 +348,7 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
       replay_post_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, s->d_samples, n);
       c->launches += 2;
       CU(cudaGetLastError());
-      CU(cudaMemcpyAsync(wk, s->master->w[0], sizeof(float) * P, cudaMemcpyDeviceToDevice,
+      CU(cudaMemcpyAsync(wk, master_w(s->master), sizeof(float) * P, cudaMemcpyDeviceToDevice,
                          c->stream));
       if (s->v_every > 0) {  // the cadence needs the accepted count (serial)
         uint64_t ver = 0;
@@ -497,10 +496,9 @@ ghc_status run_hier(ghc_session* s, float* h_loss) {
     }
     if (nfl > 0) {
       if (ghc_status st = ghc_weighted_mean(c, s->comb, s->pseudo, wts.data(), nfl, P)) return st;
-      float* tw = nullptr;
-      if (ghc_status st = ghc_master_weights(s->master, &tw, nullptr)) return st;
       if (ghc_status st = apply_master(s, s->master, s->comb, s->cfg.parent_lr, s->cfg.parent_mu))
         return st;
+      float* tw = master_w(s->master);  // the top master's new (or, rejected, unchanged) weights
       int tstat = 0;  // the top master's samples count only an accepted update
       CU(cudaMemcpyAsync(&tstat, &s->master->ms->status, sizeof(int), cudaMemcpyDeviceToHost,
                          c->stream));

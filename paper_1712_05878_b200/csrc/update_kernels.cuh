@@ -113,11 +113,16 @@ static __global__ void __launch_bounds__(256) sgd_apply_kernel(float* __restrict
 // 49-51 — the current buffer was never written).  No grid barrier, no
 // separate finite-check pass.  `flags` holds the cross-CTA bad flag and the
 // arrival counter.
+//
+// det = 1 (the master paths that track the buffer index on the host): the
+// buffers flip on EVERY call; a rejected update leaves flags->flag[1] = 1
+// and db_fixup_kernel (launched right after) copies the old w, v into the new
+// buffers — the rare path pays the copy, the common path stays one pass.
 static __global__ void __launch_bounds__(256) sgd_db_kernel(float* const* __restrict__ wb,
                                                      float* const* __restrict__ vb,
                                                      const float* __restrict__ g, long long P,
                                                      int vec, float lr, float mu, MasterDev* ms,
-                                                     MasterDev* flags) {
+                                                     MasterDev* flags, int det = 0) {
   const int cur = __ldcg(&ms->cur);
   const float* w = wb[cur];
   const float* v = vb[cur];
@@ -161,15 +166,36 @@ static __global__ void __launch_bounds__(256) sgd_db_kernel(float* const* __rest
       if (rej) {
         ms->rejected += 1ull;
         ms->status = 2;  // GHC_ERR_NONFINITE
+        if (det) ms->cur = cur ^ 1;
       } else {
         ms->cur = cur ^ 1;
         ms->version += 1ull;
         ms->status = 0;
       }
+      flags->flag[1] = det && rej;
       flags->flag[0] = 0;
       flags->arrive = 0;
       __threadfence();
     }
+  }
+}
+
+// After a rejected det-mode sgd_db: the new current buffers get the old
+// state (the update is rejected whole, optim.cpp:49-51).  Every CTA reads the
+// same stream-ordered flag; the common (accepted) case returns at once.
+static __global__ void __launch_bounds__(256) db_fixup_kernel(float* const* __restrict__ wb,
+                                                       float* const* __restrict__ vb, long long P,
+                                                       const MasterDev* ms, const MasterDev* flags) {
+  if (!__ldcg(&flags->flag[1])) return;
+  const int cur = __ldcg(&ms->cur);
+  const float* w = wb[cur ^ 1];
+  const float* v = vb[cur ^ 1];
+  float* w2 = wb[cur];
+  float* v2 = vb[cur];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x) {
+    w2[i] = w[i];
+    v2[i] = v[i];
   }
 }
 

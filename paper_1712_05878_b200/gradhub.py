@@ -66,6 +66,14 @@ class Context:
     def sync(self):
         check(self.lib.ghc_ctx_sync(self.h), "ghc_ctx_sync")
 
+    def hold(self):
+        """ghc_stream_hold: queue work behind a gate (device timing without
+        the host's launch calls); release() lets it run."""
+        check(self.lib.ghc_stream_hold(self.h))
+
+    def release(self):
+        check(self.lib.ghc_stream_release(self.h))
+
     def timer_start(self):
         check(self.lib.ghc_timer_start(self.h))
 
