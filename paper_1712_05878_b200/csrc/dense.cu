@@ -208,6 +208,14 @@ ghc_status ghc_gemm_nt(ghc_ctx* c, const float* d_a, const float* d_b, float* d_
 
 ghc_status ghc_transpose(ghc_ctx* c, float* d_out, const float* d_in, int32_t rows, int32_t cols,
                          int32_t ldin, int32_t ldout) {
+  if (ldin % 4 == 0 && ldout % 4 == 0 && aligned16(d_in) && aligned16(d_out) &&
+      static_cast<long long>(rows) * cols >= (1 << 16)) {
+    dim3 g4((cols + 63) / 64, (rows + 63) / 64);
+    transpose4_kernel<<<g4, 256, 0, c->stream>>>(d_out, d_in, rows, cols, ldin, ldout);
+    CU(cudaGetLastError());
+    c->launches++;
+    return GHC_OK;
+  }
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
   transpose_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(d_out, d_in, rows, cols, ldin, ldout);
   CU(cudaGetLastError());

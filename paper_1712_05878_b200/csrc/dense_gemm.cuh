@@ -558,4 +558,46 @@ static __global__ void transpose_kernel(float* __restrict__ out, const float* __
   }
 }
 
+// Vectorised out-of-place transpose (64×64 tiles, float4 loads and stores):
+// the per-round Wᵀ of the 4096-wide layer; needs 16-B aligned rows.
+static __global__ void __launch_bounds__(256) transpose4_kernel(float* __restrict__ out,
+                                                                const float* __restrict__ in, int rows,
+                                                                int cols, int ldin, int ldout) {
+  __shared__ float t[64][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  for (int i = ty; i < 64; i += 16) {
+    const int r = r0 + i, c = c0 + 4 * tx;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < rows) {
+      const float* p = in + (long long)r * ldin + c;
+      if (c + 3 < cols) {
+        v = __ldg(reinterpret_cast<const float4*>(p));
+      } else {
+        if (c < cols) v.x = p[0];
+        if (c + 1 < cols) v.y = p[1];
+        if (c + 2 < cols) v.z = p[2];
+      }
+    }
+    t[i][4 * tx] = v.x;
+    t[i][4 * tx + 1] = v.y;
+    t[i][4 * tx + 2] = v.z;
+    t[i][4 * tx + 3] = v.w;
+  }
+  __syncthreads();
+  for (int i = ty; i < 64; i += 16) {
+    const int c = c0 + i, r = r0 + 4 * tx;
+    if (c >= cols) continue;
+    const float4 v = make_float4(t[4 * tx][i], t[4 * tx + 1][i], t[4 * tx + 2][i], t[4 * tx + 3][i]);
+    float* p = out + (long long)c * ldout + r;
+    if (r + 3 < rows) {
+      *reinterpret_cast<float4*>(p) = v;
+    } else {
+      if (r < rows) p[0] = v.x;
+      if (r + 1 < rows) p[1] = v.y;
+      if (r + 2 < rows) p[2] = v.z;
+    }
+  }
+}
+
 }  // namespace ghc

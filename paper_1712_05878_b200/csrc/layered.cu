@@ -68,7 +68,7 @@ __global__ void head_kernel(const float* __restrict__ A, int in, const float* __
   for (int k = 0; k < KMAX; ++k) {
     e[k] = k < K ? expf(z[k] - zmax) : 0.f;
     den += e[k];
-    if (k == label) zy = z[k];
+    zy = k == label ? z[k] : zy;
   }
   const float inv = 1.0f / den;
   float dz[KMAX];
@@ -92,6 +92,141 @@ __global__ void head_kernel(const float* __restrict__ A, int in, const float* __
       if (dact >= 0) d *= gemm_detail::dact_from_y(a[i], dact);
       dA[(long long)warp * in + i] = d;
     }
+  }
+}
+
+// The same head with one 256-thread block per sample and float4 rows (the
+// wide variant's 4096-wide layer: a warp per sample left the row loop
+// latency-bound at ~10 % of HBM).  Fixed reduction order: per-thread partial
+// over its float4 chunks, butterfly within the warp, then the warps in order
+// (every thread forms the same sums from shared memory).
+template <int KMAX>
+__global__ void __launch_bounds__(256) head_block_kernel(
+    const float* __restrict__ A, int in, const float* __restrict__ Ws, const float* __restrict__ bs, int K,
+    const int32_t* __restrict__ y, int n, float scale, float* __restrict__ dlogits, float* __restrict__ loss_vec,
+    float* __restrict__ dA, int dact, float* __restrict__ probs, int* err) {
+  __shared__ float red[KMAX][8];
+  const int s = blockIdx.x;
+  if (s >= n) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int in4 = in >> 2;
+  const float4* a4 = reinterpret_cast<const float4*>(A + (long long)s * in);
+  float z[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) z[k] = 0.f;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < in4; i += blockDim.x) {
+    const float4 av = a4[i];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(Ws + (long long)k * in) + i);
+        z[k] = fmaf(w.x, av.x, z[k]);
+        z[k] = fmaf(w.y, av.y, z[k]);
+        z[k] = fmaf(w.z, av.z, z[k]);
+        z[k] = fmaf(w.w, av.w, z[k]);
+      }
+  }
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const float v = warp_sum(z[k]);
+    if (lane == 0 && k < K) red[k][warp] = v;
+  }
+  __syncthreads();
+  float zmax = -3.0e38f;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k < K) {
+      float t = 0.f;
+      for (int w = 0; w < nw; ++w) t += red[k][w];
+      z[k] = t + bs[k];
+      zmax = fmaxf(zmax, z[k]);
+    }
+  }
+  int label = y[s];
+  if (label < 0 || label >= K) {
+    if (threadIdx.x == 0) atomicOr(err, 1);
+    label = 0;
+  }
+  float den = 0.f, zy = 0.f, e[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    e[k] = k < K ? expf(z[k] - zmax) : 0.f;
+    den += e[k];
+    zy = k == label ? z[k] : zy;
+  }
+  const float inv = 1.0f / den;
+  float dz[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) dz[k] = k < K ? (e[k] * inv - (k == label ? 1.f : 0.f)) * scale : 0.f;
+  if (threadIdx.x == 0) {
+    loss_vec[s] = logf(den) - (zy - zmax);
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) {
+        if (dlogits) dlogits[(long long)s * K + k] = dz[k];
+        if (probs) probs[(long long)s * K + k] = e[k] * inv;
+      }
+  }
+  if (dA) {
+    float4* d4 = reinterpret_cast<float4*>(dA + (long long)s * in);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < in4; i += blockDim.x) {
+      float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          const float4 w = __ldg(reinterpret_cast<const float4*>(Ws + (long long)k * in) + i);
+          d.x = fmaf(w.x, dz[k], d.x);
+          d.y = fmaf(w.y, dz[k], d.y);
+          d.z = fmaf(w.z, dz[k], d.z);
+          d.w = fmaf(w.w, dz[k], d.w);
+        }
+      if (dact >= 0) {
+        const float4 av = a4[i];
+        d.x *= gemm_detail::dact_from_y(av.x, dact);
+        d.y *= gemm_detail::dact_from_y(av.y, dact);
+        d.z *= gemm_detail::dact_from_y(av.z, dact);
+        d.w *= gemm_detail::dact_from_y(av.w, dact);
+      }
+      d4[i] = d;
+    }
+  }
+}
+
+// Stage 1 of the column reduction for wide rows (cols % 4 == 0, 16-B rows):
+// thread = 4 columns × one 16-row chunk, all 16 float4 loads in flight
+// (16 MB of the 4096-wide layer ≈ all in flight at once); partials
+// [chunk][k][cols] in fixed row order, stage 2 = colsum_final_kernel.
+__global__ void __launch_bounds__(256) colsum4_partial_kernel(float* __restrict__ part,
+                                                              const float* __restrict__ X, int ldx,
+                                                              const float* __restrict__ coef, int kc,
+                                                              int n, int cols) {
+  constexpr int R = 16;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;  // column quad
+  const int ch = blockIdx.y;
+  const int k0 = 4 * blockIdx.z;
+  if (4 * q >= cols) return;
+  const int s0 = ch * R;
+  const int nk = coef ? min(4, kc - k0) : 1;
+  float4 v[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    v[i] = s0 + i < n ? __ldg(reinterpret_cast<const float4*>(X + (long long)(s0 + i) * ldx) + q)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k >= nk) break;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float cf = coef ? (s0 + i < n ? __ldg(coef + (long long)(s0 + i) * kc + k0 + k) : 0.f) : 1.f;
+      acc.x = fmaf(cf, v[i].x, acc.x);
+      acc.y = fmaf(cf, v[i].y, acc.y);
+      acc.z = fmaf(cf, v[i].z, acc.z);
+      acc.w = fmaf(cf, v[i].w, acc.w);
+    }
+    reinterpret_cast<float4*>(part + ((long long)ch * kc + k0 + k) * cols)[q] = acc;
   }
 }
 
@@ -129,8 +264,33 @@ __global__ void colsum_final_kernel(float* __restrict__ out, int ldo, const floa
   const int k = blockIdx.y;
   if (c >= cols) return;
   float t = 0.f;
+#pragma unroll 8
   for (int ch = 0; ch < nchunks; ++ch) t += part[((long long)ch * kc + k) * cols + c];
   out[(long long)k * ldo + c] = t;
+}
+
+// Stage 2 for many chunks: block = 32 columns × 8 chunk groups; chunks ty,
+// ty+8, … in order, then the 8 groups in order (deterministic).
+__global__ void __launch_bounds__(256) colsum_final2_kernel(float* __restrict__ out, int ldo,
+                                                            const float* __restrict__ part, int kc,
+                                                            int cols, int nchunks) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  const int k = blockIdx.y;
+  float t = 0.f;
+  if (c < cols) {
+#pragma unroll 8
+    for (int ch = ty; ch < nchunks; ch += 8) t += part[((long long)ch * kc + k) * cols + c];
+  }
+  red[ty][tx] = t;
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float o = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) o += red[r][tx];
+    out[(long long)k * ldo + c] = o;
+  }
 }
 
 __global__ void sum_kernel(float* out, const float* v, int n) {
@@ -174,6 +334,18 @@ namespace {
 
 ghc_status colsum(ghc_ctx* c, LayeredWorkspace& ws, float* out, int ldo, const float* X, int ldx,
                   const float* coef, int kc, int n, int cols) {
+  if (cols >= 256 && cols % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15u) == 0) {
+    const int kcc = coef ? kc : 1;
+    const int nch = (n + 15) / 16;
+    if (ghc_status s = ws.part.ensure(static_cast<size_t>(nch) * kcc * cols)) return s;
+    colsum4_partial_kernel<<<dim3((cols / 4 + 255) / 256, nch, (kcc + 3) / 4), 256, 0, c->stream>>>(
+        ws.part.p, X, ldx, coef, kcc, n, cols);
+    colsum_final2_kernel<<<dim3((cols + 31) / 32, kcc), 256, 0, c->stream>>>(out, ldo, ws.part.p, kcc,
+                                                                             cols, nch);
+    c->launches += 2;
+    CU(cudaGetLastError());
+    return GHC_OK;
+  }
   const int nch = n < 32 ? n : 32;
   const int chunk = (n + nch - 1) / nch;
   if (ghc_status s = ws.part.ensure(static_cast<size_t>(nch) * kc * cols)) return s;
@@ -288,7 +460,18 @@ ghc_status layered_step(ghc_plan* p, const float* w, const float* x, const int32
   {
     const int warps_per_block = 8;
     const dim3 grid((n + warps_per_block - 1) / warps_per_block);
-    if (K <= 4)
+    const bool vec = (a_w % 4) == 0 && a_w >= 512 && (reinterpret_cast<uintptr_t>(a) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(Ws) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(ws.dz[0].p) & 15u) == 0;
+    if (vec && K <= 4)
+      head_block_kernel<4><<<n, 256, 0, c->stream>>>(
+          a, a_w, Ws, bs, K, Y, n, scale, ws.logits.p, ws.loss.p, need_dA ? ws.dz[0].p : nullptr,
+          dact, probs, p->err);
+    else if (vec)
+      head_block_kernel<32><<<n, 256, 0, c->stream>>>(
+          a, a_w, Ws, bs, K, Y, n, scale, ws.logits.p, ws.loss.p, need_dA ? ws.dz[0].p : nullptr,
+          dact, probs, p->err);
+    else if (K <= 4)
       head_kernel<4><<<grid, 32 * warps_per_block, 0, c->stream>>>(
           a, a_w, Ws, bs, K, Y, n, scale, ws.logits.p, ws.loss.p, need_dA ? ws.dz[0].p : nullptr,
           dact, probs, p->err);
