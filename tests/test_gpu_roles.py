@@ -198,3 +198,40 @@ def test_end_to_end_learning_ac10(ctx, delta, lo, hi):
     loss, _ = s.run(order)
     (ver, acc, vloss), = s.validations()
     assert ver == len(order) and lo <= acc <= hi, (acc, vloss)
+
+
+def test_async_downpour_c4_b1000(ctx, oracle):
+    """c4 at the benchmark batch: 8 workers × B = 1000, 64 replayed arrivals."""
+    W, B = 8, 1000
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    s = g.Session(arch, g.train_config(n_workers=W, batch_size=B, epochs=1, mode=g.REPLAY),
+                  g.data_spec(16, 4000))
+    order = np.repeat(np.arange(W, dtype=np.int32), 8)  # 8 batches per worker
+    np.random.default_rng(7).shuffle(order)
+    loss, stale = s.run(order)
+    out = s.read()
+    spec, x, y = oracle_data(oracle, 16, 4000)
+    r = oracle.run_replay(oracle.parse_arch(BENCH_ARCH), spec, x, y,
+                          oracle.train_cfg(n_workers=W, batch_size=B, epochs=1), order)
+    assert np.array_equal(stale, r.extra["staleness"])
+    assert out["version"] == r.stats.updates == len(order) and out["samples"] == r.stats.samples
+    close(out["w"], r.w)
+
+
+def test_easgd_c3_b1000(ctx, oracle):
+    """c3 at the benchmark batch: 8 workers, α = 0.5, τ = 10, B = 1000, 2 epochs."""
+    W, B = 8, 1000
+    kw = dict(algo=g.EASGD, n_workers=W, batch_size=B, epochs=2, alpha=0.5, tau=10, lr=0.05)
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    s = g.Session(arch, g.train_config(mode=g.SYNC, **kw), g.data_spec(16, 4000))
+    s.run(None)
+    out = s.read()
+    order = np.tile(np.arange(W, dtype=np.int32), 2 * 8)
+    spec, x, y = oracle_data(oracle, 16, 4000)
+    r = oracle.run_replay(oracle.parse_arch(BENCH_ARCH), spec, x, y,
+                          oracle.train_cfg(algo=oracle.EASGD, n_workers=W, batch_size=B, epochs=2,
+                                           alpha=0.5, tau=10, lr=0.05), order)
+    assert out["version"] == r.stats.updates
+    close(out["w"], r.w)
+    for k in range(W):
+        close(out["worker_w"][k], r.extra["worker_w"][k])
