@@ -269,6 +269,37 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
  * ghc_master_read).  No host synchronisation. */
 ghc_status ghc_master_apply(ghc_master* m, const float* d_g);
 
+/* Resident round service: the persistent sync-round kernel launched ONCE
+ * for master m (fused SIMT cluster kernel, n samples per round, n within one
+ * sample per warp slot) and fed commands — a segment of `rounds` sync rounds
+ * on batches x/y (idx/stride as ghc_master_sync_rounds), losses to loss_out
+ * — through doorbells instead of a cooperative cluster launch per call
+ * (≈ 13 µs of device-side launch + prologue + teardown, measured).
+ *   ghc_resident_submit        host path: pinned ring + doorbell (returns seq);
+ *   ghc_resident_wait          spins on the pinned completion word;
+ *   ghc_resident_submit_stream stream path: a submit + a wait kernel on ctx's
+ *                              stream (CUDA events around them time the rounds);
+ *   ghc_resident_check         reads the service's error flags (synchronising);
+ *   ghc_resident_stop          STOP, kernel exit, master state published; frees r.
+ * With no command for idle_seconds (default 2) the kernel stops itself and
+ * later calls report GHC_ERR_CUDA.  The master must not be used by other
+ * calls while the service runs.  One submission path at a time. */
+typedef struct ghc_resident ghc_resident;
+ghc_status ghc_resident_start(ghc_master* m, int64_t n, double idle_seconds, ghc_resident** out);
+ghc_status ghc_resident_submit(ghc_resident* r, const float* x, const int32_t* y, const int32_t* idx,
+                               int64_t stride, int32_t rounds, float* loss_out, uint64_t* seq);
+ghc_status ghc_resident_wait(ghc_resident* r, uint64_t seq);
+ghc_status ghc_resident_submit_stream(ghc_resident* r, ghc_ctx* ctx, const float* x, const int32_t* y,
+                                      const int32_t* idx, int64_t stride, int32_t rounds, float* loss_out,
+                                      uint64_t* seq);
+ghc_status ghc_resident_check(ghc_resident* r);
+/* Diagnostics of the last stream-submitted command (%globaltimer ns):
+ * submit, first / last CTA past the doorbell, completion published, wait
+ * kernel saw it.  Synchronising. */
+ghc_status ghc_resident_times(ghc_resident* r, uint64_t* t5);
+ghc_status ghc_resident_stop(ghc_resident* r);
+
+
 /* ------------------------------------------------------------------ */
 /* Exchange across GPUs (one process per GPU) over NCCL / NVLink 5:     */
 /* replaces Endpoint send/recv (transport.hpp:22-44) + establish()      */

@@ -117,6 +117,13 @@ SIGNATURES = [
     ("ghc_master_read", C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     ("ghc_master_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp]),
     ("ghc_master_apply", C.c_int, [_vp, _vp]),
+    ("ghc_resident_start", C.c_int, [_vp, _i64, C.c_double, _vp]),
+    ("ghc_resident_submit", C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    ("ghc_resident_wait", C.c_int, [_vp, _u64]),
+    ("ghc_resident_submit_stream", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    ("ghc_resident_check", C.c_int, [_vp]),
+    ("ghc_resident_times", C.c_int, [_vp, _vp]),
+    ("ghc_resident_stop", C.c_int, [_vp]),
     ("ghc_comm_unique_id", C.c_int, [_vp]),
     ("ghc_comm_init", C.c_int, [_vp, _vp, _i32, _i32, _vp]),
     ("ghc_comm_split", C.c_int, [_vp, _i32, _i32, _vp]),

@@ -193,6 +193,14 @@ static __global__ void stream_gate_kernel(const volatile int* flag) {
     __nanosleep(200);
   }
 }
+// Load the gate kernel's module now (CUDA lazy loading would otherwise
+// load it at first launch, which waits for running kernels — a resident
+// round kernel never finishes on its own).
+ghc_status ghc_preload_gate() {
+  cudaFuncAttributes fa;
+  CU(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(stream_gate_kernel)));
+  return GHC_OK;
+}
 ghc_status ghc_stream_hold(ghc_ctx* c) {
   if (!c->gate_h) {
     CU(cudaHostAlloc(reinterpret_cast<void**>(&c->gate_h), sizeof(int), cudaHostAllocMapped));

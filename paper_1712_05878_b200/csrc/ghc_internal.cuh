@@ -125,6 +125,8 @@ struct ghc_master {
 
 // Current buffer index of the master (cached; one D2H read when unknown).
 extern "C" ghc_status ghc_master_current(ghc_master* m, int* cur);
+// Force-load the stream gate kernel (before a resident kernel starts).
+extern "C" ghc_status ghc_preload_gate();
 // sgd_step on the master's double buffers in ONE pass (sgd_db_kernel, det
 // mode + db_fixup_kernel): the buffers flip on every call, so the host keeps
 // knowing the current index; lr / mu as given (the top master of a
@@ -147,8 +149,11 @@ inline void step_geometry(const ghc_plan* p, int64_t n, int& ctas, int& warps) {
 
 // vr > 1: vr virtual ranks share the grid (cross-rank exchange, SIMT kernel),
 // each with max_clusters / vr clusters and n_max samples per round.
-inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 1) {
+inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 1,
+                              cudaStream_t stream = nullptr) {
   if (!p->lstm) return fail(GHC_ERR_CONFIG, "plan has no fused worker kernel");
+  if (a.res && !(p->use_cluster && p->max_clusters > 0 && !p->use_tc))
+    return fail(GHC_ERR_CONFIG, "resident rounds need the SIMT cluster round kernel");
   a.err = p->err;
   a.probe = p->probe;
   a.bar = p->bar;
@@ -181,12 +186,14 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 
     a.tw = p->tw;
     a.pstride = p->lstm->ep[p->cs_index];
     a.pipelined = n_max <= nc * cs * per_cta;
+    if (a.res && !a.pipelined)
+      return fail(GHC_ERR_CONFIG, "resident rounds: the batch must fit one sample per warp slot");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(nc * cs * vr));
     cfg.blockDim = dim3(static_cast<unsigned>(warps * 32));
     cfg.dynamicSmemBytes = tc ? p->lstm->smem_tc[p->cs_index](warps)
                               : p->lstm->smem_round[p->cs_index](warps);
-    cfg.stream = p->ctx->stream;
+    cfg.stream = stream ? stream : p->ctx->stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cs;

@@ -213,13 +213,16 @@ struct ClusterRS {
 
   // wparts: nw warp partials [nw][pstride] (P gradient entries + loss slot);
   // their sum (warp order) is the CTA partial, formed while pushing.
-  __device__ void exchange(const StepArgs& a, int r, const float* wparts, int nw, int pstride,
-                           float*& wa, float*& wb, unsigned long long* pr, int ntot) {
+  // r: round index within the segment (loss slot); rb: rounds run by this
+  // launch so far (mbarrier phases — a resident launch serves many segments).
+  __device__ void exchange(const StepArgs& a, int r, unsigned long long rb, float* loss_out,
+                           const float* wparts, int nw, int pstride, float*& wa, float*& wb,
+                           unsigned long long* pr, int ntot) {
     ++epoch;
     ++xepoch;
     const int par = epoch & 1;                 // L2 rows: epoch parity (survives launches)
-    const int mb = r & 1;                      // mbarriers: re-initialised per launch
-    const unsigned ph = (unsigned)(r >> 1) & 1;
+    const int mb = (int)(rb & 1);              // mbarriers: re-initialised per launch
+    const unsigned ph = (unsigned)(rb >> 1) & 1;
     const unsigned tag = epoch << 1;
     if (threadIdx.x == 0) {  // arm: bytes the peers will push this round
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(mbp + mb)),
@@ -285,7 +288,7 @@ struct ClusterRS {
       }
       if (GX > 1) t = cross_rank_sum(a, xepoch & 1, e, t, xepoch);
       if (e == P) {
-        if (a.loss_out) a.loss_out[r] = t;
+        if (loss_out) loss_out[r] = t;
       } else if (a.mode == MODE_GRAD) {
         a.g_out[e] = t;
       } else if (sgd) {
@@ -362,7 +365,7 @@ struct ClusterRS {
   }
 
   __device__ void publish(const StepArgs& a, float* gw, float* gv, const float* wa,
-                          unsigned long long round0) {
+                          unsigned long long round0, unsigned long long rounds) {
     if (sgd) {
       if (cid == 0)
         for (int e = threadIdx.x; e < P; e += blockDim.x) gw[e] = wa[e];
@@ -376,7 +379,7 @@ struct ClusterRS {
         a.ms->version += accepted;
         a.ms->rejected += rejected;
         a.ms->samples += acc_samples;
-        a.ms->round = round0 + (unsigned long long)a.rounds;
+        a.ms->round = round0 + rounds;
         a.ms->status = last_status;
       }
     }
@@ -717,30 +720,55 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     s1 = min(n, s0 + spc);
     s = s0 + warp;
   };
-  const int32_t* idxv = a.idx ? a.idx + (long long)rs.vrank * a.idx_vstride : nullptr;
+  // One segment of rounds per launch — or, resident (a.res), one segment per
+  // command of the ResidentCtl queue: the data pointers, round count and
+  // loss slots come from the command; weights, velocity, epochs and the
+  // mbarrier phases carry over.
+  const float* sx = a.x;
+  const int32_t* sy = a.y;
+  const int32_t* sidx = a.idx;
+  long long sstride = a.stride;
+  int srounds = a.rounds;
+  float* sloss = a.loss_out;
+  unsigned long long rg = 0;   // rounds run by this launch
+  unsigned long long seq = 0;  // resident: command sequence number
+  const int32_t* idxv = nullptr;
   auto slot_x = [&](int sp, int b) { return ws + sp * N::WARP_FLOATS + N::S_X + b * N::XWP; };
   auto slot_l = [&](int sp) { return reinterpret_cast<int*>(ws + sp * N::WARP_FLOATS + N::S_L); };
   auto fetch_nocommit = [&](int sp, int row, int b) {
-    const float* xrow = a.x + (long long)row * N::XW;
+    const float* xrow = sx + (long long)row * N::XW;
     float* dst = slot_x(sp, b);
     for (int i = lane; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);
-    if (lane == 0) cp_async4(slot_l(sp) + b, a.y + row);
+    if (lane == 0) cp_async4(slot_l(sp) + b, sy + row);
   };
   auto row_of = [&](int r, int s) {
     // no gather table: round r reads rows r*stride + s (stride 0: rows s)
-    return idxv ? __ldg(idxv + (long long)r * a.stride + s) : (int)((long long)r * a.stride + s);
+    return idxv ? __ldg(idxv + (long long)r * sstride + s) : (int)((long long)r * sstride + s);
   };
   // gather indices of round r (pipelined path): one cp.async per slot into
   // slot_l[2], fetched a round before the rows they select
   auto fetch_idx_nocommit = [&](int r) {
-    if (!idxv || lane != 0 || r >= a.rounds) return;
-    int sx, sx1;
-    first_sample(r, sx, sx1);
+    if (!idxv || lane != 0 || r >= srounds) return;
+    int sx0, sx1;
+    first_sample(r, sx0, sx1);
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp)
-      if (sx + sp * NW < sx1) cp_async4(slot_l(sp) + 2, idxv + (long long)r * a.stride + sx + sp * NW);
+      if (sx0 + sp * NW < sx1) cp_async4(slot_l(sp) + 2, idxv + (long long)r * sstride + sx0 + sp * NW);
   };
-  if (a.pipelined) {
+
+  for (;;) {  // segments
+  if (a.res) {
+    ResidentCmd cmd;
+    if (!resident_next(a.res, ++seq, cmd)) break;
+    sx = cmd.x;
+    sy = cmd.y;
+    sidx = cmd.idx;
+    sstride = cmd.stride;
+    srounds = cmd.rounds;
+    sloss = cmd.loss_out;
+  }
+  idxv = sidx ? sidx + (long long)rs.vrank * a.idx_vstride : nullptr;
+  if (a.pipelined && srounds > 0) {
     int s, s1;
     first_sample(0, s, s1);
 #pragma unroll
@@ -751,7 +779,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   }
   __syncthreads();
 
-  for (int r = 0; r < a.rounds; ++r) {
+  for (int r = 0; r < srounds; ++r, ++rg) {
     int ntot = GX * a.n;  // samples of round r over all ranks (SPEC.md:358-366 weighted mean)
     if (!fixed_n) {
       ntot = 0;
@@ -783,13 +811,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       // r-1 used) and round r+2's indices, then compute round r.
       cp_async_wait<0>();
       __syncwarp();
-      if (r + 1 < a.rounds) {
+      if (r + 1 < srounds) {
         int sn, sn1;
         first_sample(r + 1, sn, sn1);
         int rows[SPW];
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
-          rows[sp] = idxv ? slot_l(sp)[2] : (int)((long long)(r + 1) * a.stride + sn + sp * NW);
+          rows[sp] = idxv ? slot_l(sp)[2] : (int)((long long)(r + 1) * sstride + sn + sp * NW);
         __syncwarp();
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
@@ -835,8 +863,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       for (; s < s1; s += NW) {
         const int row = row_of(r, s);
         float* xs = slot_x(0, 0);
-        for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(a.x + (long long)row * N::XW + i);
-        int label = __ldg(a.y + row);
+        for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(sx + (long long)row * N::XW + i);
+        int label = __ldg(sy + row);
         __syncwarp();
         if (label < 0 || label >= K) {
           if (lane == 0) atomicOr(a.err, 1);
@@ -858,11 +886,14 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
 
     // (the CTA partial — Σ warp partials, warp order — is formed by ClusterRS (a))
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
-    rs.exchange(a, r, wpart, NW, N::PPAD, wa, wb, pr, ntot);
+    rs.exchange(a, r, rg, sloss, wpart, NW, N::PPAD, wa, wb, pr, ntot);
   }
+  if (!a.res) break;
+  resident_done(a.res, seq);
+  }  // segments
 
-  rs.publish(a, gw, gv, wa, round0);
-  if (a.probe && threadIdx.x == 0 && a.rounds > 0) {  // kernel entry / exit (launch anatomy)
+  rs.publish(a, gw, gv, wa, round0, rg);
+  if (a.probe && !a.res && threadIdx.x == 0 && a.rounds > 0) {  // kernel entry / exit (launch anatomy)
     a.probe[(long long)blockIdx.x * 16 + 14] = t_entry;
     a.probe[((long long)(a.rounds - 1) * G + blockIdx.x) * 16 + 15] = globaltimer();
   }

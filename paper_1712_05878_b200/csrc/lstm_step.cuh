@@ -37,6 +37,132 @@ enum StepMode : int {
 
 constexpr int kMaxRanks = 8;  // GPUs of one NVLink domain in the fused exchange
 
+// ---------------------------------------------------------------------------
+// Resident round service (resident.cu): the persistent round kernel stays
+// launched and serves a queue of commands — each one segment of sync rounds
+// on its own batch pointers — so a call costs a doorbell, not a cooperative
+// cluster launch (≈ 13 µs of launch + prologue + teardown, measured).
+//   host submit:   pinned ring slot + pinned doorbell; CTA 0 relays it into
+//                  the device ring and publishes the device bell;
+//   stream submit: a 1-thread kernel on the caller's stream writes the slot
+//                  and the bell; a 1-thread wait kernel on the same stream
+//                  spins until the command completed (CUDA events around
+//                  the pair time exactly the served rounds).
+// Completion: every CTA arrives on a counter after the segment's last round;
+// the last one publishes `done` (device) and the pinned host word.  With no
+// command for idle_ns the kernel publishes a STOP itself (never strands the
+// GPU) and marks the service expired.
+struct ResidentCmd {
+  const float* x;
+  const int32_t* y;
+  const int32_t* idx;
+  long long stride;
+  float* loss_out;
+  int rounds;
+  int op;  // 0 run, 1 stop
+  unsigned long long seq;
+};
+constexpr int kResRing = 8;
+struct ResidentCtl {
+  ResidentCmd cmd[kResRing];
+  unsigned long long claim;    // highest claimed command slot (submitter / relay / expiry)
+  unsigned long long bell;     // highest published command (device)
+  unsigned long long arrive;   // CTA completions, all commands
+  unsigned long long done;     // highest completed command (device)
+  int expired;                 // idle STOP published by the kernel itself
+  int submit_failed;           // a stream submit found the service expired
+  ResidentCmd* host_cmd;       // pinned ring (device-mapped pointer)
+  unsigned long long* host_bell;  // pinned doorbell
+  unsigned long long* host_done;  // pinned: [0] completed command, [1] expired
+  unsigned long long idle_ns;
+  unsigned long long t[8];     // diagnostics (%globaltimer): [0] submit, [1] first CTA past the
+                               // bell, [2] last CTA past the bell, [3] done published, [4] wait saw it
+};
+
+__device__ __forceinline__ unsigned long long res_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long res_ld_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long res_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Next command for this CTA (all threads return the same command; false on STOP).
+static __device__ __noinline__ bool resident_next(ResidentCtl* c, unsigned long long seq, ResidentCmd& out) {
+  __shared__ ResidentCmd s_cmd;
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = res_now();
+    if (blockIdx.x == 0) {  // relay of the host ring; idle expiry
+      for (;;) {
+        if (res_ld_acquire(&c->bell) >= seq) break;
+        // a slot is written only by whoever claims its sequence number, then
+        // published through the bell (release) — readers wait on the bell
+        const bool host_ready = res_ld_sys(c->host_bell) >= seq;
+        const bool idle = !host_ready && res_now() - t0 > c->idle_ns;
+        if ((host_ready || idle) && atomicCAS(&c->claim, seq - 1, seq) == seq - 1) {
+          ResidentCmd v{};
+          if (host_ready) {
+            const volatile ResidentCmd* h = c->host_cmd + (seq % kResRing);
+            v.x = h->x;
+            v.y = h->y;
+            v.idx = h->idx;
+            v.stride = h->stride;
+            v.loss_out = h->loss_out;
+            v.rounds = h->rounds;
+            v.op = h->op;
+            v.seq = h->seq;
+          } else {
+            v.op = 1;  // idle: STOP
+            v.seq = seq;
+            c->expired = 1;
+            volatile unsigned long long* hd = c->host_done;
+            hd[1] = 1ull;
+          }
+          c->cmd[seq % kResRing] = v;
+          __threadfence_system();
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&c->bell), "l"(seq) : "memory");
+          break;
+        }
+      }
+    } else {
+      for (unsigned it = 0; res_ld_acquire(&c->bell) < seq; ++it)  // one thread per CTA spins on L2
+        if ((it & 1023u) == 0 && res_now() - t0 > c->idle_ns + 10000000000ull) __trap();  // relay gone: never hang
+    }
+    s_cmd = c->cmd[seq % kResRing];
+    const unsigned long long tb = res_now();
+    atomicMin(&c->t[1], tb);
+    atomicMax(&c->t[2], tb);
+  }
+  __syncthreads();
+  out = s_cmd;
+  __syncthreads();
+  return out.op == 0;
+}
+
+// The segment of command `seq` is complete on this CTA (its last exchange
+// committed); the last CTA publishes the completion.
+static __device__ __noinline__ void resident_done(ResidentCtl* c, unsigned long long seq) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long prev = atomicAdd(&c->arrive, 1ull);
+    if (prev == seq * (unsigned long long)gridDim.x - 1ull) {
+      __threadfence_system();
+      c->t[3] = res_now();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&c->done), "l"(seq) : "memory");
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(c->host_done), "l"(seq) : "memory");
+    }
+  }
+}
+
 struct StepArgs {
   const float* x;         // dataset (or batch) rows, T*D floats each
   const int32_t* y;       // labels
@@ -77,6 +203,7 @@ struct StepArgs {
   unsigned long long* tpart;   // single-GPU exchange: tagged cluster rows [2][clusters][EP]
   unsigned long long* tw;      // single-GPU exchange: tagged new weights [2][EP]
   unsigned* gcnt[kMaxRanks];   // per rank: line [CS*kFlagStride] keeps the exchange epoch
+  ResidentCtl* res;            // non-null: resident round service (commands in res)
 };
 
 // Grid barrier for the persistent round loop (gather → broadcast):

@@ -405,6 +405,61 @@ class Master:
         return wp
 
 
+class Resident:
+    """ghc_resident: the persistent sync-round kernel launched once for
+    `master` (n samples per round) and fed commands through doorbells.
+    `submit` / `wait` use the pinned host ring (the per-call API: returns once
+    the command's rounds are committed and their losses are in loss_out);
+    `submit_stream` queues a submit + wait kernel pair on the context stream
+    (device-timed with the context's CUDA events).  `stop` publishes the
+    master state (required before reading the master)."""
+
+    def __init__(self, master: "Master", n: int, idle_seconds: float = 2.0):
+        self.master, self.ctx = master, master.ctx
+        h = C.c_void_p()
+        check(self.ctx.lib.ghc_resident_start(master.h, n, idle_seconds, C.byref(h)), "resident_start")
+        self.h = h
+
+    @staticmethod
+    def _args(x, y, idx, idx_offset, loss_out, loss_offset):
+        return (x.ptr, y.ptr, idx.offset(idx_offset) if idx is not None else None,
+                loss_out.offset(loss_offset) if loss_out is not None else None)
+
+    def submit(self, x, y, idx, stride: int, rounds: int, loss_out=None, idx_offset: int = 0,
+               loss_offset: int = 0) -> int:
+        px, py, pi, pl = self._args(x, y, idx, idx_offset, loss_out, loss_offset)
+        seq = C.c_uint64()
+        check(self.ctx.lib.ghc_resident_submit(self.h, px, py, pi, stride, rounds, pl, C.byref(seq)),
+              "resident_submit")
+        return seq.value
+
+    def wait(self, seq: int):
+        check(self.ctx.lib.ghc_resident_wait(self.h, seq), "resident_wait")
+
+    def submit_stream(self, x, y, idx, stride: int, rounds: int, loss_out=None, idx_offset: int = 0,
+                      loss_offset: int = 0) -> int:
+        px, py, pi, pl = self._args(x, y, idx, idx_offset, loss_out, loss_offset)
+        seq = C.c_uint64()
+        check(self.ctx.lib.ghc_resident_submit_stream(self.h, self.ctx.h, px, py, pi, stride, rounds,
+                                                      pl, C.byref(seq)), "resident_submit_stream")
+        return seq.value
+
+    def check(self):
+        check(self.ctx.lib.ghc_resident_check(self.h), "resident")
+
+    def stop(self):
+        if self.h is not None:
+            h, self.h = self.h, None
+            check(self.ctx.lib.ghc_resident_stop(h), "resident_stop")
+
+    def __del__(self):
+        try:
+            if self.h is not None and not _SHUTDOWN[0]:
+                self.stop()
+        except Exception:
+            pass
+
+
 def validate(w, arch: Architecture, x, y):
     """validate: (accuracy, mean loss, correct count) of
     weights w over a held-out set, one fused forward on the device."""

@@ -1,0 +1,63 @@
+"""Cost of a resident-service command vs rounds (stream and host doorbells)
+and, with the phase probe, where the time between the doorbell and the
+completion goes."""
+import json
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_1712_05878_b200 as g  # noqa: E402
+
+ARCH = "lstm(5,20,10),softmax(20,3)"
+B = 1000
+ctx = g.Context(0)
+arch = g.Architecture(ctx, ARCH)
+spec = g.data_spec(96, 9500)
+x, y = g.generate(spec)
+idx = np.random.default_rng(0).integers(0, len(y), size=3000 * B).astype(np.int32)
+dx, dy, di = ctx.upload(x), ctx.upload(y), ctx.upload(idx)
+out = {"stream_us": {}, "host_us": {}}
+m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+res = g.Resident(m, B, idle_seconds=30.0)
+res.submit_stream(dx, dy, di, B, 50)
+ctx.sync()
+for K in (1, 2, 5, 20, 200):
+    ts = []
+    for rep in range(5):
+        ctx.hold()
+        ctx.timer_start()
+        res.submit_stream(dx, dy, di, B, K)
+        ctx.release()
+        ts.append(ctx.timer_stop() * 1e3)
+    out["stream_us"][K] = float(np.median(ts))
+for K in (1, 2, 20):
+    ts = []
+    for rep in range(20):
+        t0 = time.perf_counter()
+        res.wait(res.submit(dx, dy, di, B, K))
+        ts.append((time.perf_counter() - t0) * 1e6)
+    out["host_us"][K] = float(np.median(ts))
+import ctypes as C  # noqa: E402
+tt = {}
+for K in (1, 20):
+    ctx.hold()
+    ctx.timer_start()
+    res.submit_stream(dx, dy, di, B, K)
+    ctx.release()
+    ev = ctx.timer_stop() * 1e3
+    t = (C.c_uint64 * 5)()
+    ctx.lib.ghc_resident_times(res.h, t)
+    t = [int(v) for v in t]
+    tt[K] = {"event_us": ev, "submit_to_first_cta_us": (t[1] - t[0]) / 1e3,
+             "bell_spread_us": (t[2] - t[1]) / 1e3, "rounds_to_done_us": (t[3] - t[2]) / 1e3,
+             "done_to_wait_seen_us": (t[4] - t[3]) / 1e3, "submit_to_wait_seen_us": (t[4] - t[0]) / 1e3}
+out["phases"] = tt
+# empty stream doorbell round trip without the round kernel doing rounds is
+# not expressible; fit a + b K instead
+Ks = np.array(list(out["stream_us"].keys()), float)
+b, a = np.polyfit(Ks, np.array(list(out["stream_us"].values())), 1)
+out["stream_fit"] = {"fixed_us": a, "round_us": b}
+res.stop()
+print(json.dumps(out, indent=1))
