@@ -149,6 +149,13 @@ def preroll(run_chunk, ctx, clk, min_s=0.25):
             break
 
 
+def under_profiler() -> bool:
+    """ncu/nsys inject through CUDA_INJECTION64_PATH and serialise kernels —
+    the resident round service (a kernel waiting on another kernel) cannot
+    run under them, so its measurements are skipped there."""
+    return bool(os.environ.get("CUDA_INJECTION64_PATH"))
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -231,7 +238,11 @@ def run_ours(args):
         idx = g.epoch_indices(spec, 1, 0, e, 99)
         stream.extend(idx[i:i + B] for i in range(0, per_epoch * B, B))
     idx = np.concatenate(stream[:total_rounds]).astype(np.int32)
-    dx, dy, di = ctx.upload(x), ctx.upload(y), ctx.upload(idx)
+    # packed rows (x | label | pad: 256-B rows = 2 whole 128-B lines per
+    # gathered sample, ghc_dataset_pack), the labels argument is then None
+    dx = g.pack_dataset(ctx, ctx.upload(x), ctx.upload(y))
+    dy = None
+    di = ctx.upload(idx)
     setup_s = time.time() - t0
 
     w0 = g.init_weights(arch, 7)
@@ -260,18 +271,20 @@ def run_ours(args):
         launches = ctx.launches - launches0
         # ---- the same K rounds through the resident round service
         # (ghc_resident_*: kernel launched once, one stream-doorbell command)
-        mr = g.Master(arch, w0, 0.01, 0.9)
-        res = g.Resident(mr, B, idle_seconds=30.0)
-        res.submit_stream(dx, dy, di, B, args.warmup)
-        ctx.sync()
-        ctx.hold()
-        ctx.timer_start()
-        res.submit_stream(dx, dy, di, B, args.steps, idx_offset=args.warmup * B)
-        ctx.release()
-        ms_res = ctx.timer_stop()
-        res.check()
-        res.stop()
-        del mr
+        ms_res = None
+        if not args.no_resident:
+            mr = g.Master(arch, w0, 0.01, 0.9)
+            res = g.Resident(mr, B, idle_seconds=30.0)
+            res.submit_stream(dx, dy, di, B, args.warmup)
+            ctx.sync()
+            ctx.hold()
+            ctx.timer_start()
+            res.submit_stream(dx, dy, di, B, args.steps, idx_offset=args.warmup * B)
+            ctx.release()
+            ms_res = ctx.timer_stop()
+            res.check()
+            res.stop()
+            del mr
     del mpre
     _, _, version, rejected = m.read()
     losses = loss.numpy() / B
@@ -298,8 +311,8 @@ def run_ours(args):
                                 "launch of the K rounds (device-side launch, prologue and teardown "
                                 "inside); the launch is queued behind a gate kernel so the host's "
                                 "call is not",
-                      "resident": {"ms_per_step": ms_res / args.steps,
-                                   "value": B * args.steps / (ms_res / 1e3),
+                      "resident": {"ms_per_step": ms_res / args.steps if ms_res else None,
+                                   "value": B * args.steps / (ms_res / 1e3) if ms_res else None,
                                    "path": "the same K rounds through the resident round service "
                                            "(ghc_resident_*): kernel launched once, one "
                                            "stream-doorbell command (submit+wait kernel → rounds → "
@@ -308,14 +321,31 @@ def run_ours(args):
     return 0
 
 
-# ncu --set full of one 200-round launch of lstm_round_kernel<5,20,10,3,4>
-# (profiles/r01_ncu_full_round_final_r1_raw.csv): dram__bytes_read.sum 63.50 MB +
-# dram__bytes_write.sum 1.44 MB → per round.  Algorithmic: the gathered batch,
-# 1000 × (50 + 1) × 4 B = 204 KB; the excess is 32-B sector granularity on the
-# unaligned 200-B rows and 4-B labels.
-TRAFFIC_PER_ROUND = (63.499776e6 + 1.436672e6) / 200
-TRAFFIC_SOURCE = ("ncu --set full, 200-round launch (profiles/r01_ncu_full_round_final_r1_raw.csv): "
+# ncu --set full of one 200-round launch of lstm_round_kernel<5,20,10,3,4> on the
+# packed dataset (profiles/r02_ncu_round_raw.csv): dram__bytes_read.sum 53.53 MB
+# + dram__bytes_write.sum 0.48 MB → per round.  Algorithmic: the gathered batch
+# + its indices, 1000 × (50 + 1 + 1) × 4 B = 208 KB; the packed 256-B rows are
+# two whole 128-B lines each (the unpacked 200-B rows + separate labels cost
+# 324.7 KB per round, profiles/r01_ncu_full_round_final_r1_raw.csv).
+TRAFFIC_PER_ROUND = (53.533184e6 + 0.484864e6) / 200
+TRAFFIC_SOURCE = ("ncu --set full, 200-round launch on packed rows (profiles/r02_ncu_round_raw.csv): "
                   "dram read+write / 200; traffic = per round × timed rounds")
+
+
+# Latency/throughput roofline of the fused round (DESIGN.md §4 "latency
+# roofline"): per phase the larger of the dependent-chain latency and the
+# pipe-throughput bound, from the measured per-SM costs of tools/sm_micro.cu
+# (profiles/r01_sm_micro.txt: dependent FFMA/FFMA2 4.9 cycles, EX2 17, SHFL
+# 24, LDS 35, STS→syncwarp→LDS 34; broadcast LDS.128 2.79 SM-cycles and FFMA
+# 1.24 SMSP-cycles per warp-instruction at 8 warps/SM) at 1965 MHz, and the
+# measured L2 / DSMEM hop latencies of the exchange.
+LATENCY_MODEL_US = {
+    "forward": 1.15,        # 10 × (LDS h + 10-deep FFMA2 chain + σ/tanh MUFU chain + SHFL + cell) ≈ 225 cyc
+    "softmax": 0.15,        # 3 butterfly sums + exp/log
+    "bptt": 2.27,           # smem-throughput bound: 8 warps × 20 broadcast LDS.128 × 2.79 SM-cyc × 10 steps
+    "weight_grads": 1.26,   # issue bound: 1000 FFMA per warp, 2 warps per SMSP × 1.24 cyc
+    "exchange": 2.10,       # DSMEM push 0.3 + 2 × L2 store→poll 0.7 + SGD 0.1 + DSMEM push 0.3
+}
 
 
 def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks, version,
@@ -348,7 +378,7 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
                      "frac": achieved_tflops / tensor_peak,
                      "traffic": args.traffic * args.steps if args.traffic else None,
                      "traffic_per_round_bytes": args.traffic,
-                     "algorithmic_bytes_per_round": B * (10 * 5 + 1) * 4,
+                     "algorithmic_bytes_per_round": B * (10 * 5 + 1 + 1) * 4,
                      "traffic_source": TRAFFIC_SOURCE,
                      "kernel": kernel + " (fused fwd+bwd+reduce+SGD)",
                      "peak_kind": f"{pk_kind} bf16 sustained / 2 (TF32) per GPU",
@@ -356,7 +386,14 @@ def result_line(args, world, ms, one_round_ms, chunk, e2e, upd, launches, clocks
                                    "frac": achieved_tflops / fp32_peak,
                                    "note": "the kernel is FFMA/MUFU/sync-bound by design "
                                            "(DESIGN.md §4)"},
-                     "one_round_launch_ms": one_round_ms},
+                     "one_round_launch_ms": one_round_ms,
+                     "latency": {"ideal_us_per_round": sum(LATENCY_MODEL_US.values()),
+                                 "achieved_us_per_round": 1e3 * ms / args.steps,
+                                 "frac": sum(LATENCY_MODEL_US.values()) / (1e3 * ms / args.steps),
+                                 "phases_us": LATENCY_MODEL_US,
+                                 "note": "the round is latency/smem-throughput bound, not FLOP "
+                                         "bound: per-phase critical path or pipe-throughput "
+                                         "bound from measured per-SM costs (DESIGN.md §4)"}},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "update_kernel": upd,
@@ -402,7 +439,10 @@ def run_ours_dist(args, rank, world, local):
     plan = gd.plan_worker(spec, world, rank, B, epochs, 99)
     counts = gd.round_counts(spec, world, B, epochs, 99)[:total_rounds]
     x, y = g.generate(spec, plan.first_file, plan.n_files)
-    dx, dy = ctx.upload(x), ctx.upload(y)
+    if p2p:  # packed rows (x | label | pad to 256 B) for the fused exchange's round kernel
+        dx, dy = g.pack_dataset(ctx, ctx.upload(x), ctx.upload(y)), None
+    else:
+        dx, dy = ctx.upload(x), ctx.upload(y)
     di = ctx.upload(plan.idx_local[: total_rounds * B])
     dc = ctx.upload(np.ascontiguousarray(counts, np.int32))
     setup_s = time.time() - t0
@@ -471,12 +511,12 @@ def run_e2e_dist(args, g, gd, tdist, ctx, arch, ex, x, y, plan, dc, rank, world)
     B = args.batch
     K = min(args.steps, args.e2e_steps)
     width = x.shape[1]
-    hx = ctx.host_array((K * B, width))
-    hy = ctx.host_array(K * B, np.int32)
-    hl = ctx.host_array(K)
     sel = plan.idx_local[: K * B]
-    hx.np[:] = x[sel]
-    hy.np[:] = y[sel]
+    xs = g.pack_rows(x[sel], y[sel])
+    hx = ctx.host_array(xs.shape)
+    hy = None
+    hl = ctx.host_array(K)
+    hx.np[:] = xs
     hl.np[:] = np.nan
     m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
     ctx.sync()
@@ -490,7 +530,7 @@ def run_e2e_dist(args, g, gd, tdist, ctx, arch, ex, x, y, plan, dc, rank, world)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     ok = bool(np.isfinite(hl.np).all())
-    for a in (hx, hy, hl):
+    for a in (hx, hl):
         a.free()
     return {"value": world * B * K / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": world * B * (width + 1) * 4, "d2h_bytes_per_step": world * 4,
@@ -550,35 +590,39 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
         scratch.free()
         return dt
 
-    # ---- host_dataset ----
-    hX = ctx.host_array(x.shape)
-    hY = ctx.host_array(y.shape, np.int32)
+    # ---- host_dataset (packed rows: x | label | pad, 256 B) ----
+    xp = g.pack_rows(x, y)
+    hX = ctx.host_array(xp.shape)
+    hY = None
     hI = ctx.host_array(K * B, np.int32)
     hl = ctx.host_array(K)
-    hX.np[:] = x
-    hY.np[:] = y
+    hX.np[:] = xp
     hI.np[:] = idx[: K * B]
+    del xp
     dt = launched(hX, hY, hI, B, K, hl)
     out = {"value": B * K / dt, "unit": UNIT,
            "h2d_bytes_per_step": B * (width * 4 + 4 + 4), "d2h_bytes_per_step": 4,
+           "h2d_bytes_moved_per_step": B * (64 * 4 + 4),
            "steps": K, "ms_per_step": 1e3 * dt / K, "losses_finite": bool(np.isfinite(hl.np).all()),
            "path": "ghc_master_sync_rounds with the dataset (182 MB), labels and shuffled index "
                    "stream in pinned host memory: each round's batch is gathered by the kernel "
                    "from host memory over PCIe (one round ahead), its loss stored to host memory"}
-    dtr = served(hX, hY, hI, B, K, hl)
-    out["host_dataset_resident"] = {"value": B * K / dtr, "ms_per_step": 1e3 * dtr / K,
-                                    "losses_finite": bool(np.isfinite(hl.np).all()),
-                                    "clock": "host perf_counter around submit + wait",
-                                    "path": "the same through ghc_resident_submit/wait (host doorbell)"}
-    for a in (hX, hY, hI):
+    if not args.no_resident:
+        dtr = served(hX, hY, hI, B, K, hl)
+        out["host_dataset_resident"] = {"value": B * K / dtr, "ms_per_step": 1e3 * dtr / K,
+                                        "losses_finite": bool(np.isfinite(hl.np).all()),
+                                        "clock": "host perf_counter around submit + wait",
+                                        "path": "the same through ghc_resident_submit/wait (host "
+                                                "doorbell)"}
+    for a in (hX, hI):
         a.free()
 
     # ---- pregathered ----
-    hx = ctx.host_array((K * B, width))
-    hy = ctx.host_array(K * B, np.int32)
     sel = idx[: K * B]
-    hx.np[:] = x[sel]
-    hy.np[:] = y[sel]
+    xs = g.pack_rows(x[sel], y[sel])
+    hx = ctx.host_array(xs.shape)
+    hy = None
+    hx.np[:] = xs
     dtp = launched(hx, hy, None, B, K, hl)
     out["pregathered"] = {"value": B * K / dtp, "steps": K, "ms_per_step": 1e3 * dtp / K,
                           "losses_finite": bool(np.isfinite(hl.np).all()),
@@ -587,35 +631,36 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
 
     # ---- per_call: one batch per call ----
     Kc = min(K, 200)
+    if not args.no_resident:
+        m = g.Master(arch, w0, 0.01, 0.9)
+        res = g.Resident(m, B)
+        hl.np[:] = np.nan
+        for k in range(3):
+            res.wait(res.submit(hx.sub(k * B), None, None, 0, 1, loss_out=hl.sub(k)))
+        t0 = time.perf_counter()
+        for k in range(Kc):
+            res.wait(res.submit(hx.sub(k * B), None, None, 0, 1, loss_out=hl.sub(k)))
+        dtc = time.perf_counter() - t0
+        res.stop()
+        out["per_call"] = {"value": B * Kc / dtc, "steps": Kc, "ms_per_step": 1e3 * dtc / Kc,
+                           "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
+                           "clock": "host perf_counter",
+                           "path": "per batch: ghc_resident_submit(1 round, batch zero-copy from "
+                                   "pinned host memory) + ghc_resident_wait (returns with the loss "
+                                   "in host memory)"}
     m = g.Master(arch, w0, 0.01, 0.9)
-    res = g.Resident(m, B)
-    hl.np[:] = np.nan
     for k in range(3):
-        res.wait(res.submit(hx.sub(k * B), hy.sub(k * B), None, 0, 1, loss_out=hl.sub(k)))
-    t0 = time.perf_counter()
-    for k in range(Kc):
-        res.wait(res.submit(hx.sub(k * B), hy.sub(k * B), None, 0, 1, loss_out=hl.sub(k)))
-    dtc = time.perf_counter() - t0
-    res.stop()
-    out["per_call"] = {"value": B * Kc / dtc, "steps": Kc, "ms_per_step": 1e3 * dtc / Kc,
-                       "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
-                       "clock": "host perf_counter",
-                       "path": "per batch: ghc_resident_submit(1 round, batch zero-copy from pinned "
-                               "host memory) + ghc_resident_wait (returns with the loss in host "
-                               "memory)"}
-    m = g.Master(arch, w0, 0.01, 0.9)
-    for k in range(3):
-        m.sync_rounds(hx.sub(k * B), hy.sub(k * B), None, 0, B, 1, loss_out=hl.sub(k))
+        m.sync_rounds(hx.sub(k * B), None, None, 0, B, 1, loss_out=hl.sub(k))
     ctx.sync()
     ctx.timer_start()
     for k in range(Kc):
-        m.sync_rounds(hx.sub(k * B), hy.sub(k * B), None, 0, B, 1, loss_out=hl.sub(k))
+        m.sync_rounds(hx.sub(k * B), None, None, 0, B, 1, loss_out=hl.sub(k))
     msl = ctx.timer_stop()
     ctx.sync()
     out["per_call_launch"] = {"value": B * Kc / (msl / 1e3), "steps": Kc, "ms_per_step": msl / Kc,
                               "path": "one ghc_master_sync_rounds(1 round) launch per batch, queued "
                                       "on one stream (CUDA events)"}
-    for a in (hx, hy, hl):
+    for a in (hx, hl):
         a.free()
     return out
 
@@ -684,6 +729,8 @@ def main():
     ap.add_argument("--ref-workers", type=int, default=0,
                     help="reference arm worker threads (0: one per host core, minus the master)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-resident", action="store_true",
+                    help="skip the resident-service measurements (automatic under ncu/nsys)")
     ap.add_argument("--preroll-calls", type=int, default=20,
                     help="N>1: untimed busy calls before the timed region (same on every rank)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "reduce_bcast", "allreduce"])
@@ -692,6 +739,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if under_profiler():
+        args.no_resident = True
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return spawn(args.gpus)
     _, world, _ = dist_env()

@@ -269,6 +269,16 @@ ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t
  * ghc_master_read).  No host synchronisation. */
 ghc_status ghc_master_apply(ghc_master* m, const float* d_g);
 
+/* Packed dataset rows for the fused sync rounds: row r = x[r][0..width) |
+ * label r (int32 bits) | zero pad, stride ghc_packed_row_floats(width) =
+ * the next multiple of 32 floats (128 B: the DRAM fetch granularity the
+ * random gather sees, measured — 224-B rows still cost 311 B per sample).
+ * A gathered sample is then whole 128-B lines with its label inside.  Pass the packed array
+ * as d_x with d_y == NULL to ghc_master_sync_rounds / ghc_p2p_sync_rounds /
+ * the resident service (SIMT cluster round kernel). */
+int32_t ghc_packed_row_floats(int32_t width);
+ghc_status ghc_dataset_pack(ghc_ctx* ctx, const float* d_x, const int32_t* d_y, int64_t rows,
+                            int32_t width, float* d_out);
 /* Resident round service: the persistent sync-round kernel launched ONCE
  * for master m (fused SIMT cluster kernel, n samples per round, n within one
  * sample per warp slot) and fed commands — a segment of `rounds` sync rounds

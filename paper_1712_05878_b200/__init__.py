@@ -11,6 +11,7 @@ from .gradhub import (Architecture, arch_info, CacheMismatchError, ConfigError, 
                       forward_backward, generate, init_weights, sgd_step, shard_files,
                       worker_grad_device, Session, train_config, DOWNPOUR, EASGD, SYNC,
                       REPLAY, validate, HostArray, encode_frame, decode_frame,
-                      FRAME_SHUTDOWN, FRAME_WEIGHTS, FRAME_GRADIENT, Resident)
+                      FRAME_SHUTDOWN, FRAME_WEIGHTS, FRAME_GRADIENT, Resident, pack_rows,
+                      pack_dataset)
 
 BENCH_ARCH = "lstm(5,20,10),softmax(20,3)"

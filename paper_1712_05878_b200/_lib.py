@@ -117,6 +117,8 @@ SIGNATURES = [
     ("ghc_master_read", C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     ("ghc_master_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp]),
     ("ghc_master_apply", C.c_int, [_vp, _vp]),
+    ("ghc_packed_row_floats", _i32, [_i32]),
+    ("ghc_dataset_pack", C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
     ("ghc_resident_start", C.c_int, [_vp, _i64, C.c_double, _vp]),
     ("ghc_resident_submit", C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     ("ghc_resident_wait", C.c_int, [_vp, _u64]),

@@ -780,11 +780,45 @@ static __global__ void count_accepted_kernel(MasterDev* ms, int n) {
   if (ms->status == 0) ms->samples += static_cast<unsigned long long>(n);
 }
 
+// Packed dataset rows (d_y == NULL): the SIMT cluster round kernel only.
+static ghc_status check_packed(const ghc_plan* p, const int32_t* d_y) {
+  if (d_y) return GHC_OK;
+  if (p->layered || !p->lstm || !p->use_cluster || p->max_clusters < 1 || p->use_tc)
+    return fail(GHC_ERR_CONFIG, "packed dataset rows (labels == NULL) need the SIMT cluster round kernel");
+  return GHC_OK;
+}
+
+__global__ void pack_rows_kernel(float* __restrict__ out, const float* __restrict__ x,
+                                 const int32_t* __restrict__ y, long long rows, int width, int stride) {
+  const long long tot = rows * stride;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / stride;
+    const int c = static_cast<int>(i - r * stride);
+    out[i] = c < width ? x[r * width + c] : (c == width ? __int_as_float(y[r]) : 0.0f);
+  }
+}
+
+int32_t ghc_packed_row_floats(int32_t width) { return (width + 1 + 31) & ~31; }
+
+ghc_status ghc_dataset_pack(ghc_ctx* c, const float* d_x, const int32_t* d_y, int64_t rows, int32_t width,
+                            float* d_out) {
+  if (!c || !d_x || !d_y || !d_out || rows < 0 || width < 1) return fail(GHC_ERR_CONFIG, "dataset_pack: bad argument");
+  const int stride = ghc_packed_row_floats(width);
+  const long long tot = rows * stride;
+  const int grid = static_cast<int>(std::min<long long>((tot + 255) / 256, 8LL * c->num_sms));
+  pack_rows_kernel<<<grid > 0 ? grid : 1, 256, 0, c->stream>>>(d_out, d_x, d_y, rows, width, stride);
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
 ghc_status ghc_master_sync_rounds(ghc_master* m, const float* d_x, const int32_t* d_y,
                                   const int32_t* d_idx, int64_t stride, const int32_t* d_counts,
                                   int64_t n, int32_t n_rounds, float* d_loss_out) {
   if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");
   if (n_rounds < 1) return GHC_OK;
+  if (ghc_status s = check_packed(m->plan, d_y)) return s;
   if (m->plan->layered) {
     // layered archs: per round the layered worker step (scale 1/n_r) then the
     // rejecting in-place sgd_step on the master's current buffers

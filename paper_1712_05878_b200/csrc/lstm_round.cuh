@@ -735,11 +735,14 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   const int32_t* idxv = nullptr;
   auto slot_x = [&](int sp, int b) { return ws + sp * N::WARP_FLOATS + N::S_X + b * N::XWP; };
   auto slot_l = [&](int sp) { return reinterpret_cast<int*>(ws + sp * N::WARP_FLOATS + N::S_L); };
+  // y == nullptr: packed dataset rows (ghc_dataset_pack) — x padded to a
+  // 32-byte multiple with the label inside the padding: one row = whole
+  // sectors, no separate label sector (DRAM traffic ≈ the algorithmic bytes)
   auto fetch_nocommit = [&](int sp, int row, int b) {
-    const float* xrow = sx + (long long)row * N::XW;
+    const float* xrow = sx + (long long)row * (sy ? N::XW : N::XWPK);
     float* dst = slot_x(sp, b);
     for (int i = lane; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);
-    if (lane == 0) cp_async4(slot_l(sp) + b, sy + row);
+    if (lane == 0) cp_async4(slot_l(sp) + b, sy ? static_cast<const void*>(sy + row) : xrow + N::XW);
   };
   auto row_of = [&](int r, int s) {
     // no gather table: round r reads rows r*stride + s (stride 0: rows s)
@@ -863,8 +866,9 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       for (; s < s1; s += NW) {
         const int row = row_of(r, s);
         float* xs = slot_x(0, 0);
-        for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(sx + (long long)row * N::XW + i);
-        int label = __ldg(sy + row);
+        const float* xrow = sx + (long long)row * (sy ? N::XW : N::XWPK);
+        for (int i = lane; i < N::XW; i += 32) xs[N::xoff(i)] = __ldg(xrow + i);
+        int label = sy ? __ldg(sy + row) : __float_as_int(__ldg(xrow + N::XW));
         __syncwarp();
         if (label < 0 || label >= K) {
           if (lane == 0) atomicOr(a.err, 1);

@@ -268,6 +268,7 @@ struct LstmNet {
   static constexpr int P = OFF_BS + K;
   static constexpr int PPAD = (P + 1 + 3) & ~3;    // + loss slot, 16-B rows
   static constexpr int XW = T * D;                       // global row width
+  static constexpr int XWPK = (XW + 1 + 31) & ~31;       // packed row: x, label, pad to 128 B
   static constexpr int DP = (D + 3) & ~3;                // x_t padded to float4s in smem
   static constexpr int XWP = T * DP;
   static constexpr bool HV = (H % 4) == 0;               // h rows loadable as float4

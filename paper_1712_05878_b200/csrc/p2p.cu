@@ -135,6 +135,8 @@ ghc_status ghc_p2p_sync_rounds(ghc_master* m, ghc_p2p* p, const float* d_x, cons
   if (n_rounds < 1) return GHC_OK;
   for (int q = 0; q < p->G; ++q)
     if (!p->gpart[q]) return fail(GHC_ERR_TRANSPORT, "p2p_sync_rounds: peers not imported");
+  if (!d_y && (p->plan->use_tc || !p->plan->use_cluster))
+    return fail(GHC_ERR_CONFIG, "packed dataset rows need the SIMT cluster round kernel");
   StepArgs a{};
   a.x = d_x;
   a.y = d_y;

@@ -126,7 +126,7 @@ ghc_status ghc_resident_start(ghc_master* m, int64_t n, double idle_seconds, ghc
 ghc_status ghc_resident_submit(ghc_resident* r, const float* x, const int32_t* y, const int32_t* idx,
                                int64_t stride, int32_t rounds, float* loss_out, uint64_t* seq_out) {
   if (!r || r->stopped) return fail(GHC_ERR_CONFIG, "resident_submit: service stopped");
-  if (rounds < 1 || !x || !y) return fail(GHC_ERR_SHAPE, "resident_submit: empty command");
+  if (rounds < 1 || !x) return fail(GHC_ERR_SHAPE, "resident_submit: empty command");
   if (vol(r->h_done + 1)) return fail(GHC_ERR_CUDA, "resident service expired (idle timeout)");
   const uint64_t seq = r->next++;
   const auto t0 = std::chrono::steady_clock::now();
@@ -168,7 +168,7 @@ ghc_status ghc_resident_submit_stream(ghc_resident* r, ghc_ctx* c, const float* 
                                       const int32_t* idx, int64_t stride, int32_t rounds, float* loss_out,
                                       uint64_t* seq_out) {
   if (!r || r->stopped || !c) return fail(GHC_ERR_CONFIG, "resident_submit_stream: service stopped");
-  if (rounds < 1 || !x || !y) return fail(GHC_ERR_SHAPE, "resident_submit_stream: empty command");
+  if (rounds < 1 || !x) return fail(GHC_ERR_SHAPE, "resident_submit_stream: empty command");
   ResidentCmd cmd{};
   cmd.x = x;
   cmd.y = y;

@@ -199,7 +199,8 @@ class P2PExchange:
                     counts_offset: int = 0, loss_offset: int = 0):
         """ghc_p2p_sync_rounds; counts: device int32 [rounds][world] or None."""
         g.check(self.ctx.lib.ghc_p2p_sync_rounds(
-            master.h, self.h, x.ptr, y.ptr, idx.offset(idx_offset) if idx is not None else None,
+            master.h, self.h, x.ptr, y.ptr if y is not None else None,
+            idx.offset(idx_offset) if idx is not None else None,
             stride, idx_vstride, counts.offset(counts_offset) if counts is not None else None,
             n_max, rounds, loss_out.offset(loss_offset) if loss_out is not None else None),
             "p2p_sync_rounds")

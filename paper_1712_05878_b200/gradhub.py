@@ -385,7 +385,8 @@ class Master:
                     loss_out: DeviceArray | None = None, idx_offset: int = 0,
                     loss_offset: int = 0, counts_offset: int = 0):
         check(self.ctx.lib.ghc_master_sync_rounds(
-            self.h, x.ptr, y.ptr, idx.offset(idx_offset) if idx is not None else None, stride,
+            self.h, x.ptr, y.ptr if y is not None else None,
+            idx.offset(idx_offset) if idx is not None else None, stride,
             counts.offset(counts_offset) if counts is not None else None, n, rounds,
             loss_out.offset(loss_offset) if loss_out is not None else None), "sync_rounds")
 
@@ -405,6 +406,27 @@ class Master:
         return wp
 
 
+def pack_rows(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Packed dataset rows on the host (ghc_dataset_pack's layout): x, the
+    label's int32 bits, zero pad to a multiple of 32 floats (128-byte rows)."""
+    x = np.ascontiguousarray(x, np.float32)
+    n, width = x.shape
+    stride = (width + 1 + 31) & ~31
+    out = np.zeros((n, stride), np.float32)
+    out[:, :width] = x
+    out[:, width] = np.ascontiguousarray(y, np.int32).view(np.float32)
+    return out
+
+
+def pack_dataset(ctx: Context, dx: DeviceArray, dy: DeviceArray) -> DeviceArray:
+    """ghc_dataset_pack on the device; pass the result as x with y=None."""
+    n, width = dx.shape
+    stride = int(ctx.lib.ghc_packed_row_floats(width))
+    out = DeviceArray(ctx, (n, stride))
+    check(ctx.lib.ghc_dataset_pack(ctx.h, dx.ptr, dy.ptr, n, width, out.ptr), "dataset_pack")
+    return out
+
+
 class Resident:
     """ghc_resident: the persistent sync-round kernel launched once for
     `master` (n samples per round) and fed commands through doorbells.
@@ -422,7 +444,8 @@ class Resident:
 
     @staticmethod
     def _args(x, y, idx, idx_offset, loss_out, loss_offset):
-        return (x.ptr, y.ptr, idx.offset(idx_offset) if idx is not None else None,
+        return (x.ptr, y.ptr if y is not None else None,
+                idx.offset(idx_offset) if idx is not None else None,
                 loss_out.offset(loss_offset) if loss_out is not None else None)
 
     def submit(self, x, y, idx, stride: int, rounds: int, loss_out=None, idx_offset: int = 0,

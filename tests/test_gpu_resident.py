@@ -99,3 +99,31 @@ def test_resident_config_errors(ctx):
     mw = g.Master(wide, g.init_weights(wide, 7), 0.01, 0.9)
     with pytest.raises(g.ConfigError):
         g.Resident(mw, 100)
+
+
+def test_packed_rows_bit_identical(ctx, monkeypatch):
+    """Packed dataset rows (x | label | pad to 32 B, labels == NULL): the same
+    rounds, bit for bit, with fewer DRAM sectors per gathered sample."""
+    R, B = 20, 1000
+    arch, x, y, idx, dx, dy, di = _setup(ctx, R, B)
+    w0 = g.init_weights(arch, 7)
+    dp = g.pack_dataset(ctx, dx, dy)
+    hp = g.pack_rows(x, y)
+    assert dp.shape[1] == 64 and np.array_equal(dp.numpy(), hp)
+    outs = []
+    for xs, ys in ((dx, dy), (dp, None)):
+        m = g.Master(arch, w0, 0.01, 0.9)
+        loss = ctx.array(R)
+        m.sync_rounds(xs, ys, di, B, B, R, loss_out=loss)
+        outs.append((m.read()[0], loss.numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    m = g.Master(arch, w0, 0.01, 0.9)  # resident service on packed rows
+    res = g.Resident(m, B)
+    res.wait(res.submit(dp, None, di, B, R))
+    res.stop()
+    assert np.array_equal(m.read()[0], outs[0][0])
+    monkeypatch.setenv("GHC_STEP", "tc")
+    atc = g.Architecture(ctx, BENCH_ARCH)
+    mt = g.Master(atc, w0, 0.01, 0.9)
+    with pytest.raises(g.ConfigError):
+        mt.sync_rounds(dp, None, di, B, B, 1)
