@@ -150,10 +150,12 @@ def preroll(run_chunk, ctx, clk, min_s=0.25):
 
 
 def under_profiler() -> bool:
-    """ncu/nsys inject through CUDA_INJECTION64_PATH and serialise kernels —
-    the resident round service (a kernel waiting on another kernel) cannot
-    run under them, so its measurements are skipped there."""
-    return bool(os.environ.get("CUDA_INJECTION64_PATH"))
+    """ncu/nsys inject into the process and serialise kernels — the gate
+    kernel and the resident round service (kernels waiting on other work)
+    cannot run under them, so the gate is skipped and the resident
+    measurements too (paper_1712_05878_b200/_lib.py PROFILER_ENV)."""
+    from paper_1712_05878_b200 import _lib
+    return _lib.under_profiler()
 
 
 def dist_env():
@@ -260,11 +262,14 @@ def run_ours(args):
         # launch is queued behind a gate kernel (ghc_stream_hold, nvbench's
         # blocking kernel) so the host's call is not inside — the device-side
         # launch, prologue and teardown are
-        ctx.hold()
+        gate = not args.no_resident  # (no gate under a profiler either)
+        if gate:
+            ctx.hold()
         ctx.timer_start()
         m.sync_rounds(dx, dy, di, B, B, args.steps, loss_out=loss, idx_offset=args.warmup * B,
                       loss_offset=args.warmup)
-        ctx.release()
+        if gate:
+            ctx.release()
         ms = ctx.timer_stop()
         ctx.sync()
         clk.mark("stop")
@@ -475,10 +480,13 @@ def run_ours_dist(args, rank, world, local):
         ctx.sync()
         tdist.barrier()
         clk.mark("start")
-        ctx.hold()  # queue the timed launches behind a gate (device time only)
+        gate = not under_profiler()
+        if gate:
+            ctx.hold()  # queue the timed launches behind a gate (device time only)
         ctx.timer_start()
         rounds(args.warmup, args.steps, args.warmup)
-        ctx.release()
+        if gate:
+            ctx.release()
         ms_local = ctx.timer_stop()
         ctx.sync()
         clk.mark("stop")

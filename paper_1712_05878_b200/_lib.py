@@ -163,6 +163,17 @@ SIGNATURES = [
 
 _lib = None
 
+# Nsight Compute / Systems inject into the process and serialise kernels:
+# cooperative cluster launches are not replayable there (plain cluster
+# launches of the same grid are — it never exceeds the co-resident clusters),
+# and kernels that wait on other kernels (the stream gate, the resident round
+# service) cannot make progress.
+PROFILER_ENV = ("NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "CUDA_INJECTION64_PATH")
+
+
+def under_profiler() -> bool:
+    return any(os.environ.get(k) for k in PROFILER_ENV)
+
 
 def load():
     """Load the in-tree libghc.so (raises if it was not built)."""
@@ -171,6 +182,8 @@ def load():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1712_05878_b200.build` "
                               "(no CPU fallback exists)")
+        if under_profiler():
+            os.environ.setdefault("GHC_NO_COOP", "1")
         lib = C.CDLL(LIB_PATH)
         for name, res, args in SIGNATURES:
             fn = getattr(lib, name)
