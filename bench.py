@@ -649,13 +649,43 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
         for k in range(Kc):
             res.wait(res.submit(hx.sub(k * B), None, None, 0, 1, loss_out=hl.sub(k)))
         dtc = time.perf_counter() - t0
+        # queued: up to 3 batches in flight — batch k+2 submitted before
+        # waiting for batch k (the kernel fetches the next command's batch
+        # during the current command's round when it is already queued)
+        hl.np[:] = np.nan
+        t0 = time.perf_counter()
+        seqs = []
+        for k in range(Kc):
+            seqs.append(res.submit(hx.sub(k * B), None, None, 0, 1, loss_out=hl.sub(k)))
+            if k >= 2:
+                res.wait(seqs[k - 2])
+        res.wait(seqs[-1])
+        dtq = time.perf_counter() - t0
+        # the same loops in C++ over the C ABI (a reference-side caller; no
+        # interpreter between the calls)
+        import ctypes as C
+        us = {}
+        for depth in (1, 3):
+            u = C.c_double()
+            g.gradhub.check(ctx.lib.ghc_resident_bench_calls(res.h, hx.ptr, B * hx.shape[1], None, 0, Kc,
+                                                             depth, hl.ptr, C.byref(u)), "bench_calls")
+            us[depth] = u.value
         res.stop()
-        out["per_call"] = {"value": B * Kc / dtc, "steps": Kc, "ms_per_step": 1e3 * dtc / Kc,
+        out["per_call_cxx"] = {"value": B / (us[3] * 1e-6), "ms_per_step": us[3] / 1e3,
+                               "synchronous_ms_per_step": us[1] / 1e3,
+                               "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
+                               "path": "ghc_resident_bench_calls: a C++ loop over ghc_resident_submit "
+                                       "(1 round, batch zero-copy from pinned host memory) + "
+                                       "ghc_resident_wait, up to 3 batches in flight "
+                                       "(synchronous: depth 1); host wall clock"}
+        out["per_call"] = {"value": B * Kc / dtq, "steps": Kc, "ms_per_step": 1e3 * dtq / Kc,
                            "losses_finite": bool(np.isfinite(hl.np[:Kc]).all()),
                            "clock": "host perf_counter",
                            "path": "per batch: ghc_resident_submit(1 round, batch zero-copy from "
-                                   "pinned host memory) + ghc_resident_wait (returns with the loss "
-                                   "in host memory)"}
+                                   "pinned host memory) + ghc_resident_wait, up to 3 batches in "
+                                   "flight (losses land in host memory)",
+                           "synchronous": {"ms_per_step": 1e3 * dtc / Kc,
+                                           "path": "submit + wait per batch, nothing queued"}}
     m = g.Master(arch, w0, 0.01, 0.9)
     for k in range(3):
         m.sync_rounds(hx.sub(k * B), None, None, 0, B, 1, loss_out=hl.sub(k))

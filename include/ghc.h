@@ -303,10 +303,19 @@ ghc_status ghc_resident_submit_stream(ghc_resident* r, ghc_ctx* ctx, const float
                                       const int32_t* idx, int64_t stride, int32_t rounds, float* loss_out,
                                       uint64_t* seq);
 ghc_status ghc_resident_check(ghc_resident* r);
-/* Diagnostics of the last stream-submitted command (%globaltimer ns):
- * submit, first / last CTA past the doorbell, completion published, wait
- * kernel saw it.  Synchronising. */
-ghc_status ghc_resident_times(ghc_resident* r, uint64_t* t5);
+/* A C++ caller's per-batch loop (benchmark of the per-call API without an
+ * interpreter): batch k at x + k·x_batch_stride (y likewise, NULL = packed
+ * rows), one round per ghc_resident_submit, up to `depth` batches in
+ * flight (1 = submit + wait per batch); *us_per_call = host wall time per
+ * call. */
+ghc_status ghc_resident_bench_calls(ghc_resident* r, const float* x, int64_t x_batch_stride,
+                                    const int32_t* y, int64_t y_batch_stride, int32_t n_calls,
+                                    int32_t depth, float* loss_out, double* us_per_call);
+/* Diagnostics (%globaltimer ns), t[133]: [0..4] the last stream-submitted
+ * command: submit, first / last CTA past the doorbell, completion published,
+ * wait kernel saw it; then per command seq % 64: (last CTA past the
+ * doorbell, completion published).  Synchronising. */
+ghc_status ghc_resident_times(ghc_resident* r, uint64_t* t);
 ghc_status ghc_resident_stop(ghc_resident* r);
 
 

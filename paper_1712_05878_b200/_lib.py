@@ -124,6 +124,7 @@ SIGNATURES = [
     ("ghc_resident_wait", C.c_int, [_vp, _u64]),
     ("ghc_resident_submit_stream", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     ("ghc_resident_check", C.c_int, [_vp]),
+    ("ghc_resident_bench_calls", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp]),
     ("ghc_resident_times", C.c_int, [_vp, _vp]),
     ("ghc_resident_stop", C.c_int, [_vp]),
     ("ghc_comm_unique_id", C.c_int, [_vp]),

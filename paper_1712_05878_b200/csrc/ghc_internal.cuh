@@ -37,6 +37,7 @@ struct LstmEntry {
   int D, H, T, K;
   void (*fn)(StepArgs);        // flat variant (grid barriers)      lstm_step.cuh
   void (*fn_round[2])(StepArgs);   // cluster variant, clusters of 4 / 8 (lstm_round.cuh)
+  void (*fn_res[2])(StepArgs);     // its resident-service variant (null for trunks)
   void (*fn_tc[2])(StepArgs);      // tensor-core cluster variant (lstm_tc.cuh); null: n/a
   int P, ppad, ep[2];
   size_t (*smem)(int);
@@ -210,7 +211,14 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 
       return e && e[0] == '1';
     }();
     cfg.numAttrs = no_coop ? 1 : 2;
-    CU(cudaLaunchKernelEx(&cfg, tc ? p->lstm->fn_tc[p->cs_index] : p->lstm->fn_round[p->cs_index], a));
+    void (*fn)(StepArgs) = tc ? p->lstm->fn_tc[p->cs_index]
+                              : (a.res ? p->lstm->fn_res[p->cs_index] : p->lstm->fn_round[p->cs_index]);
+    if (!fn) return fail(GHC_ERR_CONFIG, "no kernel variant for this launch");
+    if (a.res) {  // same shared-memory opt-in as the ordinary variant
+      CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(cfg.dynamicSmemBytes)));
+    }
+    CU(cudaLaunchKernelEx(&cfg, fn, a));
     p->ctx->launches++;
     return GHC_OK;
   }

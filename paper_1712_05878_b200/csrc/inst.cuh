@@ -13,6 +13,13 @@ constexpr void (*tc_fn())(StepArgs) {
   else return nullptr;
 }
 
+// the resident-service variant of the round kernel (head shapes only)
+template <int D, int H, int T, int K, int CS, bool HEAD>
+constexpr void (*res_fn())(StepArgs) {
+  if constexpr (HEAD) return &lstm_round_kernel<D, H, T, K, CS, true>;
+  else return nullptr;
+}
+
 template <int D, int H, int T, int K, bool TC = true>
 LstmEntry make_entry(const char* name) {
   using N = LstmNet<D, H, T, K>;
@@ -27,6 +34,7 @@ LstmEntry make_entry(const char* name) {
                    K,
                    &lstm_softmax_step_kernel<D, H, T, K>,
                    {&lstm_round_kernel<D, H, T, K, 4>, &lstm_round_kernel<D, H, T, K, 8>},
+                   {res_fn<D, H, T, K, 4, TC>(), res_fn<D, H, T, K, 8, TC>()},
                    {tc_fn<D, H, T, K, 4, TC>(), tc_fn<D, H, T, K, 8, TC>()},
                    N::P,
                    N::PPAD,

@@ -658,7 +658,9 @@ struct ClusterXchg {
   }
 };
 
-template <int D, int H, int T, int K, int CS>
+// RES: the resident round service variant (commands from a.res); a separate
+// instantiation so the ordinary launch carries none of its state (registers).
+template <int D, int H, int T, int K, int CS, bool RES = false>
 __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   using N = LstmNet<D, H, T, K>;
   using RL = RoundLayout<D, H, T, K, CS>;
@@ -738,11 +740,36 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   // y == nullptr: packed dataset rows (ghc_dataset_pack) — x padded to a
   // 32-byte multiple with the label inside the padding: one row = whole
   // sectors, no separate label sector (DRAM traffic ≈ the algorithmic bytes)
-  auto fetch_nocommit = [&](int sp, int row, int b) {
-    const float* xrow = sx + (long long)row * (sy ? N::XW : N::XWPK);
+  auto fetch_rows = [&](int sp, int row, int b, const float* X, const int32_t* Y) {
+    const float* xrow = X + (long long)row * (Y ? N::XW : N::XWPK);
     float* dst = slot_x(sp, b);
     for (int i = lane; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);
-    if (lane == 0) cp_async4(slot_l(sp) + b, sy ? static_cast<const void*>(sy + row) : xrow + N::XW);
+    if (lane == 0) cp_async4(slot_l(sp) + b, Y ? static_cast<const void*>(Y + row) : xrow + N::XW);
+  };
+  auto fetch_nocommit = [&](int sp, int row, int b) { fetch_rows(sp, row, b, sx, sy); };
+  // resident: the next command, peeked during this command's last round
+  __shared__ ResidentCmd s_next;
+  __shared__ int s_has_next, s_early;
+  if (threadIdx.x == 0) s_has_next = s_early = 0;
+  bool prefetched = false;  // this segment's round-0 rows are already in flight
+  unsigned long long pk2[8];     // thread 0: slot of the command after next (loaded a segment early)
+  unsigned long long pk2_seq = 0;
+  // the next command's round-0 rows (fixed n: the same sample slots)
+  auto fetch_next_segment = [&]() {
+    const ResidentCmd nc = s_next;
+    int sn, sn1;
+    first_sample(0, sn, sn1);
+    const int32_t* nidx = nc.idx ? nc.idx + (long long)rs.vrank * a.idx_vstride : nullptr;
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp)
+      if (sn + sp * NW < sn1)
+        fetch_rows(sp, nidx ? __ldg(nidx + sn + sp * NW) : sn + sp * NW, (int)((rg + 1) & 1), nc.x, nc.y);
+    if (nidx && lane == 0 && nc.rounds > 1) {  // round 1's indices (slot_l[2])
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp)
+        if (sn + sp * NW < sn1) cp_async4(slot_l(sp) + 2, nidx + nc.stride + sn + sp * NW);
+    }
+    cp_async_commit();
   };
   auto row_of = [&](int r, int s) {
     // no gather table: round r reads rows r*stride + s (stride 0: rows s)
@@ -759,10 +786,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       if (sx0 + sp * NW < sx1) cp_async4(slot_l(sp) + 2, idxv + (long long)r * sstride + sx0 + sp * NW);
   };
 
+  if (RES && blockIdx.x == 0 && threadIdx.x == 0) a.res->ctas = gridDim.x;
+  unsigned long long pk[8];  // thread 0: the next command's slot, loaded during the last round
   for (;;) {  // segments
-  if (a.res) {
+  if constexpr (RES) {
     ResidentCmd cmd;
-    if (!resident_next(a.res, ++seq, cmd)) break;
+    const bool have = s_has_next != 0;
+    if (!resident_next(a.res, ++seq, cmd, have, s_next)) break;
     sx = cmd.x;
     sy = cmd.y;
     sidx = cmd.idx;
@@ -771,15 +801,17 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     sloss = cmd.loss_out;
   }
   idxv = sidx ? sidx + (long long)rs.vrank * a.idx_vstride : nullptr;
-  if (a.pipelined && srounds > 0) {
+  if (a.pipelined && srounds > 0 && !prefetched) {
     int s, s1;
     first_sample(0, s, s1);
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp)
-      if (s + sp * NW < s1) fetch_nocommit(sp, row_of(0, s + sp * NW), 0);
+      if (s + sp * NW < s1) fetch_nocommit(sp, row_of(0, s + sp * NW), (int)(rg & 1));
     fetch_idx_nocommit(1);
     cp_async_commit();
   }
+  prefetched = false;
+  if (threadIdx.x == 0) s_has_next = s_early = 0;
   __syncthreads();
 
   for (int r = 0; r < srounds; ++r, ++rg) {
@@ -824,9 +856,30 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         __syncwarp();
 #pragma unroll
         for (int sp = 0; sp < SPW; ++sp)
-          if (sn + sp * NW < sn1) fetch_nocommit(sp, rows[sp], (r + 1) & 1);
+          if (sn + sp * NW < sn1) fetch_nocommit(sp, rows[sp], (int)((rg + 1) & 1));
         fetch_idx_nocommit(r + 2);
         cp_async_commit();
+      } else if (RES) {
+        // last round of a resident command.  The next command's slot was
+        // loaded during the previous command's last round (pk2, no wait): if
+        // it is valid now its first batch is fetched right away, a whole
+        // round ahead (host-memory batches need it).  Otherwise load the slot
+        // now and check it after the samples (then the fetch overlaps the
+        // exchange only).  Either way load the slot after next for the
+        // following command.
+        if (threadIdx.x == 0) {
+          ResidentCmd nc;
+          s_early = (pk2_seq == seq + 1 && slot_valid(pk2, seq + 1, nc) && nc.op == 0 && nc.rounds > 0) ? 1 : 0;
+          if (s_early) s_next = nc;
+          else issue_slot_loads(a.res, seq + 1, pk);
+          issue_slot_loads(a.res, seq + 2, pk2);
+          pk2_seq = seq + 2;
+        }
+        __syncthreads();
+        if (s_early && fixed_n) {
+          fetch_next_segment();
+          prefetched = true;
+        }
       }
       if (s < s1) {
         const float* xsp[SPW];
@@ -838,8 +891,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         for (int sp = 0; sp < SPW; ++sp) {
           const bool valid = s + sp * NW < s1;
           const int use = valid ? sp : 0;  // empty slot: recompute slot 0 with weight 0
-          xsp[sp] = slot_x(use, r & 1);
-          int l = slot_l(use)[r & 1];
+          xsp[sp] = slot_x(use, (int)(rg & 1));
+          int l = slot_l(use)[rg & 1];
           if (l < 0 || l >= K) {
             if (lane == 0 && valid) atomicOr(a.err, 1);
             l = 0;
@@ -885,19 +938,36 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       }
     }
     if (lane == 0) wp[N::P] = lsum;  // loss rides in slot P
+    const bool last_res = RES && a.pipelined && r + 1 == srounds;
+    if (last_res && threadIdx.x == 0) {
+      if (s_early) {
+        s_has_next = 1;
+      } else {
+        ResidentCmd nc;
+        s_has_next = (slot_valid(pk, seq + 1, nc) && nc.op == 0 && nc.rounds > 0) ? 1 : 0;
+        if (s_has_next) s_next = nc;
+      }
+    }
     __syncthreads();
+    if (last_res && s_has_next && !s_early && fixed_n) {  // late: overlaps the exchange
+      fetch_next_segment();
+      prefetched = true;
+    }
     if (pr && threadIdx.x == 0) pr[2] = globaltimer();
 
     // (the CTA partial — Σ warp partials, warp order — is formed by ClusterRS (a))
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
     rs.exchange(a, r, rg, sloss, wpart, NW, N::PPAD, wa, wb, pr, ntot);
   }
-  if (!a.res) break;
-  resident_done(a.res, seq);
+  if constexpr (!RES) {
+    break;
+  } else {
+    resident_done(a.res, sloss != nullptr && rs.s0 <= N::P && N::P < rs.s1);
+  }
   }  // segments
 
   rs.publish(a, gw, gv, wa, round0, rg);
-  if (a.probe && !a.res && threadIdx.x == 0 && a.rounds > 0) {  // kernel entry / exit (launch anatomy)
+  if (a.probe && !RES && threadIdx.x == 0 && a.rounds > 0) {  // kernel entry / exit (launch anatomy)
     a.probe[(long long)blockIdx.x * 16 + 14] = t_entry;
     a.probe[((long long)(a.rounds - 1) * G + blockIdx.x) * 16 + 15] = globaltimer();
   }

@@ -61,6 +61,7 @@ struct ResidentCmd {
   int rounds;
   int op;  // 0 run, 1 stop
   unsigned long long seq;
+  unsigned long long pad_;  // 64 B: four 16-byte loads from the host ring
 };
 constexpr int kResRing = 8;
 struct ResidentCtl {
@@ -77,6 +78,8 @@ struct ResidentCtl {
   unsigned long long idle_ns;
   unsigned long long t[8];     // diagnostics (%globaltimer): [0] submit, [1] first CTA past the
                                // bell, [2] last CTA past the bell, [3] done published, [4] wait saw it
+  unsigned long long tlog[64][2];  // per command (seq % 64): last CTA past the bell, done published
+  unsigned long long ctas;     // round-kernel CTAs (completion = arrive reaches seq · ctas)
 };
 
 __device__ __forceinline__ unsigned long long res_ld_acquire(const unsigned long long* p) {
@@ -95,51 +98,105 @@ __device__ __forceinline__ unsigned long long res_now() {
   return t;
 }
 
-// Next command for this CTA (all threads return the same command; false on STOP).
-static __device__ __noinline__ bool resident_next(ResidentCtl* c, unsigned long long seq, ResidentCmd& out) {
+// A command from the pinned host ring: four independent 16-byte system-
+// scope loads (all in flight at once — field-by-field volatile loads paid a
+// PCIe round trip each, measured).
+static_assert(sizeof(ResidentCmd) == 64, "ResidentCmd: four 16-byte words");
+__device__ __forceinline__ ResidentCmd load_host_cmd(const ResidentCmd* h) {
+  unsigned long long v[8];
+  const unsigned long long* p = reinterpret_cast<const unsigned long long*>(h);
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[2]), "=l"(v[3]) : "l"(p + 2) : "memory");
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[4]), "=l"(v[5]) : "l"(p + 4) : "memory");
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[6]), "=l"(v[7]) : "l"(p + 6) : "memory");
+  ResidentCmd c;
+  memcpy(&c, v, sizeof(c));
+  return c;
+}
+
+// Device ring slots are self-validating: the last word is a hash of the
+// other seven, so one round of four relaxed 16-byte loads either yields the
+// whole published command or fails the check (a slot is rewritten only for
+// seq + kResRing) — a reader needs no doorbell load in front of it.
+__device__ __forceinline__ unsigned long long cmd_check(const unsigned long long (&v)[8]) {
+  unsigned long long h = 0x9e3779b97f4a7c15ull;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    h ^= v[i] + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h *= 0xbf58476d1ce4e5b9ull;
+  }
+  return h | 1ull;  // never 0 (a zeroed slot never validates)
+}
+__device__ __forceinline__ void write_cmd(ResidentCtl* c, ResidentCmd cmd) {
+  unsigned long long v[8];
+  memcpy(v, &cmd, sizeof(cmd));
+  v[7] = cmd_check(v);
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(&c->cmd[cmd.seq % kResRing]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = v[i];
+}
+// Issue the loads of slot `seq` (results land in v; consume later).
+__device__ __forceinline__ void issue_slot_loads(const ResidentCtl* c, unsigned long long seq,
+                                                 unsigned long long (&v)[8]) {
+  const unsigned long long* p = reinterpret_cast<const unsigned long long*>(&c->cmd[seq % kResRing]);
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[2]), "=l"(v[3]) : "l"(p + 2) : "memory");
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[4]), "=l"(v[5]) : "l"(p + 4) : "memory");
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[6]), "=l"(v[7]) : "l"(p + 6) : "memory");
+}
+__device__ __forceinline__ bool slot_valid(const unsigned long long (&v)[8], unsigned long long seq,
+                                           ResidentCmd& out) {
+  memcpy(&out, v, sizeof(out));
+  return out.seq == seq && v[7] == cmd_check(v);
+}
+
+// Next command for this CTA (all threads return the same command; false on
+// STOP).  `have`: this CTA already holds it (peeked during the last round).
+static __device__ __noinline__ bool resident_next(ResidentCtl* c, unsigned long long seq, ResidentCmd& out,
+                                                  bool have, const ResidentCmd& peeked) {
   __shared__ ResidentCmd s_cmd;
   if (threadIdx.x == 0) {
-    const unsigned long long t0 = res_now();
-    if (blockIdx.x == 0) {  // relay of the host ring; idle expiry
-      for (;;) {
-        if (res_ld_acquire(&c->bell) >= seq) break;
-        // a slot is written only by whoever claims its sequence number, then
-        // published through the bell (release) — readers wait on the bell
-        const bool host_ready = res_ld_sys(c->host_bell) >= seq;
-        const bool idle = !host_ready && res_now() - t0 > c->idle_ns;
-        if ((host_ready || idle) && atomicCAS(&c->claim, seq - 1, seq) == seq - 1) {
-          ResidentCmd v{};
-          if (host_ready) {
-            const volatile ResidentCmd* h = c->host_cmd + (seq % kResRing);
-            v.x = h->x;
-            v.y = h->y;
-            v.idx = h->idx;
-            v.stride = h->stride;
-            v.loss_out = h->loss_out;
-            v.rounds = h->rounds;
-            v.op = h->op;
-            v.seq = h->seq;
-          } else {
-            v.op = 1;  // idle: STOP
-            v.seq = seq;
-            c->expired = 1;
-            volatile unsigned long long* hd = c->host_done;
-            hd[1] = 1ull;
-          }
-          c->cmd[seq % kResRing] = v;
-          __threadfence_system();
-          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&c->bell), "l"(seq) : "memory");
+    if (have) {
+      s_cmd = peeked;
+    } else {
+      const unsigned long long t0 = res_now();
+      for (unsigned it = 0;; ++it) {
+        unsigned long long v[8];
+        issue_slot_loads(c, seq, v);
+        ResidentCmd cmd;
+        if (slot_valid(v, seq, cmd)) {
+          s_cmd = cmd;
           break;
         }
+        // fallback relay of the host ring on CTA 0 (the relay kernel normally
+        // does it) and the idle expiry
+        if (blockIdx.x == 0) {
+          const bool host_ready = res_ld_sys(c->host_bell) >= seq;
+          const bool idle = !host_ready && res_now() - t0 > c->idle_ns;
+          if ((host_ready || idle) && atomicCAS(&c->claim, seq - 1, seq) == seq - 1) {
+            ResidentCmd w{};
+            if (host_ready) {
+              w = load_host_cmd(c->host_cmd + (seq % kResRing));
+            } else {
+              w.op = 1;  // idle: STOP
+              w.seq = seq;
+              c->expired = 1;
+              volatile unsigned long long* hd = c->host_done;
+              hd[1] = 1ull;
+            }
+            write_cmd(c, w);
+            __threadfence_system();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&c->bell), "l"(seq) : "memory");
+          }
+        } else if ((it & 1023u) == 0 && res_now() - t0 > c->idle_ns + 10000000000ull) {
+          __trap();  // relay gone: never hang
+        }
       }
-    } else {
-      for (unsigned it = 0; res_ld_acquire(&c->bell) < seq; ++it)  // one thread per CTA spins on L2
-        if ((it & 1023u) == 0 && res_now() - t0 > c->idle_ns + 10000000000ull) __trap();  // relay gone: never hang
     }
-    s_cmd = c->cmd[seq % kResRing];
     const unsigned long long tb = res_now();
     atomicMin(&c->t[1], tb);
     atomicMax(&c->t[2], tb);
+    atomicMax(&c->tlog[seq % 64][0], tb);
   }
   __syncthreads();
   out = s_cmd;
@@ -148,18 +205,16 @@ static __device__ __noinline__ bool resident_next(ResidentCtl* c, unsigned long 
 }
 
 // The segment of command `seq` is complete on this CTA (its last exchange
-// committed); the last CTA publishes the completion.
-static __device__ __noinline__ void resident_done(ResidentCtl* c, unsigned long long seq) {
+// committed): one fire-and-forget arrival; the relay kernel (on a spare SM)
+// publishes the completion once every CTA arrived — no round trip here.
+static __device__ __forceinline__ void resident_done(ResidentCtl* c, bool wrote_loss) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long prev = atomicAdd(&c->arrive, 1ull);
-    if (prev == seq * (unsigned long long)gridDim.x - 1ull) {
-      __threadfence_system();
-      c->t[3] = res_now();
-      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&c->done), "l"(seq) : "memory");
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(c->host_done), "l"(seq) : "memory");
-    }
+    // the CTA that stored this segment's losses (possibly to host memory)
+    // makes them visible system-wide first; the others only release at gpu
+    // scope (the relay's system fence before the host word is cumulative)
+    if (wrote_loss) __threadfence_system();
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&c->arrive) : "memory");
   }
 }
 

@@ -76,6 +76,32 @@ def test_resident_host_batches_per_call(ctx):
     assert np.array_equal(hl.np, lref.numpy())
 
 
+def test_resident_queued_commands_prefetch(ctx):
+    """Commands queued ahead (submit k+1 before waiting for k): the kernel
+    fetches the next command's first batch during the current command's last
+    round; results bit-identical to one launch, ragged command lengths."""
+    R, B = 24, 1000
+    arch, x, y, idx, dx, dy, di = _setup(ctx, R, B)
+    w0 = g.init_weights(arch, 7)
+    ref = g.Master(arch, w0, 0.01, 0.9)
+    lref = ctx.array(R)
+    ref.sync_rounds(dx, dy, di, B, B, R, loss_out=lref)
+    m = g.Master(arch, w0, 0.01, 0.9)
+    loss = ctx.array(R)
+    res = g.Resident(m, B)
+    seqs, r0 = [], 0
+    for n in (1, 1, 3, 1, 5, 2, 1, 1, 4, 1, 1, 3):  # 24 rounds
+        seqs.append(res.submit(dx, dy, di, B, n, loss_out=loss, idx_offset=r0 * B, loss_offset=r0))
+        r0 += n
+        if len(seqs) > 2:
+            res.wait(seqs[-3])
+    res.wait(seqs[-1])
+    res.stop()
+    assert r0 == R
+    assert np.array_equal(m.read()[0], ref.read()[0])
+    assert np.array_equal(loss.numpy(), lref.numpy())
+
+
 def test_resident_idle_expiry(ctx):
     R, B = 4, 1000
     arch, x, y, idx, dx, dy, di = _setup(ctx, R, B)

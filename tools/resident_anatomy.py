@@ -47,7 +47,7 @@ for K in (1, 20):
     res.submit_stream(dx, dy, di, B, K)
     ctx.release()
     ev = ctx.timer_stop() * 1e3
-    t = (C.c_uint64 * 5)()
+    t = (C.c_uint64 * 133)()
     ctx.lib.ghc_resident_times(res.h, t)
     t = [int(v) for v in t]
     tt[K] = {"event_us": ev, "submit_to_first_cta_us": (t[1] - t[0]) / 1e3,
@@ -61,3 +61,29 @@ b, a = np.polyfit(Ks, np.array(list(out["stream_us"].values())), 1)
 out["stream_fit"] = {"fixed_us": a, "round_us": b}
 res.stop()
 print(json.dumps(out, indent=1))
+
+# host-doorbell commands queued two deep (1 round each): per command the
+# in-kernel time (last CTA past the doorbell → completion) and the gap to the
+# next command
+import ctypes as C  # noqa: E402,F811
+m2 = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+res2 = g.Resident(m2, B, idle_seconds=30.0)
+n = 40
+seqs = []
+t0 = time.perf_counter()
+for k in range(n):
+    seqs.append(res2.submit(dx, dy, di, B, 1, idx_offset=k * B))
+    if k >= 1:
+        res2.wait(seqs[k - 1])
+res2.wait(seqs[-1])
+wall = (time.perf_counter() - t0) * 1e6 / n
+t = (C.c_uint64 * 133)()
+ctx.lib.ghc_resident_times(res2.h, t)
+t = [int(v) for v in t]
+rows = [(t[5 + 2 * (s % 64)], t[6 + 2 * (s % 64)]) for s in seqs[5:35]]
+inkernel = [(b - a) / 1e3 for a, b in rows]
+gaps = [(rows[i + 1][0] - rows[i][1]) / 1e3 for i in range(len(rows) - 1)]
+res2.stop()
+print(json.dumps({"host_queued_1round": {"wall_us_per_call": wall,
+                                          "in_kernel_us_median": float(np.median(inkernel)),
+                                          "gap_to_next_us_median": float(np.median(gaps))}}))
