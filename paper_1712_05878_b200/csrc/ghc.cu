@@ -349,7 +349,7 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
     if (step == "tc" && p->lstm->fn_tc[0]) {
       int64_t best_passes = INT64_MAX;
       for (int ci = 1; ci >= 0; --ci) {
-        const int cs = ci ? 8 : 4;
+        const int cs = kClusterSizes[ci];
         const int ncl = max_clusters(p->lstm->fn_tc[ci], cs, 8, p->lstm->smem_tc[ci](8));
         if (ncl < 1) continue;
         const int64_t slots = static_cast<int64_t>(ncl) * cs * kTcSamples;
@@ -365,9 +365,17 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
       }
     }
     if (!p->use_tc) {
+      // fewest warps per CTA for the bench batch; clusters of 2 (148 CTAs,
+      // 7 warps) only when forced: the sample phase is latency-bound, so 7
+      // instead of 8 warps per SM saves 0.25 µs, while 74 cluster rows per
+      // sub-slice poll cost 3 µs more in the exchange (15.5 vs 12.7 µs per
+      // round, measured).  GHC_CS=2|4|8 forces a cluster size (A/B runs).
+      const char* fcs = std::getenv("GHC_CS");
+      const int force_cs = fcs ? std::atoi(fcs) : 0;
       int best_warps = 1 << 30;
-      for (int ci = 1; ci >= 0; --ci) {
-        const int cs = ci ? 8 : 4;
+      for (int ci : {1, 0, 2}) {
+        const int cs = kClusterSizes[ci];
+        if (force_cs ? cs != force_cs : cs == 2) continue;
         int warps = 8;
         while (warps > 1 && p->lstm->smem_round[ci](warps) > static_cast<size_t>(smem_optin)) --warps;
         const int ncl = max_clusters(p->lstm->fn_round[ci], cs, warps, p->lstm->smem_round[ci](warps));
@@ -392,7 +400,7 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
   }
   CU(cudaMalloc(&p->part, sizeof(float) * static_cast<size_t>(p->max_ctas) * p->lstm->ppad));
   {  // tagged rows of the exchange: [2][clusters][EP] + weights [ranks][2][EP], tags start at 0
-    const size_t ep = static_cast<size_t>(std::max(p->lstm->ep[0], p->lstm->ep[1]));
+    const size_t ep = static_cast<size_t>(std::max({p->lstm->ep[0], p->lstm->ep[1], p->lstm->ep[2]}));
     const size_t n = 2 * static_cast<size_t>(p->max_ctas) * ep + 2 * kMaxRanks * ep;  // + weights per rank
     CU(cudaMalloc(&p->tpart, sizeof(unsigned long long) * n));
     CU(cudaMemset(p->tpart, 0, sizeof(unsigned long long) * n));

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
@@ -36,15 +37,18 @@ ghc_status ghc_fail(ghc_status s, const std::string& msg);
 struct LstmEntry {
   int D, H, T, K;
   void (*fn)(StepArgs);        // flat variant (grid barriers)      lstm_step.cuh
-  void (*fn_round[2])(StepArgs);   // cluster variant, clusters of 4 / 8 (lstm_round.cuh)
-  void (*fn_res[2])(StepArgs);     // its resident-service variant (null for trunks)
-  void (*fn_tc[2])(StepArgs);      // tensor-core cluster variant (lstm_tc.cuh); null: n/a
-  int P, ppad, ep[2];
+  // cluster variants, index ci → clusters of kClusterSizes[ci] = 4 / 8 / 2
+  void (*fn_round[3])(StepArgs);   // SIMT round kernel (lstm_round.cuh)
+  void (*fn_res[3])(StepArgs);     // its resident-service variant (null for trunks)
+  void (*fn_tc[3])(StepArgs);      // tensor-core cluster variant (lstm_tc.cuh); null: n/a
+  int P, ppad, ep[3];
   size_t (*smem)(int);
-  size_t (*smem_round[2])(int);
-  size_t (*smem_tc[2])(int);
+  size_t (*smem_round[3])(int);
+  size_t (*smem_tc[3])(int);
   const char* name;
 };
+
+constexpr int kClusterSizes[3] = {4, 8, 2};
 
 // The instantiated fused-kernel shapes (defined in ghc.cu only).
 const std::vector<LstmEntry>& lstm_table();

@@ -25,6 +25,7 @@ LstmEntry make_entry(const char* name) {
   using N = LstmNet<D, H, T, K>;
   using R4 = RoundLayout<D, H, T, K, 4>;
   using R8 = RoundLayout<D, H, T, K, 8>;
+  using R2 = RoundLayout<D, H, T, K, 2>;
   using C4 = TcLayout<D, H, T, K, 4>;
   using C8 = TcLayout<D, H, T, K, 8>;
   static_assert(C4::EP == R4::EP && C8::EP == R8::EP, "same partial-row layout");
@@ -33,15 +34,16 @@ LstmEntry make_entry(const char* name) {
                    T,
                    K,
                    &lstm_softmax_step_kernel<D, H, T, K>,
-                   {&lstm_round_kernel<D, H, T, K, 4>, &lstm_round_kernel<D, H, T, K, 8>},
-                   {res_fn<D, H, T, K, 4, TC>(), res_fn<D, H, T, K, 8, TC>()},
-                   {tc_fn<D, H, T, K, 4, TC>(), tc_fn<D, H, T, K, 8, TC>()},
+                   {&lstm_round_kernel<D, H, T, K, 4>, &lstm_round_kernel<D, H, T, K, 8>,
+                    &lstm_round_kernel<D, H, T, K, 2>},
+                   {res_fn<D, H, T, K, 4, TC>(), res_fn<D, H, T, K, 8, TC>(), res_fn<D, H, T, K, 2, TC>()},
+                   {tc_fn<D, H, T, K, 4, TC>(), tc_fn<D, H, T, K, 8, TC>(), nullptr},
                    N::P,
                    N::PPAD,
-                   {R4::EP, R8::EP},
+                   {R4::EP, R8::EP, R2::EP},
                    &N::smem_bytes,
-                   {&R4::smem_bytes, &R8::smem_bytes},
-                   {&C4::smem_bytes, &C8::smem_bytes},
+                   {&R4::smem_bytes, &R8::smem_bytes, &R2::smem_bytes},
+                   {&C4::smem_bytes, &C8::smem_bytes, nullptr},
                    name};
 }
 
