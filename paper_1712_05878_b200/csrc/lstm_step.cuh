@@ -310,6 +310,35 @@ __device__ __forceinline__ int flag_barrier(unsigned* bar, unsigned epoch, int b
   return s_bad;
 }
 
+// Operands of the CTA's weight-gradient GEMM on the tensor core
+// (lstm_round.cuh, tcgen05 kind::tf32, 3×TF32):
+//   dW[m][n] = Σ_k A[m][k] · B[n][k],  m = gate row (4H), n = [x_t | h_{t-1} | 1],
+//   k = (warp, t) — one sample per warp, T columns each.
+// Both K-major, canonical SWIZZLE_NONE layout: element (row, k) at byte
+// (k/4)·chunk + row·16 + (k%4)·4, every value split into hi = tf32(v) and
+// lo = tf32(v − hi).  lstm_samples<…, MMADW> writes this warp's columns.
+struct DwOps {
+  uint8_t* a_hi;
+  uint8_t* a_lo;
+  uint8_t* b_hi;
+  uint8_t* b_lo;
+  int a_chunk, b_chunk;  // bytes per 4-column chunk (rows · 16)
+  int kb;                // this warp's first column
+  __device__ __forceinline__ static void put(uint8_t* hi, uint8_t* lo, int off, float v) {
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - __uint_as_float(h)));
+    *reinterpret_cast<uint32_t*>(hi + off) = h;
+    *reinterpret_cast<uint32_t*>(lo + off) = l;
+  }
+  __device__ __forceinline__ void put_a(int m, int k, float v) const {
+    put(a_hi, a_lo, (k >> 2) * a_chunk + m * 16 + (k & 3) * 4, v);
+  }
+  __device__ __forceinline__ void put_b(int n, int k, float v) const {
+    put(b_hi, b_lo, (k >> 2) * b_chunk + n * 16 + (k & 3) * 4, v);
+  }
+};
+
 template <int D, int H, int T, int K>
 struct LstmNet {
   static_assert(H >= 1 && H <= 32, "one lane per hidden unit");
@@ -353,14 +382,19 @@ struct LstmNet {
 // backward starts from dh_T read from trunk_io[sp] (already scaled).
 // ACC = false: the gradient entries are STORED into wp (one sample per warp
 // and round: no zeroing of the 8.6 KB partial needed); true: added.
-template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true, bool ACC = true>
+// MMADW (SPW = 1, HEAD): no per-warp weight-gradient pass — the forward
+// writes this sample's [x_t | h_{t-1}] and the BPTT its dz_t into the CTA's
+// tensor-core operands `dw` (DwOps); wp receives only the softmax-head entries.
+template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true, bool ACC = true,
+          bool MMADW = false>
 __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, float* __restrict__ ws,
                                              float* __restrict__ wp,
                                              const float* const (&xs)[SPW],
                                              const int (&label)[SPW], const float (&scale)[SPW],
                                              int lane, float* const (&probs_row)[SPW],
                                              float (&loss)[SPW], unsigned long long* pr,
-                                             float* const (&trunk_io)[SPW]) {
+                                             float* const (&trunk_io)[SPW], const DwOps* dw = nullptr) {
+  static_assert(!MMADW || (SPW == 1 && HEAD && BWD), "tensor-core dW: one sample per warp, softmax head");
   using N = LstmNet<D, H, T, K>;
   constexpr int DP = N::DP;
   const bool act = lane < H;
@@ -470,56 +504,79 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     float c[SPW];
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp) c[sp] = 0.0f;
+    // b + Wx·x_t of one sample (the first terms of each row's sum)
+    auto xpart = [&](int sp, int t, float2 (&a)[NR]) {
+      float xv[DP];
+      load_x(sp, t, xv);
+#pragma unroll
+      for (int sl = 0; sl < NR; ++sl) {
+        a[sl] = make_float2(br[sl], 0.0f);
+#pragma unroll
+        for (int m = 0; m < DH; ++m) a[sl] = __ffma2_rn(wxr[sl][m], make_float2(xv[2 * m], xv[2 * m + 1]), a[sl]);
+        if (D & 1) a[sl].x = fmaf(wxt[sl], xv[D - 1], a[sl].x);
+      }
+    };
+    // activations, gate gather, cell update, cache + h_t stores
+    auto gates = [&](int sp, int t, const float2 (&a)[NR]) {
+      float y[NR];
+#pragma unroll
+      for (int sl = 0; sl < NR; ++sl)
+        y[sl] = fmaf(be[sl], rcp_approx(1.0f + ex2_approx(al[sl] * (a[sl].x + a[sl].y))), ga[sl]);
+      float gq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        unsigned pv = 0u;
+#pragma unroll
+        for (int sl = 0; sl < NR; ++sl) pv |= __float_as_uint(y[sl]) & pick[q][sl];
+        gq[q] = __shfl_sync(0xffffffffu, __uint_as_float(pv), src[q]);
+      }
+      const float ig = gq[0], fg = gq[1], gg = gq[2], og = gq[3];
+      c[sp] = fmaf(fg, c[sp], ig * gg);
+      const float tc = tanh_f(c[sp]);
+      float* ct = cs[sp] + (t * H + j) * 8;
+      reinterpret_cast<float4*>(ct)[0] = make_float4(ig, fg, gg, og);
+      reinterpret_cast<float2*>(ct)[2] = make_float2(c[sp], tc);
+      hs[sp][t * H + j] = og * tc;
+    };
+    // Software-pipelined over t: step t's chain is LDS h_{t-1} → Wh·h → σ/tanh
+    // → h_t; the input projection of step t+1 (independent of h) is computed
+    // inside step t, off that chain.  Same operations in the same order per
+    // row as the straight loop: bit-identical.
+    float2 accn[SPW][NR];
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) xpart(sp, 0, accn[sp]);
+    {
+      float2 acc[SPW][NR];
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp)
+#pragma unroll
+        for (int sl = 0; sl < NR; ++sl) acc[sp][sl] = accn[sp][sl];
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp) xpart(sp, T > 1 ? 1 : 0, accn[sp]);
+#pragma unroll
+      for (int sp = 0; sp < SPW; ++sp) gates(sp, 0, acc[sp]);
+      __syncwarp();
+    }
 #pragma unroll 1
-    for (int t = 0; t < T; ++t) {
+    for (int t = 1; t < T; ++t) {
       float2 acc[SPW][NR];
 #pragma unroll
       for (int sp = 0; sp < SPW; ++sp) {
-        float xv[DP];
-        load_x(sp, t, xv);
+        float hv[H];
+        load_h(sp, t - 1, hv);
 #pragma unroll
-        for (int sl = 0; sl < NR; ++sl) {
-          acc[sp][sl] = make_float2(br[sl], 0.0f);
+        for (int sl = 0; sl < NR; ++sl) acc[sp][sl] = accn[sp][sl];
 #pragma unroll
-          for (int m = 0; m < DH; ++m)
-            acc[sp][sl] = __ffma2_rn(wxr[sl][m], make_float2(xv[2 * m], xv[2 * m + 1]), acc[sp][sl]);
-          if (D & 1) acc[sp][sl].x = fmaf(wxt[sl], xv[D - 1], acc[sp][sl].x);
-        }
+        for (int m = 0; m < HH; ++m)
+#pragma unroll
+          for (int sl = 0; sl < NR; ++sl)
+            acc[sp][sl] = __ffma2_rn(whr[sl][m], make_float2(hv[2 * m], hv[2 * m + 1]), acc[sp][sl]);
       }
-      if (t > 0) {
+      const int tn = t + 1 < T ? t + 1 : t;  // last step: a harmless reload
 #pragma unroll
-        for (int sp = 0; sp < SPW; ++sp) {
-          float hv[H];
-          load_h(sp, t - 1, hv);
+      for (int sp = 0; sp < SPW; ++sp) xpart(sp, tn, accn[sp]);
 #pragma unroll
-          for (int m = 0; m < HH; ++m)
-#pragma unroll
-            for (int sl = 0; sl < NR; ++sl)
-              acc[sp][sl] = __ffma2_rn(whr[sl][m], make_float2(hv[2 * m], hv[2 * m + 1]), acc[sp][sl]);
-        }
-      }
-#pragma unroll
-      for (int sp = 0; sp < SPW; ++sp) {
-        float y[NR];
-#pragma unroll
-        for (int sl = 0; sl < NR; ++sl)
-          y[sl] = fmaf(be[sl], rcp_approx(1.0f + ex2_approx(al[sl] * (acc[sp][sl].x + acc[sp][sl].y))), ga[sl]);
-        float gq[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          unsigned pv = 0u;
-#pragma unroll
-          for (int sl = 0; sl < NR; ++sl) pv |= __float_as_uint(y[sl]) & pick[q][sl];
-          gq[q] = __shfl_sync(0xffffffffu, __uint_as_float(pv), src[q]);
-        }
-        const float ig = gq[0], fg = gq[1], gg = gq[2], og = gq[3];
-        c[sp] = fmaf(fg, c[sp], ig * gg);
-        const float tc = tanh_f(c[sp]);
-        float* ct = cs[sp] + (t * H + j) * 8;
-        reinterpret_cast<float4*>(ct)[0] = make_float4(ig, fg, gg, og);
-        reinterpret_cast<float2*>(ct)[2] = make_float2(c[sp], tc);
-        hs[sp][t * H + j] = og * tc;
-      }
+      for (int sp = 0; sp < SPW; ++sp) gates(sp, t, acc[sp]);
       __syncwarp();
     }
   } else {
@@ -606,6 +663,10 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     }
   }
   if (pr && lane == 0) pr[9] = globaltimer();
+  if constexpr (MMADW) {  // B columns of this sample: x_t (rows 0..D-1), h_{t-1} (rows D..D+H-1, t ≥ 1)
+    for (int i = lane; i < T * D; i += 32) dw->put_b(i % D, dw->kb + i / D, xs[0][(i / D) * DP + (i % D)]);
+    for (int i = lane; i < (T - 1) * H; i += 32) dw->put_b(D + i % H, dw->kb + 1 + i / H, hs[0][i]);
+  }
 
   float dh[SPW];
   if constexpr (!HEAD) {
@@ -681,25 +742,48 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     float dc[SPW];
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp) dc[sp] = 0.0f;
+    // the forward cache of step t (gates; c, tanh c) and c_{t-1}, loaded one
+    // step ahead so their shared-memory latency is off the dh chain
+    auto cache_g = [&](int sp, int t) { return reinterpret_cast<const float4*>(cs[sp] + (t * H + j) * 8)[0]; };
+    auto cache_c = [&](int sp, int t) { return reinterpret_cast<const float2*>(cs[sp] + (t * H + j) * 8)[2]; };
+    float4 gn[SPW];
+    float2 cn[SPW], cpn[SPW];
+#pragma unroll
+    for (int sp = 0; sp < SPW; ++sp) {
+      gn[sp] = cache_g(sp, T - 1);
+      cn[sp] = cache_c(sp, T - 1);
+      cpn[sp] = cache_c(sp, T > 1 ? T - 2 : 0);
+    }
 #pragma unroll 1
     for (int t = T - 1; t >= 0; --t) {
       float fgs[SPW];
 #pragma unroll
       for (int sp = 0; sp < SPW; ++sp) {
-        const float* ct = cs[sp] + (t * H + j) * 8;
-        const float4 g4 = reinterpret_cast<const float4*>(ct)[0];
+        const float4 g4 = gn[sp];
         const float ig = g4.x, fg = g4.y, gg = g4.z, og = g4.w;
-        const float tc = ct[5];
-        const float cp = t > 0 ? cs[sp][((t - 1) * H + j) * 8 + 4] : 0.0f;
+        const float tc = cn[sp].y;
+        const float cp = t > 0 ? cpn[sp].x : 0.0f;
+        const int t1 = t > 0 ? t - 1 : 0, t2 = t > 1 ? t - 2 : 0;
+        gn[sp] = cache_g(sp, t1);
+        cn[sp] = cpn[sp];
+        cpn[sp] = cache_c(sp, t2);
         fgs[sp] = fg;
         const float dout = dh[sp] * tc;
         dc[sp] = fmaf(dh[sp] * og, 1.0f - tc * tc, dc[sp]);
         const float di = dc[sp] * gg, dg = dc[sp] * ig, df = dc[sp] * cp;
         float* dzt = dzs[sp] + t * 4 * H;
-        dzt[0 * H + j] = di * ig * (1.0f - ig);
-        dzt[1 * H + j] = df * fg * (1.0f - fg);
-        dzt[2 * H + j] = dg * (1.0f - gg * gg);
-        dzt[3 * H + j] = dout * og * (1.0f - og);
+        const float z0 = di * ig * (1.0f - ig), z1 = df * fg * (1.0f - fg);
+        const float z2 = dg * (1.0f - gg * gg), z3 = dout * og * (1.0f - og);
+        dzt[0 * H + j] = z0;
+        dzt[1 * H + j] = z1;
+        dzt[2 * H + j] = z2;
+        dzt[3 * H + j] = z3;
+        if constexpr (MMADW) {  // off the dh chain: stores only
+          dw->put_a(0 * H + j, dw->kb + t, z0);
+          dw->put_a(1 * H + j, dw->kb + t, z1);
+          dw->put_a(2 * H + j, dw->kb + t, z2);
+          dw->put_a(3 * H + j, dw->kb + t, z3);
+        }
       }
       __syncwarp();
       if (t > 0) {  // dh_{t-1} = Whᵀ dz_t (the reference also does this at t=0, unused)
@@ -722,7 +806,9 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   if (pr && lane == 0) pr[11] = globaltimer();
 
   // ------- backward pass 2: dWx, dWh, db = Σ_{s,t} dz ⊗ [x_t, h_{t-1}] -------
-  if (act) {
+  if constexpr (MMADW) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // operands → tensor core (async proxy)
+  } else if (act) {
     float dz[SPW][T][4];
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp)
