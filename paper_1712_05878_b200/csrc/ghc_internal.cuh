@@ -179,10 +179,6 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 
       const int64_t slots = static_cast<int64_t>(maxc) * cs * spw;
       warps = static_cast<int>((n_max + slots - 1) / slots);
       warps = warps < 1 ? 1 : (warps > p->round_warps ? p->round_warps : warps);
-      // the tensor-core weight gradient reads its 4H accumulator rows through
-      // the TMEM lane quarters of warps 0..3 (RoundLayout::kMinWarps)
-      const int minw = (4 * p->lstm->H + 31) / 32;
-      if (spw == 1 && warps < minw) warps = minw;
       per_cta = static_cast<int64_t>(warps) * spw;
     }
     int64_t ctas = (n_max + per_cta - 1) / per_cta;

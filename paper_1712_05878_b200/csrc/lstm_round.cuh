@@ -24,7 +24,6 @@
 
 #include <cooperative_groups.h>
 
-#include "dense_gemm.cuh"
 #include "lstm_step.cuh"
 
 namespace ghc {
@@ -397,29 +396,8 @@ struct RoundLayout {
   // weight buffers receive whole slices (st.async) → at least EP floats
   static constexpr int WBP = N::PPAD > EP ? N::PPAD : EP;
   static constexpr int RSF = ClusterRS<N::P, SL, EP, CS>::smem_floats();
-  // Weight gradient on the tensor core (pipelined backward rounds, DwOps):
-  // A = dz [MA = 4H rows][KP], B = [x | h | 1] [NB rows][KP], hi + lo each;
-  // per-warp softmax-head partials [nw][HP]; the CTA partial [PPAD].  The
-  // MMA is M = 128: rows MA..127 read the following bytes (ignored outputs).
-  static constexpr int MA = 4 * H;
-  static constexpr int NB = ((D + H + 1 + 15) / 16) * 16;
-  static constexpr int HP = (K * H + K + 1 + 3) & ~3;
-  static constexpr int NACC = 4;  // TMEM accumulators, K-steps rotate over them
-  static constexpr int TCOLS = NACC * NB <= 32 ? 32 : NACC * NB <= 64 ? 64 : NACC * NB <= 128 ? 128 : 256;
-  static_assert(MA <= 128 && NB <= 64, "tensor-core dW tile");
-  __host__ __device__ static int kpad(int nw) { return ((nw * T + 7) / 8) * 8; }
-  __host__ __device__ static int a_bytes(int nw) { return kpad(nw) / 4 * MA * 16; }
-  __host__ __device__ static int b_bytes(int nw) { return kpad(nw) / 4 * NB * 16; }
-  // the partial region: per-warp partials [nw][PPAD] (non-pipelined rounds)
-  // or the tensor-core operands + head partials + CTA partial
-  __host__ __device__ static int part_floats(int nw) {
-    const int mma = (2 * a_bytes(nw) + 2 * b_bytes(nw)) / 4 + nw * HP + N::PPAD;
-    return nw * N::PPAD > mma ? nw * N::PPAD : mma;
-  }
-  // fewest warps per CTA for which the 4 TMEM lane quarters cover the MA rows
-  static constexpr int kMinWarps = (MA + 31) / 32;
   static size_t smem_bytes(int nw) {
-    return sizeof(float) * (size_t)(2 * WBP + nw * SPW * N::WARP_FLOATS + part_floats(nw) + 2 * SL +
+    return sizeof(float) * (size_t)(2 * WBP + nw * SPW * N::WARP_FLOATS + nw * N::PPAD + 2 * SL +
                                     ((CS + 3) & ~3) + RSF);
   }
 };
@@ -698,8 +676,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   float* wbuf0 = smem;
   float* wbuf1 = smem + RL::WBP;
   float* ws = smem + 2 * RL::WBP + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
-  float* wpart = smem + 2 * RL::WBP + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD] (or the dW operands)
-  float* vsl = wpart + RL::part_floats(NW);                     // [SL] velocity slice
+  float* wpart = smem + 2 * RL::WBP + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
+  float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
   ClusterRS<N::P, SL, RL::EP, CS> rs;  // the round's exchange (one GPU or GX ranks)
   rs.init(a, cluster, vsl + 2 * SL + ((CS + 3) & ~3));
 
@@ -713,51 +691,6 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   float* gw = sgd ? (cur ? a.w1 : a.w0) : nullptr;  // master weights in HBM
   float* gv = sgd ? (cur ? a.v1 : a.v0) : nullptr;
   rs.load_state(sgd ? gw : a.w_in, gv, wbuf0);
-
-  // ---- weight gradient on the tensor core (pipelined backward rounds) ----
-  // Each warp writes its sample's dz / [x, h, 1] columns (lstm_samples
-  // MMADW); one thread issues the 3×TF32 tcgen05.mma chain over K = NW·T;
-  // TMEM → the CTA partial.  Replaces the per-warp FFMA pass (≈ 1000 FFMA
-  // per warp on 20 of 32 lanes) and the 8-way warp-partial sum.
-  constexpr bool kMma = SPW == 1;
-  const bool use_mma = kMma && a.pipelined && a.mode != MODE_FWD;
-  if (use_mma && NW < RL::kMinWarps) __trap();  // the host sizes CTAs for the TMEM lane quarters
-  uint8_t* const opb = reinterpret_cast<uint8_t*>(wpart);
-  DwOps dw;
-  dw.a_hi = opb;
-  dw.a_lo = opb + RL::a_bytes(NW);
-  dw.b_hi = opb + 2 * RL::a_bytes(NW);
-  dw.b_lo = dw.b_hi + RL::b_bytes(NW);
-  dw.a_chunk = RL::MA * 16;
-  dw.b_chunk = RL::NB * 16;
-  dw.kb = warp * T;
-  float* const hpart = reinterpret_cast<float*>(dw.b_lo + RL::b_bytes(NW));  // [NW][HP]
-  float* const cpart = hpart + NW * RL::HP;                                  // [PPAD]
-  __shared__ uint64_t s_mma_bar;
-  __shared__ uint32_t s_tmem;
-  unsigned mma_phase = 0;
-  if (use_mma) {
-    // zero the operands: pad columns k ≥ NW·T and h_{-1} stay 0; row D+H of
-    // B (the bias column of dW) is 1
-    const int nz = (2 * RL::a_bytes(NW) + 2 * RL::b_bytes(NW)) / 16;
-    for (int i = threadIdx.x; i < nz; i += blockDim.x)
-      reinterpret_cast<float4*>(opb)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
-    for (int k = threadIdx.x; k < NW * T; k += blockDim.x)
-      *reinterpret_cast<float*>(dw.b_hi + (k >> 2) * dw.b_chunk + (D + H) * 16 + (k & 3) * 4) = 1.0f;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (threadIdx.x == 0) {
-      gemm_detail::mbar_init(&s_mma_bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       gemm_detail::smem_u32(&s_tmem)),
-                   "n"(RL::TCOLS));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-  }
   cluster.sync();  // peers' mbarriers initialised before any st.async
   float* wa = wbuf0;  // weights the samples use
   float* wb = wbuf1;  // peers deposit the next weights here
@@ -899,17 +832,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     // One sample per warp (pipelined, SPW = 1): lstm_samples STORES every
     // gradient entry of the warp partial; otherwise zero it and accumulate.
     constexpr bool kStore = SPW == 1;
-    float* wp = use_mma ? hpart + warp * RL::HP - N::OFF_WS  // head entries only
-                        : wpart + warp * N::PPAD;
-    if (use_mma) {
-      if (s >= s1) {  // no sample: zero head partial, dz and [x, h] columns of this warp
-        for (int p = lane; p < RL::HP; p += 32) hpart[warp * RL::HP + p] = 0.0f;
-        for (int i = lane; i < RL::MA * T; i += 32) dw.put_a(i % RL::MA, dw.kb + i / RL::MA, 0.0f);
-        for (int i = lane; i < (D + H) * T; i += 32) dw.put_b(i % (D + H), dw.kb + i / (D + H), 0.0f);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-      }
-    } else if (!(a.pipelined && kStore) || s >= s1) {
+    float* wp = wpart + warp * N::PPAD;
+    if (!(a.pipelined && kStore) || s >= s1) {
       for (int p = lane; p < N::PPAD / 4; p += 32)
         reinterpret_cast<float4*>(wp)[p] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
@@ -984,9 +908,6 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         if (a.mode == MODE_FWD)
           lstm_samples<D, H, T, K, false, SPW, true, !kStore>(wa, ws, wp, xsp, lab, scl, lane, prb,
                                                               lo, ps, tio);
-        else if constexpr (kMma)
-          lstm_samples<D, H, T, K, true, SPW, true, false, true>(wa, ws, wp, xsp, lab, scl, lane, prb, lo,
-                                                                 ps, tio, &dw);
         else
           lstm_samples<D, H, T, K, true, SPW, true, !kStore>(wa, ws, wp, xsp, lab, scl, lane, prb, lo,
                                                              ps, tio);
@@ -1034,75 +955,9 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     }
     if (pr && threadIdx.x == 0) pr[2] = globaltimer();
 
-    if (use_mma) {
-      // dW[m][n] = Σ_k A[m][k]·B[n][k] over the CTA's NW·T columns, 3×TF32
-      // (lo·hi + hi·lo + hi·hi; K-steps rotate over NACC accumulators so each
-      // takes few of the tensor core's truncating fp32 adds — dense_gemm.cuh)
-      if (threadIdx.x == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t ahi = gemm_detail::smem_u32(dw.a_hi), alo = gemm_detail::smem_u32(dw.a_lo);
-        const uint32_t bhi = gemm_detail::smem_u32(dw.b_hi), blo = gemm_detail::smem_u32(dw.b_lo);
-        constexpr uint32_t idesc = gemm_detail::make_idesc(RL::NB);
-        const int nks = RL::kpad(NW) / 8;
-        for (int ks = 0; ks < nks; ++ks) {
-          const uint32_t ao = ks * 2 * dw.a_chunk, bo = ks * 2 * dw.b_chunk;
-          const uint64_t dah = gemm_detail::make_desc(ahi + ao, dw.a_chunk, 128);
-          const uint64_t dal = gemm_detail::make_desc(alo + ao, dw.a_chunk, 128);
-          const uint64_t dbh = gemm_detail::make_desc(bhi + bo, dw.b_chunk, 128);
-          const uint64_t dbl = gemm_detail::make_desc(blo + bo, dw.b_chunk, 128);
-          const uint32_t d = s_tmem + (uint32_t)((ks % RL::NACC) * RL::NB);
-          gemm_detail::umma_tf32(d, dal, dbh, idesc, ks >= RL::NACC ? 1u : 0u);
-          gemm_detail::umma_tf32(d, dah, dbl, idesc, 1u);
-          gemm_detail::umma_tf32(d, dah, dbh, idesc, 1u);
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            gemm_detail::smem_u32(&s_mma_bar)));
-      }
-      gemm_detail::mbar_wait(&s_mma_bar, mma_phase);
-      mma_phase ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const int nacc = min(RL::NACC, RL::kpad(NW) / 8);
-      if (warp < 4 && warp * 32 < RL::MA) {  // TMEM lane quarter `warp` = gate rows 32·warp + lane
-        const int m = warp * 32 + lane;
-        const uint32_t trow = s_tmem + ((uint32_t)(warp * 32) << 16);
-        constexpr int NU = D + H + 1;
-#pragma unroll
-        for (int c0 = 0; c0 < RL::NB; c0 += 16) {
-          float acc[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
-          for (int q = 0; q < nacc; ++q) {
-            uint32_t v[16];
-            tmem_ld<16>(v, trow + (uint32_t)(q * RL::NB + c0));
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] += __uint_as_float(v[i]);
-          }
-          if (m < RL::MA) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int n = c0 + i;
-              if (n < D) cpart[N::OFF_WX + m * D + n] = acc[i];
-              else if (n < D + H) cpart[N::OFF_WH + m * H + (n - D)] = acc[i];
-              else if (n < NU) cpart[N::OFF_B + m] = acc[i];
-            }
-          }
-        }
-      }
-      // softmax head + loss: Σ warp partials in warp order
-      for (int i = threadIdx.x; i < K * H + K + 1; i += blockDim.x) {
-        float t = hpart[i];
-        for (int w = 1; w < NW; ++w) t += hpart[w * RL::HP + i];
-        cpart[N::OFF_WS + i] = t;
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
-      if (pr && threadIdx.x == 0) pr[3] = globaltimer();
-      rs.exchange(a, r, rg, sloss, cpart, 1, N::PPAD, wa, wb, pr, ntot);
-    } else {
     // (the CTA partial — Σ warp partials, warp order — is formed by ClusterRS (a))
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
     rs.exchange(a, r, rg, sloss, wpart, NW, N::PPAD, wa, wb, pr, ntot);
-    }
   }
   if constexpr (!RES) {
     break;
@@ -1111,12 +966,6 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   }
   }  // segments
 
-  if (use_mma) {
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (warp == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(RL::TCOLS));
-  }
   rs.publish(a, gw, gv, wa, round0, rg);
   if (a.probe && !RES && threadIdx.x == 0 && a.rounds > 0) {  // kernel entry / exit (launch anatomy)
     a.probe[(long long)blockIdx.x * 16 + 14] = t_entry;

@@ -310,35 +310,6 @@ __device__ __forceinline__ int flag_barrier(unsigned* bar, unsigned epoch, int b
   return s_bad;
 }
 
-// Operands of the CTA's weight-gradient GEMM on the tensor core
-// (lstm_round.cuh, tcgen05 kind::tf32, 3×TF32):
-//   dW[m][n] = Σ_k A[m][k] · B[n][k],  m = gate row (4H), n = [x_t | h_{t-1} | 1],
-//   k = (warp, t) — one sample per warp, T columns each.
-// Both K-major, canonical SWIZZLE_NONE layout: element (row, k) at byte
-// (k/4)·chunk + row·16 + (k%4)·4, every value split into hi = tf32(v) and
-// lo = tf32(v − hi).  lstm_samples<…, MMADW> writes this warp's columns.
-struct DwOps {
-  uint8_t* a_hi;
-  uint8_t* a_lo;
-  uint8_t* b_hi;
-  uint8_t* b_lo;
-  int a_chunk, b_chunk;  // bytes per 4-column chunk (rows · 16)
-  int kb;                // this warp's first column
-  __device__ __forceinline__ static void put(uint8_t* hi, uint8_t* lo, int off, float v) {
-    uint32_t h, l;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - __uint_as_float(h)));
-    *reinterpret_cast<uint32_t*>(hi + off) = h;
-    *reinterpret_cast<uint32_t*>(lo + off) = l;
-  }
-  __device__ __forceinline__ void put_a(int m, int k, float v) const {
-    put(a_hi, a_lo, (k >> 2) * a_chunk + m * 16 + (k & 3) * 4, v);
-  }
-  __device__ __forceinline__ void put_b(int n, int k, float v) const {
-    put(b_hi, b_lo, (k >> 2) * b_chunk + n * 16 + (k & 3) * 4, v);
-  }
-};
-
 template <int D, int H, int T, int K>
 struct LstmNet {
   static_assert(H >= 1 && H <= 32, "one lane per hidden unit");
@@ -382,19 +353,14 @@ struct LstmNet {
 // backward starts from dh_T read from trunk_io[sp] (already scaled).
 // ACC = false: the gradient entries are STORED into wp (one sample per warp
 // and round: no zeroing of the 8.6 KB partial needed); true: added.
-// MMADW (SPW = 1, HEAD): no per-warp weight-gradient pass — the forward
-// writes this sample's [x_t | h_{t-1}] and the BPTT its dz_t into the CTA's
-// tensor-core operands `dw` (DwOps); wp receives only the softmax-head entries.
-template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true, bool ACC = true,
-          bool MMADW = false>
+template <int D, int H, int T, int K, bool BWD, int SPW, bool HEAD = true, bool ACC = true>
 __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, float* __restrict__ ws,
                                              float* __restrict__ wp,
                                              const float* const (&xs)[SPW],
                                              const int (&label)[SPW], const float (&scale)[SPW],
                                              int lane, float* const (&probs_row)[SPW],
                                              float (&loss)[SPW], unsigned long long* pr,
-                                             float* const (&trunk_io)[SPW], const DwOps* dw = nullptr) {
-  static_assert(!MMADW || (SPW == 1 && HEAD && BWD), "tensor-core dW: one sample per warp, softmax head");
+                                             float* const (&trunk_io)[SPW]) {
   using N = LstmNet<D, H, T, K>;
   constexpr int DP = N::DP;
   const bool act = lane < H;
@@ -663,10 +629,6 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     }
   }
   if (pr && lane == 0) pr[9] = globaltimer();
-  if constexpr (MMADW) {  // B columns of this sample: x_t (rows 0..D-1), h_{t-1} (rows D..D+H-1, t ≥ 1)
-    for (int i = lane; i < T * D; i += 32) dw->put_b(i % D, dw->kb + i / D, xs[0][(i / D) * DP + (i % D)]);
-    for (int i = lane; i < (T - 1) * H; i += 32) dw->put_b(D + i % H, dw->kb + 1 + i / H, hs[0][i]);
-  }
 
   float dh[SPW];
   if constexpr (!HEAD) {
@@ -742,48 +704,25 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     float dc[SPW];
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp) dc[sp] = 0.0f;
-    // the forward cache of step t (gates; c, tanh c) and c_{t-1}, loaded one
-    // step ahead so their shared-memory latency is off the dh chain
-    auto cache_g = [&](int sp, int t) { return reinterpret_cast<const float4*>(cs[sp] + (t * H + j) * 8)[0]; };
-    auto cache_c = [&](int sp, int t) { return reinterpret_cast<const float2*>(cs[sp] + (t * H + j) * 8)[2]; };
-    float4 gn[SPW];
-    float2 cn[SPW], cpn[SPW];
-#pragma unroll
-    for (int sp = 0; sp < SPW; ++sp) {
-      gn[sp] = cache_g(sp, T - 1);
-      cn[sp] = cache_c(sp, T - 1);
-      cpn[sp] = cache_c(sp, T > 1 ? T - 2 : 0);
-    }
 #pragma unroll 1
     for (int t = T - 1; t >= 0; --t) {
       float fgs[SPW];
 #pragma unroll
       for (int sp = 0; sp < SPW; ++sp) {
-        const float4 g4 = gn[sp];
+        const float* ct = cs[sp] + (t * H + j) * 8;
+        const float4 g4 = reinterpret_cast<const float4*>(ct)[0];
         const float ig = g4.x, fg = g4.y, gg = g4.z, og = g4.w;
-        const float tc = cn[sp].y;
-        const float cp = t > 0 ? cpn[sp].x : 0.0f;
-        const int t1 = t > 0 ? t - 1 : 0, t2 = t > 1 ? t - 2 : 0;
-        gn[sp] = cache_g(sp, t1);
-        cn[sp] = cpn[sp];
-        cpn[sp] = cache_c(sp, t2);
+        const float tc = ct[5];
+        const float cp = t > 0 ? cs[sp][((t - 1) * H + j) * 8 + 4] : 0.0f;
         fgs[sp] = fg;
         const float dout = dh[sp] * tc;
         dc[sp] = fmaf(dh[sp] * og, 1.0f - tc * tc, dc[sp]);
         const float di = dc[sp] * gg, dg = dc[sp] * ig, df = dc[sp] * cp;
         float* dzt = dzs[sp] + t * 4 * H;
-        const float z0 = di * ig * (1.0f - ig), z1 = df * fg * (1.0f - fg);
-        const float z2 = dg * (1.0f - gg * gg), z3 = dout * og * (1.0f - og);
-        dzt[0 * H + j] = z0;
-        dzt[1 * H + j] = z1;
-        dzt[2 * H + j] = z2;
-        dzt[3 * H + j] = z3;
-        if constexpr (MMADW) {  // off the dh chain: stores only
-          dw->put_a(0 * H + j, dw->kb + t, z0);
-          dw->put_a(1 * H + j, dw->kb + t, z1);
-          dw->put_a(2 * H + j, dw->kb + t, z2);
-          dw->put_a(3 * H + j, dw->kb + t, z3);
-        }
+        dzt[0 * H + j] = di * ig * (1.0f - ig);
+        dzt[1 * H + j] = df * fg * (1.0f - fg);
+        dzt[2 * H + j] = dg * (1.0f - gg * gg);
+        dzt[3 * H + j] = dout * og * (1.0f - og);
       }
       __syncwarp();
       if (t > 0) {  // dh_{t-1} = Whᵀ dz_t (the reference also does this at t=0, unused)
@@ -806,9 +745,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
   if (pr && lane == 0) pr[11] = globaltimer();
 
   // ------- backward pass 2: dWx, dWh, db = Σ_{s,t} dz ⊗ [x_t, h_{t-1}] -------
-  if constexpr (MMADW) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // operands → tensor core (async proxy)
-  } else if (act) {
+  if (act) {
     float dz[SPW][T][4];
 #pragma unroll
     for (int sp = 0; sp < SPW; ++sp)
