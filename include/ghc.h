@@ -215,6 +215,23 @@ ghc_status ghc_transpose(ghc_ctx* ctx, float* d_out, const float* d_in, int32_t 
 ghc_status ghc_sgd_apply(ghc_ctx* ctx, float* d_w, float* d_v, const float* d_g,
                          int64_t p, float lr, float mu, int32_t* d_status,
                          uint64_t* d_version);
+/* sgd_step with the reference's value semantics (optim.cpp:39-65 returns a
+ * new WeightSet / OptimState): reads w, v, g and writes the updated weights
+ * and velocity to w_out, v_out in ONE pass (20 B/param; the in-place
+ * ghc_sgd_apply must see all of g before its first write: two passes).
+ * Non-finite g → *d_status = GHC_ERR_NONFINITE and w_out / v_out hold no
+ * update (the caller keeps w, v — never written); else GHC_OK and
+ * *d_version += 1.  Outputs must not overlap the inputs (GHC_ERR_CONFIG). */
+ghc_status ghc_sgd_step_out(ghc_ctx* ctx, const float* d_w, const float* d_v, const float* d_g,
+                            float* d_w_out, float* d_v_out, int64_t p, float lr, float mu,
+                            int32_t* d_status, uint64_t* d_version);
+/* easgd_worker_step (optim.cpp:82-105) with value semantics, one pass:
+ * w_out = w - lr*g, pulled toward c when batch_index % tau == 0.
+ * Non-finite g → *d_status = GHC_ERR_NONFINITE (w untouched, w_out no update). */
+ghc_status ghc_easgd_worker_step_out(ghc_ctx* ctx, const float* d_w, const float* d_c,
+                                     const float* d_g, float* d_w_out, int64_t p, float lr,
+                                     float alpha, uint64_t tau, uint64_t batch_index,
+                                     int32_t* d_status);
 /* elastic_pull (optim.cpp:67-80): w -= alpha*(w - c). */
 ghc_status ghc_elastic_pull(ghc_ctx* ctx, float* d_w, const float* d_c, int64_t p,
                             float alpha);

@@ -109,6 +109,8 @@ SIGNATURES = [
     ("ghc_sgd_apply", C.c_int, [_vp, _vp, _vp, _vp, _i64, _f32, _f32, _vp, _vp]),
     ("ghc_elastic_pull", C.c_int, [_vp, _vp, _vp, _i64, _f32]),
     ("ghc_easgd_worker_step", C.c_int, [_vp, _vp, _vp, _vp, _i64, _f32, _f32, _u64, _u64, _vp]),
+    ("ghc_sgd_step_out", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _f32, _f32, _vp, _vp]),
+    ("ghc_easgd_worker_step_out", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _f32, _u64, _u64, _vp]),
     ("ghc_easgd_center_step", C.c_int, [_vp, _vp, _vp, _i64, _f32, _vp]),
     ("ghc_weighted_mean", C.c_int, [_vp, _vp, _vp, _vp, _i32, _i64]),
     ("ghc_master_create", C.c_int, [_vp, _vp, _f32, _f32, _vp]),

@@ -282,20 +282,22 @@ std::pair<WeightSet, OptimState> sgd_step(const WeightSet& w, const Gradient& g,
   if (!shape_congruent(w.tensors, s.velocity)) throw ShapeError("sgd_step: velocity shape mismatch");
   const size_t P = DevWeights::count(w.tensors);
   Dev dw = upload_f32(w.tensors), dv = upload_f32(s.velocity), dg = upload_f32(g.tensors), ds(4);
+  Dev dw2(P * 4), dv2(P * 4);  // value semantics: one pass into new buffers
   int32_t st = 0;
   ds.put(&st, 4);
-  check(ghc_sgd_apply(thread_context(), dw.as<float>(), dv.as<float>(), dg.as<float>(),
-                      static_cast<int64_t>(P), static_cast<float>(s.learning_rate),
-                      static_cast<float>(s.momentum), ds.as<int32_t>(), nullptr),
+  check(ghc_sgd_step_out(thread_context(), dw.as<float>(), dv.as<float>(), dg.as<float>(),
+                         dw2.as<float>(), dv2.as<float>(), static_cast<int64_t>(P),
+                         static_cast<float>(s.learning_rate), static_cast<float>(s.momentum),
+                         ds.as<int32_t>(), nullptr),
         "sgd_step");
   ds.get(&st, 4);
   if (st == GHC_ERR_NONFINITE)
     throw NonFiniteGradientError("sgd_step: gradient has NaN/Inf entries; update rejected");
   WeightSet out;
-  out.tensors = from_f32(w.tensors, download(dw, P));
+  out.tensors = from_f32(w.tensors, download(dw2, P));
   out.version = w.version + 1;
   OptimState ns = s;
-  ns.velocity = from_f32(s.velocity, download(dv, P));
+  ns.velocity = from_f32(s.velocity, download(dv2, P));
   return {std::move(out), std::move(ns)};
 }
 
@@ -321,17 +323,19 @@ WeightSet easgd_worker_step(const WeightSet& w, const WeightSet& center, const G
     throw ShapeError("easgd_worker_step: gradient shape does not match weights");
   const size_t P = DevWeights::count(w.tensors);
   Dev dw = upload_f32(w.tensors), dc = upload_f32(center.tensors), dg = upload_f32(g.tensors), ds(4);
+  Dev dw2(P * 4);
   int32_t st = 0;
   ds.put(&st, 4);
-  check(ghc_easgd_worker_step(thread_context(), dw.as<float>(), dc.as<float>(), dg.as<float>(),
-                              static_cast<int64_t>(P), static_cast<float>(s.learning_rate),
-                              static_cast<float>(e.alpha), e.tau, batch_index, ds.as<int32_t>()),
+  check(ghc_easgd_worker_step_out(thread_context(), dw.as<float>(), dc.as<float>(), dg.as<float>(),
+                                  dw2.as<float>(), static_cast<int64_t>(P),
+                                  static_cast<float>(s.learning_rate), static_cast<float>(e.alpha),
+                                  e.tau, batch_index, ds.as<int32_t>()),
         "easgd_worker_step");
   ds.get(&st, 4);
   if (st == GHC_ERR_NONFINITE)
     throw NonFiniteGradientError("easgd_worker_step: gradient has NaN/Inf entries");
   WeightSet out = w;
-  out.tensors = from_f32(w.tensors, download(dw, P));
+  out.tensors = from_f32(w.tensors, download(dw2, P));
   return out;
 }
 

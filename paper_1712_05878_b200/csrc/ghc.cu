@@ -639,6 +639,60 @@ ghc_status ghc_sgd_apply(ghc_ctx* c, float* d_w, float* d_v, const float* d_g, i
   return GHC_OK;
 }
 
+namespace {
+bool overlaps(const void* a, const void* b, int64_t bytes) {
+  const char* x = static_cast<const char*>(a);
+  const char* y = static_cast<const char*>(b);
+  return x < y + bytes && y < x + bytes;
+}
+}  // namespace
+
+ghc_status ghc_sgd_step_out(ghc_ctx* c, const float* d_w, const float* d_v, const float* d_g,
+                            float* d_w_out, float* d_v_out, int64_t P, float lr, float mu,
+                            int32_t* d_status, uint64_t* d_version) {
+  if (ghc_status s = validate_sgd(lr, mu)) return s;
+  if (P < 1) return fail(GHC_ERR_SHAPE, "sgd_step: empty weight set");
+  const int64_t b = 4 * P;
+  if (overlaps(d_w_out, d_w, b) || overlaps(d_w_out, d_v, b) || overlaps(d_w_out, d_g, b) ||
+      overlaps(d_v_out, d_w, b) || overlaps(d_v_out, d_v, b) || overlaps(d_v_out, d_g, b) ||
+      overlaps(d_w_out, d_v_out, b))
+    return fail(GHC_ERR_CONFIG, "sgd_step_out: outputs must not overlap the inputs (use ghc_sgd_apply)");
+  MasterDev* ms = ctx_scratch_ms(c);
+  if (!ms) return fail(GHC_ERR_CUDA, "scratch allocation failed");
+  const int vec = aligned16(d_w) && aligned16(d_v) && aligned16(d_g) && aligned16(d_w_out) &&
+                  aligned16(d_v_out);
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(sgd_out_kernel), 256);
+  sgd_out_kernel<<<grid, 256, 0, c->stream>>>(d_w, d_v, d_g, d_w_out, d_v_out, P, vec, lr, mu, ms,
+                                              d_status,
+                                              reinterpret_cast<unsigned long long*>(d_version));
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
+ghc_status ghc_easgd_worker_step_out(ghc_ctx* c, const float* d_w, const float* d_c,
+                                     const float* d_g, float* d_w_out, int64_t P, float lr,
+                                     float alpha, uint64_t tau, uint64_t batch_index,
+                                     int32_t* d_status) {
+  if (!(lr > 0.0f)) return fail(GHC_ERR_CONFIG, "learning_rate must be > 0");
+  if (ghc_status s = validate_alpha(alpha)) return s;
+  if (tau < 1) return fail(GHC_ERR_CONFIG, "elastic_tau must be >= 1");
+  const int64_t b = 4 * P;
+  if (overlaps(d_w_out, d_w, b) || overlaps(d_w_out, d_c, b) || overlaps(d_w_out, d_g, b))
+    return fail(GHC_ERR_CONFIG,
+                "easgd_worker_step_out: output must not overlap the inputs (use ghc_easgd_worker_step)");
+  MasterDev* ms = ctx_scratch_ms(c);
+  if (!ms) return fail(GHC_ERR_CUDA, "scratch allocation failed");
+  const int vec = aligned16(d_w) && aligned16(d_c) && aligned16(d_g) && aligned16(d_w_out);
+  const int pull = (batch_index % tau) == 0;
+  const int grid = occupancy_grid(c, reinterpret_cast<const void*>(easgd_worker_out_kernel), 256);
+  easgd_worker_out_kernel<<<grid, 256, 0, c->stream>>>(d_w, d_c, d_g, d_w_out, P, vec, lr, alpha, pull,
+                                                       ms, d_status);
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
 ghc_status ghc_elastic_pull(ghc_ctx* c, float* d_w, const float* d_c, int64_t P, float alpha) {
   const int grid = occupancy_grid(c, reinterpret_cast<const void*>(elastic_kernel), 256);
   elastic_kernel<<<grid, 256, 0, c->stream>>>(d_w, d_c, P, aligned16(d_w) && aligned16(d_c), alpha,

@@ -106,28 +106,12 @@ static __global__ void __launch_bounds__(256) sgd_apply_kernel(float* __restrict
   finish_rejecting(ms, rej, status, version, rejected);
 }
 
-// sgd_step for the double-buffered master (optim.cpp:39-65) in ONE pass:
-// read w, v, g of the current buffer, write the new w, v into the other one
-// (20 B/param, the algorithmic minimum); the last CTA out commits by flipping
-// ms->cur (version + 1) or rejects a non-finite gradient whole (optim.cpp:
-// 49-51 — the current buffer was never written).  No grid barrier, no
-// separate finite-check pass.  `flags` holds the cross-CTA bad flag and the
-// arrival counter.
-//
-// det = 1 (the master paths that track the buffer index on the host): the
-// buffers flip on EVERY call; a rejected update leaves flags->flag[1] = 1
-// and db_fixup_kernel (launched right after) copies the old w, v into the new
-// buffers — the rare path pays the copy, the common path stays one pass.
-static __global__ void __launch_bounds__(256) sgd_db_kernel(float* const* __restrict__ wb,
-                                                     float* const* __restrict__ vb,
-                                                     const float* __restrict__ g, long long P,
-                                                     int vec, float lr, float mu, MasterDev* ms,
-                                                     MasterDev* flags, int det = 0) {
-  const int cur = __ldcg(&ms->cur);
-  const float* w = wb[cur];
-  const float* v = vb[cur];
-  float* w2 = wb[cur ^ 1];
-  float* v2 = vb[cur ^ 1];
+// One streaming pass of sgd_step (optim.cpp:59-60) from (w, v, g) into
+// (w2, v2): 20 B/param; returns this thread's "saw a non-finite g" bit.
+__device__ __forceinline__ int sgd_pass(const float* __restrict__ w, const float* __restrict__ v,
+                                        const float* __restrict__ g, float* __restrict__ w2,
+                                        float* __restrict__ v2, long long P, int vec, float lr,
+                                        float mu) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
   const long long n4 = vec ? (P >> 2) : 0;
@@ -155,6 +139,109 @@ static __global__ void __launch_bounds__(256) sgd_db_kernel(float* const* __rest
     v2[i] = vn;
     w2[i] = w[i] + vn;
   }
+  return bad;
+}
+
+// The grid's OR of the per-thread bad bits, seen by the last CTA to arrive
+// (flags->flag[0] / arrive reset for the next launch); returns -1 in every
+// other CTA, else the OR (0 / 1).  No grid barrier.
+__device__ __forceinline__ int last_cta_or(int bad, MasterDev* flags) {
+  bad = __syncthreads_or(bad);
+  int res = -1;
+  if (threadIdx.x == 0) {
+    if (bad) atomicOr(&flags->flag[0], 1);
+    __threadfence();
+    const unsigned prev = atomicAdd(&flags->arrive, 1u);
+    if (prev == gridDim.x - 1) {  // last CTA: every write and flag of the grid is visible
+      __threadfence();
+      res = atomicAdd(&flags->flag[0], 0) ? 1 : 0;
+      flags->flag[0] = 0;
+      flags->arrive = 0;
+    }
+  }
+  return res;
+}
+
+// sgd_step with value semantics (the drop-in's `sgd_step(w, g, s)` returns
+// new weights / state): (w, v, g) → (w2, v2) in one pass, 20 B/param — the
+// in-place form has to see all of g before its first write (two passes).  A
+// non-finite g sets *status = GHC_ERR_NONFINITE (w2, v2 then hold no update;
+// the inputs were never written), else 0 and *version += 1.
+static __global__ void __launch_bounds__(256) sgd_out_kernel(const float* __restrict__ w,
+                                                      const float* __restrict__ v,
+                                                      const float* __restrict__ g,
+                                                      float* __restrict__ w2, float* __restrict__ v2,
+                                                      long long P, int vec, float lr, float mu,
+                                                      MasterDev* flags, int* status,
+                                                      unsigned long long* version) {
+  const int rej = last_cta_or(sgd_pass(w, v, g, w2, v2, P, vec, lr, mu), flags);
+  if (rej >= 0) {
+    if (status) *status = rej ? 2 /*GHC_ERR_NONFINITE*/ : 0;
+    if (version && !rej) *version += 1ull;
+    __threadfence();
+  }
+}
+
+// easgd_worker_step with value semantics: w2 = w − lr·g, pulled toward c on
+// pull rounds (optim.cpp:82-105), one pass (16 B/param on pull rounds).
+static __global__ void __launch_bounds__(256) easgd_worker_out_kernel(
+    const float* __restrict__ w, const float* __restrict__ c, const float* __restrict__ g,
+    float* __restrict__ w2, long long P, int vec, float lr, float alpha, int pull, MasterDev* flags,
+    int* status) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  const long long n4 = vec ? (P >> 2) : 0;
+  int bad = 0;
+  for (long long i = tid; i < n4; i += nth) {
+    const float4 gv = __ldcs(reinterpret_cast<const float4*>(g) + i);
+    float4 wv = __ldcs(reinterpret_cast<const float4*>(w) + i);
+    bad |= !finite4(gv);
+    wv.x -= lr * gv.x;  // optim.cpp:97-98
+    wv.y -= lr * gv.y;
+    wv.z -= lr * gv.z;
+    wv.w -= lr * gv.w;
+    if (pull) {  // optim.cpp:76
+      const float4 cv = __ldcs(reinterpret_cast<const float4*>(c) + i);
+      wv.x -= alpha * (wv.x - cv.x);
+      wv.y -= alpha * (wv.y - cv.y);
+      wv.z -= alpha * (wv.z - cv.z);
+      wv.w -= alpha * (wv.w - cv.w);
+    }
+    __stcs(reinterpret_cast<float4*>(w2) + i, wv);
+  }
+  for (long long i = (n4 << 2) + tid; i < P; i += nth) {
+    const float gi = g[i];
+    bad |= !isfinite(gi);
+    float wv = w[i] - lr * gi;
+    if (pull) wv -= alpha * (wv - c[i]);
+    w2[i] = wv;
+  }
+  const int rej = last_cta_or(bad, flags);
+  if (rej >= 0 && status) {
+    *status = rej ? 2 : 0;
+    __threadfence();
+  }
+}
+
+// sgd_step for the double-buffered master (optim.cpp:39-65) in ONE pass:
+// read w, v, g of the current buffer, write the new w, v into the other one
+// (20 B/param, the algorithmic minimum); the last CTA out commits by flipping
+// ms->cur (version + 1) or rejects a non-finite gradient whole (optim.cpp:
+// 49-51 — the current buffer was never written).  No grid barrier, no
+// separate finite-check pass.  `flags` holds the cross-CTA bad flag and the
+// arrival counter.
+//
+// det = 1 (the master paths that track the buffer index on the host): the
+// buffers flip on EVERY call; a rejected update leaves flags->flag[1] = 1
+// and db_fixup_kernel (launched right after) copies the old w, v into the new
+// buffers — the rare path pays the copy, the common path stays one pass.
+static __global__ void __launch_bounds__(256) sgd_db_kernel(float* const* __restrict__ wb,
+                                                     float* const* __restrict__ vb,
+                                                     const float* __restrict__ g, long long P,
+                                                     int vec, float lr, float mu, MasterDev* ms,
+                                                     MasterDev* flags, int det = 0) {
+  const int cur = __ldcg(&ms->cur);
+  int bad = sgd_pass(wb[cur], vb[cur], g, wb[cur ^ 1], vb[cur ^ 1], P, vec, lr, mu);
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     if (bad) atomicOr(&flags->flag[0], 1);

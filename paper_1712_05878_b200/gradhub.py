@@ -322,12 +322,14 @@ def sgd_step(ctx: Context, w: np.ndarray, g: np.ndarray, s: OptimState):
         raise ShapeError("sgd_step: gradient/velocity shape does not match weights")
     dw = ctx.upload(w); dv = ctx.upload(np.asarray(s.velocity, np.float32))
     dg = ctx.upload(np.asarray(g, np.float32))
+    w2, v2 = ctx.array(w.shape), ctx.array(w.shape)
     st = ctx.upload(np.zeros(1, np.int32))
-    check(ctx.lib.ghc_sgd_apply(ctx.h, dw.ptr, dv.ptr, dg.ptr, w.size, s.learning_rate,
-                                s.momentum, st.ptr, None), "sgd_step")
+    # value semantics → the one-pass out-of-place kernel (ghc_sgd_step_out)
+    check(ctx.lib.ghc_sgd_step_out(ctx.h, dw.ptr, dv.ptr, dg.ptr, w2.ptr, v2.ptr, w.size,
+                                   s.learning_rate, s.momentum, st.ptr, None), "sgd_step")
     if int(st.numpy()[0]) == 2:
         raise NonFiniteGradientError("sgd_step: gradient has NaN/Inf entries; update rejected")
-    return dw.numpy(), OptimState(dv.numpy(), s.learning_rate, s.momentum)
+    return w2.numpy(), OptimState(v2.numpy(), s.learning_rate, s.momentum)
 
 
 def elastic_pull(ctx: Context, w: np.ndarray, center: np.ndarray, alpha: float) -> np.ndarray:
@@ -342,12 +344,13 @@ def easgd_worker_step(ctx: Context, w, center, g, s: OptimState, alpha: float, t
     """easgd_worker_step (optim.cpp:82-105)."""
     dw = ctx.upload(np.asarray(w, np.float32)); dc = ctx.upload(np.asarray(center, np.float32))
     dg = ctx.upload(np.asarray(g, np.float32)); st = ctx.upload(np.zeros(1, np.int32))
-    check(ctx.lib.ghc_easgd_worker_step(ctx.h, dw.ptr, dc.ptr, dg.ptr, dw.shape[0],
-                                        s.learning_rate, alpha, tau, batch_index, st.ptr),
+    w2 = ctx.array(dw.shape)
+    check(ctx.lib.ghc_easgd_worker_step_out(ctx.h, dw.ptr, dc.ptr, dg.ptr, w2.ptr, dw.shape[0],
+                                            s.learning_rate, alpha, tau, batch_index, st.ptr),
           "easgd_worker_step")
     if int(st.numpy()[0]) == 2:
         raise NonFiniteGradientError("easgd_worker_step: gradient has NaN/Inf entries")
-    return dw.numpy()
+    return w2.numpy()
 
 
 def easgd_center_step(ctx: Context, center, worker, alpha: float, version: int = 0):

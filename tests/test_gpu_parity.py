@@ -143,6 +143,59 @@ def test_sgd_rejects_nonfinite_whole_update(ctx, bad):
     assert np.allclose(w2, 0.9)
 
 
+@pytest.mark.parametrize("P", [1, 4097, 1_000_003])
+def test_sgd_in_place_equals_one_pass(ctx, P):
+    """ghc_sgd_apply (in place, check pass + update pass) and ghc_sgd_step_out
+    (value semantics, one pass) give the same bits; a rejected in-place update
+    leaves w, v untouched; overlapping outputs are refused."""
+    rng = np.random.default_rng(P + 1)
+    w, v, gr = (rng.normal(size=P).astype(np.float32) for _ in range(3))
+    lib = ctx.lib
+    dw, dv, dg = ctx.upload(w), ctx.upload(v), ctx.upload(gr)
+    w2, v2, st = ctx.array(P), ctx.array(P), ctx.upload(np.full(1, 7, np.int32))
+    ver = ctx.upload(np.zeros(1, np.uint64))
+    g.gradhub.check(lib.ghc_sgd_step_out(ctx.h, dw.ptr, dv.ptr, dg.ptr, w2.ptr, v2.ptr, P, 0.01, 0.9,
+                                         st.ptr, ver.ptr), "sgd_step_out")
+    assert int(st.numpy()[0]) == 0 and int(ver.numpy()[0]) == 1
+    np.testing.assert_array_equal(dw.numpy(), w)  # inputs untouched
+    g.gradhub.check(lib.ghc_sgd_apply(ctx.h, dw.ptr, dv.ptr, dg.ptr, P, 0.01, 0.9, st.ptr, ver.ptr),
+                    "sgd_apply")
+    assert int(st.numpy()[0]) == 0 and int(ver.numpy()[0]) == 2
+    np.testing.assert_array_equal(dw.numpy(), w2.numpy())
+    np.testing.assert_array_equal(dv.numpy(), v2.numpy())
+    gb = gr.copy(); gb[P // 2] = np.nan
+    dgb = ctx.upload(gb)
+    before_w, before_v = dw.numpy(), dv.numpy()
+    g.gradhub.check(lib.ghc_sgd_apply(ctx.h, dw.ptr, dv.ptr, dgb.ptr, P, 0.01, 0.9, st.ptr, ver.ptr),
+                    "sgd_apply")
+    assert int(st.numpy()[0]) == 2 and int(ver.numpy()[0]) == 2
+    np.testing.assert_array_equal(dw.numpy(), before_w)
+    np.testing.assert_array_equal(dv.numpy(), before_v)
+    g.gradhub.check(lib.ghc_sgd_step_out(ctx.h, dw.ptr, dv.ptr, dgb.ptr, w2.ptr, v2.ptr, P, 0.01, 0.9,
+                                         st.ptr, ver.ptr), "sgd_step_out")
+    assert int(st.numpy()[0]) == 2 and int(ver.numpy()[0]) == 2
+    np.testing.assert_array_equal(dw.numpy(), before_w)
+    with pytest.raises(g.ConfigError):
+        g.gradhub.check(lib.ghc_sgd_step_out(ctx.h, dw.ptr, dv.ptr, dg.ptr, dw.ptr, v2.ptr, P, 0.01, 0.9,
+                                             st.ptr, None), "sgd_step_out")
+
+
+def test_easgd_worker_in_place_equals_one_pass(ctx):
+    P = 300_007
+    rng = np.random.default_rng(5)
+    w, c, gr = (rng.normal(size=P).astype(np.float32) for _ in range(3))
+    lib = ctx.lib
+    for bi in (0, 3):
+        dw, dc, dg = ctx.upload(w), ctx.upload(c), ctx.upload(gr)
+        w2, st = ctx.array(P), ctx.upload(np.full(1, 7, np.int32))
+        g.gradhub.check(lib.ghc_easgd_worker_step_out(ctx.h, dw.ptr, dc.ptr, dg.ptr, w2.ptr, P, 0.05,
+                                                      0.5, 3, bi, st.ptr), "easgd_out")
+        assert int(st.numpy()[0]) == 0
+        g.gradhub.check(lib.ghc_easgd_worker_step(ctx.h, dw.ptr, dc.ptr, dg.ptr, P, 0.05, 0.5, 3, bi,
+                                                  st.ptr), "easgd")
+        np.testing.assert_array_equal(dw.numpy(), w2.numpy())
+
+
 def test_sgd_spec_examples(ctx):
     w, _ = g.sgd_step(ctx, np.array([1.0], np.float32), np.array([2.0], np.float32),
                       g.OptimState(np.zeros(1, np.float32), 0.1, 0.0))

@@ -49,7 +49,7 @@ def main():
                          c=ctx.upload(w0 * 0.5),
                          g=ctx.upload((rng.normal(size=P) * 1e-3).astype(np.float32)),
                          slots=ctx.upload(np.tile((rng.normal(size=P) * 1e-3).astype(np.float32), W)),
-                         out=ctx.array(P)))
+                         out=ctx.array(P), w2=ctx.array(P), v2=ctx.array(P)))
     st = ctx.array(1, np.int32)
     ver = ctx.array(2, np.int32)  # uint64 version
     counts_arr = (C.c_double * W)(*[1000.0 + k for k in range(W)])
@@ -64,6 +64,12 @@ def main():
         ("sgd_apply_kernel", "ghc_sgd_apply (in place)", 20,
          lambda i, s: ck(lib.ghc_sgd_apply(ctx.h, s["w"].ptr, s["v"].ptr, s["g"].ptr, P, 0.01, 0.9,
                                            st.ptr, None))),
+        ("sgd_out_kernel", "ghc_sgd_step_out (value semantics, one pass)", 20,
+         lambda i, s: ck(lib.ghc_sgd_step_out(ctx.h, s["w"].ptr, s["v"].ptr, s["g"].ptr, s["w2"].ptr,
+                                              s["v2"].ptr, P, 0.01, 0.9, st.ptr, None))),
+        ("easgd_worker_out_kernel", "ghc_easgd_worker_step_out, pull round (one pass)", 16,
+         lambda i, s: ck(lib.ghc_easgd_worker_step_out(ctx.h, s["w"].ptr, s["c"].ptr, s["g"].ptr,
+                                                       s["w2"].ptr, P, 0.01, 0.5, 10, 0, st.ptr))),
         ("easgd_worker_kernel", "ghc_easgd_worker_step, pull round (batch_index % tau == 0)", 16,
          lambda i, s: ck(lib.ghc_easgd_worker_step(ctx.h, s["w"].ptr, s["c"].ptr, s["g"].ptr, P, 0.01,
                                                    0.5, 10, 0, st.ptr))),
