@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -81,6 +82,43 @@ ghc_status launch_gemm_tma(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta,
   return GHC_OK;
 }
 
+// CTA-pair kernel (tcgen05 cta_group::2, 256 × 2·NH tiles): large M and N.
+// GHC_GEMM=single keeps the single-CTA kernel (A/B comparisons).
+bool pair_allowed() {
+  static const bool ok = [] {
+    const char* e = std::getenv("GHC_GEMM");
+    return !(e && (std::string(e) == "single" || std::string(e) == "legacy"));
+  }();
+  return ok;
+}
+
+template <int NH>
+ghc_status launch_gemm_pair(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta,
+                            const CUtensorMap& tb) {
+  constexpr int stage = 2 * gemm_detail::BM * gemm_detail::BK * 4 + 2 * NH * gemm_detail::BK * 4;
+  const size_t smem = gemm_detail::kTmaStages * stage;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CU(cudaFuncSetAttribute(tcgen05_gemm_pair_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    attr_set = true;
+  }
+  dim3 grid(2 * ((g.N + 2 * NH - 1) / (2 * NH)), (g.M + 2 * gemm_detail::BM - 1) / (2 * gemm_detail::BM));
+  if (std::getenv("GHC_PAIR_DEBUG")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, tcgen05_gemm_pair_kernel<NH>);
+    int nb = -1;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tcgen05_gemm_pair_kernel<NH>, 320, smem);
+    std::fprintf(stderr, "pair: regs %d maxthr %d static %zu local %zu maxdyn %d occ %d (%s) smem %zu\n", fa.numRegs,
+                 fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxDynamicSharedSizeBytes, nb,
+                 cudaGetErrorString(e), smem);
+  }
+  tcgen05_gemm_pair_kernel<NH><<<grid, 320, smem, c->stream>>>(ta, tb, g);
+  CU(cudaGetLastError());
+  c->launches++;
+  return GHC_OK;
+}
+
 // Narrow outputs with a long K (dX of the N = 20 input layer, K = 4096: only
 // ⌈M/128⌉ = 8 tiles for 148 SMs): split K over ≈ one wave of CTAs into
 // per-split partials, then one deterministic combine + epilogue pass.
@@ -142,6 +180,9 @@ ghc_status gemm_nt_ct(ghc_ctx* c, const float* d_a, const float* d_b, float* d_c
     }
   }
   CUtensorMap ta, tb;
+  if (pair_allowed() && M >= 256 && N >= 256 && K >= 4 * gemm_detail::BK &&
+      make_map(&ta, d_a, M, K, lda, gemm_detail::BM) && make_map(&tb, d_b, N, K, ldb, 128))
+    return launch_gemm_pair<128>(c, g, ta, tb);
   if (tma_allowed() && make_map(&ta, d_a, M, K, lda, gemm_detail::BM) &&
       make_map(&tb, d_b, N, K, ldb, bn)) {
     const long long tiles = static_cast<long long>((M + gemm_detail::BM - 1) / gemm_detail::BM) *

@@ -524,6 +524,259 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of 2 CTAs on the two SMs
+// of a TPC computes one 256 × NP tile.  CTA r holds A rows m0 + 128r.. and B
+// rows (= C columns) n0 + r·NH.. (NH = NP/2) in its own shared memory; the
+// leader (r = 0) issues `tcgen05.mma.cta_group::2` with M = 256, N = NP, which
+// reads each CTA's halves from its own SM — per SM, one MMA covers 128 × NP
+// outputs for the operand bytes of 128 × NH: half the shared-memory reads per
+// output of the single-CTA kernel (whose 3×TF32 stage is bound by the smem
+// port).  Accumulators: CTA r's TMEM holds its 128 rows × NP.
+// Barriers: each CTA's TMA completes its own `full`; every worker warp of
+// both CTAs arrives on the leader's `split` (count 16, mapa'd address); the
+// leader's commits arrive on `empty` / accumulator barriers of both CTAs
+// (multicast).
+namespace gemm_detail {
+__host__ __device__ constexpr uint32_t make_idesc_m(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {  // → the same barrier in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {  // arrive on CTA 0's copy
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned phase) {
+  for (long long spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (spin > (1ll << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+}  // namespace gemm_detail
+
+// Accuracy: the tensor core's fp32 accumulation truncates (error ∝ adds per
+// accumulator).  Two 256-column TMEM accumulators alternate
+// over segments of DS K-blocks; the 8 worker warps drain a finished segment
+// into fp32 registers (round-to-nearest FADD; 128 columns × 1 row per
+// thread) S K-blocks after it ends, while the tensor core fills the other.
+// Warps: 0 TMA producer, 1 MMA issuer (leader CTA), 2..9 split + drain +
+// epilogue (TMEM lane quarter = warp % 4, column half = (warp − 2) / 4).
+template <int NH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    tcgen05_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                             const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+  using namespace gemm_detail;
+  constexpr int NP = 2 * NH;  // the pair's N (MMA N ≤ 256, multiple of 16)
+  static_assert(NP == 256, "pair N tile: two 256-column accumulators fill TMEM");
+  constexpr int S = kTmaStages;
+  constexpr int DS = 16;      // K-blocks per accumulator segment (≤ 192 adds per accumulator)
+  static_assert(DS > S, "a segment is drained S K-blocks after it ends, before its accumulator is reused");
+  constexpr int A_BYTES = BM * BK * 4;
+  constexpr int B_BYTES = NH * BK * 4;
+  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi | A_lo | B_hi | B_lo (this CTA's halves)
+  constexpr int TCOLS = 512;
+  constexpr int NW = 256;  // worker threads
+  extern __shared__ __align__(1024) uint8_t gsm[];
+  __shared__ uint64_t full[S], split[S], empty[S], accfull[2], accempty[2];
+  __shared__ uint32_t tmem_base_s;
+
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * 2 * BM + static_cast<int>(rank) * BM;  // this CTA's A / C rows
+  const int n0 = (blockIdx.x >> 1) * NP;                             // the pair's C columns
+  const int nb0 = n0 + static_cast<int>(rank) * NH;                  // this CTA's B rows
+  const int nkb = (g.K + BK - 1) / BK;
+  const int nseg = (nkb + DS - 1) / DS;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 16);  // one arrival per worker warp of both CTAs
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&accfull[a], 1);
+      mbar_init(&accempty[a], 16);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (each CTA: its own halves) ----------------
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        if (kb >= S) mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+        uint8_t* st = gsm + s * STAGE;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+#pragma unroll
+        for (int c = 0; c < BK / 4; ++c) {
+          tma_load_2d(st + c * BM * 16, &tmA, kb * BK + 4 * c, m0, &full[s]);
+          tma_load_2d(st + 2 * A_BYTES + c * NH * 16, &tmB, kb * BK + 4 * c, nb0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA) ----------------
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_m(2 * BM, NP);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % S;
+        const int seg = kb / DS, acc = seg & 1;
+        const bool first = kb % DS == 0, last = kb % DS == DS - 1 || kb == nkb - 1;
+        if (first && seg >= 2) mbar_wait(&accempty[acc], ((seg >> 1) - 1) & 1);  // drained
+        mbar_wait(&split[s], (kb / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_hi = smem_u32(gsm + s * STAGE), a_lo = a_hi + A_BYTES;
+        const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * NP);
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t ao = ks * 2 * BM * 16, bo = ks * 2 * NH * 16;
+          const uint64_t dah = make_desc(a_hi + ao, BM * 16, 128);
+          const uint64_t dal = make_desc(a_lo + ao, BM * 16, 128);
+          const uint64_t dbh = make_desc(b_hi + bo, NH * 16, 128);
+          const uint64_t dbl = make_desc(b_lo + bo, NH * 16, 128);
+          const uint32_t acc0 = (first && ks == 0) ? 0u : 1u;
+          umma_tf32_pair(d, dal, dbh, idesc, acc0);  // lo·hi (small terms first)
+          umma_tf32_pair(d, dah, dbl, idesc, 1u);    // hi·lo
+          umma_tf32_pair(d, dah, dbh, idesc, 1u);    // hi·hi
+        }
+        commit_pair(&empty[s]);
+        if (last) commit_pair(&accfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- workers: split, drain, epilogue ----------------
+    const int t = tid - 64;
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    float sum[128];
+#pragma unroll
+    for (int i = 0; i < 128; ++i) sum[i] = 0.f;
+    auto drain = [&](int seg) {
+      const int acc = seg & 1;
+      mbar_wait(&accfull[acc], (seg >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t v[16];
+        tmem_ld<16>(v, tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * NP + h * 128 + c * 16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sum[c * 16 + i] += __uint_as_float(v[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) arrive_leader(&accempty[acc]);
+    };
+    int drained = 0;
+    for (int kb = 0;; ++kb) {
+      if (kb < nkb) {
+        const int s = kb % S;
+        mbar_wait(&full[s], (kb / S) & 1);
+        uint8_t* st = gsm + s * STAGE;
+        auto split_tile = [&](const uint8_t* hi, uint8_t* lo, int bytes) {
+#pragma unroll 2
+          for (int i = t; i < bytes / 16; i += NW) {
+            const uint4 x = reinterpret_cast<const uint4*>(hi)[i];
+            float4 l;
+            l.x = __uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u);
+            l.y = __uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u);
+            l.z = __uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u);
+            l.w = __uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u);
+            reinterpret_cast<float4*>(lo)[i] = l;
+          }
+        };
+        split_tile(st, st + A_BYTES, A_BYTES);
+        split_tile(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES, B_BYTES);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores → tensor core
+        __syncwarp();
+        if (lane == 0) arrive_leader(&split[s]);
+      } else if (drained >= nseg) {
+        break;
+      }
+      // a segment is drained S K-blocks after its last one was split (one
+      // call site: the 128 running sums stay in registers)
+      if (drained < nseg && (kb >= nkb || min(nkb, (drained + 1) * DS) - 1 + S <= kb)) drain(drained++);
+    }
+    // ---------------- epilogue from registers ----------------
+    const int row = m0 + q * 32 + lane;
+    const int cb = n0 + h * 128;
+    if (row < g.M) {
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        const int col = cb + i;
+        float o = sum[i];
+        if (col < g.N) {
+          if (g.epi == EPI_BIAS_ACT) o = act_f(o + __ldg(g.bias + col), g.act);
+          else if (g.epi == EPI_DACT) o *= dact_from_y(__ldg(g.Y + (long long)row * g.ldy + col), g.act);
+          else o *= g.alpha;
+        }
+        sum[i] = o;
+      }
+      float* crow = g.C + (long long)row * g.ldc + cb;
+      const bool vec = (g.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15u) == 0);
+      if (vec && cb + 128 <= g.N) {
+#pragma unroll
+        for (int i = 0; i < 128; i += 4)
+          reinterpret_cast<float4*>(crow)[i / 4] = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (cb + i < g.N) crow[i] = sum[i];
+      }
+      if (g.CT) {  // lanes = consecutive rows → each store is one coalesced 128-B line
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (cb + i < g.N) g.CT[(long long)(cb + i) * g.ldct + row] = sum[i];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // no CTA frees TMEM / leaves while its peer's MMAs or arrivals are in flight
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+}
+
 // Split-K combine: C = epilogue(Σ_z part[z]) in z order (deterministic),
 // with the same epilogues as the GEMM kernels.
 static __global__ void splitk_reduce_kernel(const float* __restrict__ part, int nz, GemmArgs g) {
