@@ -92,28 +92,34 @@ bool pair_allowed() {
   return ok;
 }
 
+#ifndef GHC_PAIR_BK
+#define GHC_PAIR_BK 16
+#endif
+constexpr int kPairBK = GHC_PAIR_BK;                  // K elements per stage
+constexpr int kPairStages = 96 / kPairBK;             // 6 × 32 KB (BK 16) or 3 × 64 KB (BK 32)
 template <int NH>
 ghc_status launch_gemm_pair(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta,
                             const CUtensorMap& tb) {
-  constexpr int stage = 2 * gemm_detail::BM * gemm_detail::BK * 4 + 2 * NH * gemm_detail::BK * 4;
-  const size_t smem = gemm_detail::kTmaStages * stage;
+  constexpr int BKP = kPairBK, SP = kPairStages;
+  constexpr int stage = 2 * gemm_detail::BM * BKP * 4 + 2 * NH * BKP * 4;
+  const size_t smem = SP * stage;
   static bool attr_set = false;
   if (!attr_set) {
-    CU(cudaFuncSetAttribute(tcgen05_gemm_pair_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(tcgen05_gemm_pair_kernel<NH, BKP, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)));
     attr_set = true;
   }
   dim3 grid(2 * ((g.N + 2 * NH - 1) / (2 * NH)), (g.M + 2 * gemm_detail::BM - 1) / (2 * gemm_detail::BM));
   if (std::getenv("GHC_PAIR_DEBUG")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, tcgen05_gemm_pair_kernel<NH>);
+    cudaFuncGetAttributes(&fa, tcgen05_gemm_pair_kernel<NH, BKP, SP>);
     int nb = -1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tcgen05_gemm_pair_kernel<NH>, 320, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tcgen05_gemm_pair_kernel<NH, BKP, SP>, 320, smem);
     std::fprintf(stderr, "pair: regs %d maxthr %d static %zu local %zu maxdyn %d occ %d (%s) smem %zu\n", fa.numRegs,
                  fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxDynamicSharedSizeBytes, nb,
                  cudaGetErrorString(e), smem);
   }
-  tcgen05_gemm_pair_kernel<NH><<<grid, 320, smem, c->stream>>>(ta, tb, g);
+  tcgen05_gemm_pair_kernel<NH, BKP, SP><<<grid, 320, smem, c->stream>>>(ta, tb, g);
   CU(cudaGetLastError());
   c->launches++;
   return GHC_OK;

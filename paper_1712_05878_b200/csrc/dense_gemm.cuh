@@ -588,18 +588,18 @@ __device__ __forceinline__ void cluster_sync_all() {
 // thread) S K-blocks after it ends, while the tensor core fills the other.
 // Warps: 0 TMA producer, 1 MMA issuer (leader CTA), 2..9 split + drain +
 // epilogue (TMEM lane quarter = warp % 4, column half = (warp − 2) / 4).
-template <int NH>
+template <int NH, int BKP, int SP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     tcgen05_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
   using namespace gemm_detail;
   constexpr int NP = 2 * NH;  // the pair's N (MMA N ≤ 256, multiple of 16)
   static_assert(NP == 256, "pair N tile: two 256-column accumulators fill TMEM");
-  constexpr int S = kTmaStages;
-  constexpr int DS = 16;      // K-blocks per accumulator segment (≤ 192 adds per accumulator)
+  constexpr int S = SP;
+  constexpr int DS = 512 / BKP;  // K-blocks per accumulator segment (K = 512: ≤ 192 adds per accumulator)
   static_assert(DS > S, "a segment is drained S K-blocks after it ends, before its accumulator is reused");
-  constexpr int A_BYTES = BM * BK * 4;
-  constexpr int B_BYTES = NH * BK * 4;
+  constexpr int A_BYTES = BM * BKP * 4;
+  constexpr int B_BYTES = NH * BKP * 4;
   constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi | A_lo | B_hi | B_lo (this CTA's halves)
   constexpr int TCOLS = 512;
   constexpr int NW = 256;  // worker threads
@@ -613,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int m0 = blockIdx.y * 2 * BM + static_cast<int>(rank) * BM;  // this CTA's A / C rows
   const int n0 = (blockIdx.x >> 1) * NP;                             // the pair's C columns
   const int nb0 = n0 + static_cast<int>(rank) * NH;                  // this CTA's B rows
-  const int nkb = (g.K + BK - 1) / BK;
+  const int nkb = (g.K + BKP - 1) / BKP;
   const int nseg = (nkb + DS - 1) / DS;
 
   if (warp == 1) {
@@ -650,9 +650,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         uint8_t* st = gsm + s * STAGE;
         mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
 #pragma unroll
-        for (int c = 0; c < BK / 4; ++c) {
-          tma_load_2d(st + c * BM * 16, &tmA, kb * BK + 4 * c, m0, &full[s]);
-          tma_load_2d(st + 2 * A_BYTES + c * NH * 16, &tmB, kb * BK + 4 * c, nb0, &full[s]);
+        for (int c = 0; c < BKP / 4; ++c) {
+          tma_load_2d(st + c * BM * 16, &tmA, kb * BKP + 4 * c, m0, &full[s]);
+          tma_load_2d(st + 2 * A_BYTES + c * NH * 16, &tmB, kb * BKP + 4 * c, nb0, &full[s]);
         }
       }
     }
@@ -671,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
         const uint32_t d = tmem + static_cast<uint32_t>(acc * NP);
 #pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
+        for (int ks = 0; ks < BKP / 8; ++ks) {
           const uint32_t ao = ks * 2 * BM * 16, bo = ks * 2 * NH * 16;
           const uint64_t dah = make_desc(a_hi + ao, BM * 16, 128);
           const uint64_t dal = make_desc(a_lo + ao, BM * 16, 128);
@@ -738,36 +738,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       // call site: the 128 running sums stay in registers)
       if (drained < nseg && (kb >= nkb || min(nkb, (drained + 1) * DS) - 1 + S <= kb)) drain(drained++);
     }
-    // ---------------- epilogue from registers ----------------
-    const int row = m0 + q * 32 + lane;
-    const int cb = n0 + h * 128;
-    if (row < g.M) {
+    // ---------------- epilogue through shared memory ----------------
+    // (the stages are idle: every TMA load was consumed and the last
+    // accumulator commit tracked every MMA).  Sums → smem [128][257], then
+    // warps sweep rows with lanes along columns: coalesced C / Y / bias
+    // accesses and one loop body (instead of 128 unrolled epilogues).
+    constexpr int LD = NP + 1;
+    float* tile = reinterpret_cast<float*>(gsm);
+    {
+      const int r = q * 32 + lane;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        const int col = cb + i;
-        float o = sum[i];
-        if (col < g.N) {
-          if (g.epi == EPI_BIAS_ACT) o = act_f(o + __ldg(g.bias + col), g.act);
-          else if (g.epi == EPI_DACT) o *= dact_from_y(__ldg(g.Y + (long long)row * g.ldy + col), g.act);
-          else o *= g.alpha;
+      for (int i = 0; i < 128; ++i) tile[r * LD + h * 128 + i] = sum[i];
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int wk = t >> 5;  // worker warp 0..7
+#pragma unroll 1
+    for (int r = wk; r < BM; r += 8) {
+      const int row = m0 + r;
+      if (row >= g.M) break;
+#pragma unroll 1
+      for (int c = lane; c < NP; c += 32) {
+        const int col = n0 + c;
+        if (col >= g.N) break;
+        float o = tile[r * LD + c];
+        if (g.epi == EPI_BIAS_ACT) o = act_f(o + __ldg(g.bias + col), g.act);
+        else if (g.epi == EPI_DACT) o *= dact_from_y(__ldg(g.Y + (long long)row * g.ldy + col), g.act);
+        else o *= g.alpha;
+        g.C[(long long)row * g.ldc + col] = o;
+        tile[r * LD + c] = o;
+      }
+    }
+    if (g.CT) {  // transposed copy: lanes along rows → coalesced CT rows
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll 1
+      for (int c = wk; c < NP; c += 8) {
+        const int col = n0 + c;
+        if (col >= g.N) break;
+#pragma unroll 1
+        for (int r = lane; r < BM; r += 32) {
+          const int row = m0 + r;
+          if (row < g.M) g.CT[(long long)col * g.ldct + row] = tile[r * LD + c];
         }
-        sum[i] = o;
-      }
-      float* crow = g.C + (long long)row * g.ldc + cb;
-      const bool vec = (g.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15u) == 0);
-      if (vec && cb + 128 <= g.N) {
-#pragma unroll
-        for (int i = 0; i < 128; i += 4)
-          reinterpret_cast<float4*>(crow)[i / 4] = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (cb + i < g.N) crow[i] = sum[i];
-      }
-      if (g.CT) {  // lanes = consecutive rows → each store is one coalesced 128-B line
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (cb + i < g.N) g.CT[(long long)(cb + i) * g.ldct + row] = sum[i];
       }
     }
   }
