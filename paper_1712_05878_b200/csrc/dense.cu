@@ -110,15 +110,6 @@ ghc_status launch_gemm_pair(ghc_ctx* c, const GemmArgs& g, const CUtensorMap& ta
     attr_set = true;
   }
   dim3 grid(2 * ((g.N + 2 * NH - 1) / (2 * NH)), (g.M + 2 * gemm_detail::BM - 1) / (2 * gemm_detail::BM));
-  if (std::getenv("GHC_PAIR_DEBUG")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, tcgen05_gemm_pair_kernel<NH, BKP, SP>);
-    int nb = -1;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tcgen05_gemm_pair_kernel<NH, BKP, SP>, 320, smem);
-    std::fprintf(stderr, "pair: regs %d maxthr %d static %zu local %zu maxdyn %d occ %d (%s) smem %zu\n", fa.numRegs,
-                 fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxDynamicSharedSizeBytes, nb,
-                 cudaGetErrorString(e), smem);
-  }
   tcgen05_gemm_pair_kernel<NH, BKP, SP><<<grid, 320, smem, c->stream>>>(ta, tb, g);
   CU(cudaGetLastError());
   c->launches++;

@@ -788,11 +788,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
 
   if (RES && blockIdx.x == 0 && threadIdx.x == 0) a.res->ctas = gridDim.x;
   unsigned long long pk[8];  // thread 0: the next command's slot, loaded during the last round
+  unsigned long long* prl = nullptr;  // probe row of the last round run (resident: segment-boundary probes)
   for (;;) {  // segments
   if constexpr (RES) {
     ResidentCmd cmd;
     const bool have = s_has_next != 0;
     if (!resident_next(a.res, ++seq, cmd, have, s_next)) break;
+    if (prl && threadIdx.x == 0) prl[15] = globaltimer();  // next command in hand
     sx = cmd.x;
     sy = cmd.y;
     sidx = cmd.idx;
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     }
     const float scale = sgd ? 1.0f / (float)ntot : a.grad_scale;
     unsigned long long* pr =
-        a.probe ? a.probe + ((long long)r * gridDim.x + blockIdx.x) * 16 : nullptr;
+        a.probe ? a.probe + ((long long)(RES ? (long long)rg : r) * gridDim.x + blockIdx.x) * 16 : nullptr;
     if (pr && threadIdx.x == 0) pr[0] = globaltimer();
 
     // ---- samples ----
@@ -861,19 +863,16 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
         cp_async_commit();
       } else if (RES) {
         // last round of a resident command.  The next command's slot was
-        // loaded during the previous command's last round (pk2, no wait): if
-        // it is valid now its first batch is fetched right away, a whole
-        // round ahead (host-memory batches need it).  Otherwise load the slot
-        // now and check it after the samples (then the fetch overlaps the
-        // exchange only).  Either way load the slot after next for the
-        // following command.
+        // loaded at the end of the previous command (pk2, no wait): if it is
+        // valid now its first batch is fetched right away, a whole round
+        // ahead (host-memory batches need it).  Otherwise load the slot now
+        // and check it after the samples (then the fetch overlaps the
+        // exchange only).
         if (threadIdx.x == 0) {
           ResidentCmd nc;
           s_early = (pk2_seq == seq + 1 && slot_valid(pk2, seq + 1, nc) && nc.op == 0 && nc.rounds > 0) ? 1 : 0;
           if (s_early) s_next = nc;
           else issue_slot_loads(a.res, seq + 1, pk);
-          issue_slot_loads(a.res, seq + 2, pk2);
-          pk2_seq = seq + 2;
         }
         __syncthreads();
         if (s_early && fixed_n) {
@@ -958,11 +957,21 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     // (the CTA partial — Σ warp partials, warp order — is formed by ClusterRS (a))
     if (pr && threadIdx.x == 0) pr[3] = globaltimer();
     rs.exchange(a, r, rg, sloss, wpart, NW, N::PPAD, wa, wb, pr, ntot);
+    prl = pr;
   }
   if constexpr (!RES) {
     break;
   } else {
     resident_done(a.res, sloss != nullptr && rs.s0 <= N::P && N::P < rs.s1);
+    if (prl && threadIdx.x == 0) prl[14] = globaltimer();  // completion arrival issued
+    // the slot after next, loaded as late as possible (a host queueing a few
+    // commands ahead has filled it by now; after the arrival, whose release
+    // would otherwise wait for these loads) and checked at the start of the
+    // next command's last round
+    if (threadIdx.x == 0) {
+      issue_slot_loads(a.res, seq + 2, pk2);
+      pk2_seq = seq + 2;
+    }
   }
   }  // segments
 

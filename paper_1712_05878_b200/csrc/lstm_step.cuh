@@ -152,13 +152,11 @@ __device__ __forceinline__ bool slot_valid(const unsigned long long (&v)[8], uns
 
 // Next command for this CTA (all threads return the same command; false on
 // STOP).  `have`: this CTA already holds it (peeked during the last round).
-static __device__ __noinline__ bool resident_next(ResidentCtl* c, unsigned long long seq, ResidentCmd& out,
-                                                  bool have, const ResidentCmd& peeked) {
+static __device__ __noinline__ bool resident_wait_cmd(ResidentCtl* c, unsigned long long seq,
+                                                      ResidentCmd& out) {
   __shared__ ResidentCmd s_cmd;
   if (threadIdx.x == 0) {
-    if (have) {
-      s_cmd = peeked;
-    } else {
+    {
       const unsigned long long t0 = res_now();
       for (unsigned it = 0;; ++it) {
         unsigned long long v[8];
@@ -202,6 +200,18 @@ static __device__ __noinline__ bool resident_next(ResidentCtl* c, unsigned long 
   out = s_cmd;
   __syncthreads();
   return out.op == 0;
+}
+// Fast path inline: the command was peeked during the last round (shared
+// memory, behind a CTA barrier) — no barrier and no call (a call would make
+// thread 0 wait for its in-flight slot loads to save their registers).
+static __device__ __forceinline__ bool resident_next(ResidentCtl* c, unsigned long long seq, ResidentCmd& out,
+                                                     bool have, const ResidentCmd& peeked) {
+  if (have) {
+    out = peeked;
+    if (threadIdx.x == 0) atomicMax(&c->tlog[seq % 64][0], res_now());
+    return out.op == 0;
+  }
+  return resident_wait_cmd(c, seq, out);
 }
 
 // The segment of command `seq` is complete on this CTA (its last exchange

@@ -75,6 +75,36 @@ def test_gemm_splitk_epilogues(ctx, act):
     assert np.max(np.abs(gemm(ctx, A, B, alpha=0.25) - 0.25 * D)) <= 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (300, 260, 77), (1000, 4096, 4100), (513, 700, 1000)])
+def test_gemm_pair_shapes(ctx, M, N, K):
+    """CTA-pair kernel (M, N ≥ 256): ragged M / N / K edges (TMA zero-fill),
+    several accumulator segments (K > 512), and repeat → same bits."""
+    rng = np.random.default_rng(M + N + K)
+    A = rng.normal(size=(M, K)).astype(np.float32)
+    B = rng.normal(size=(N, K)).astype(np.float32)
+    Cg = gemm(ctx, A, B)
+    Cr = A.astype(np.float64) @ B.astype(np.float64).T
+    assert np.linalg.norm(Cg - Cr) / np.linalg.norm(Cr) <= 1e-5
+    assert np.array_equal(Cg, gemm(ctx, A, B))
+
+
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_gemm_pair_epilogues(ctx, act):
+    rng = np.random.default_rng(20 + act)
+    M, N, K = 520, 384, 640
+    A = rng.normal(size=(M, K)).astype(np.float32) * 0.05
+    B = rng.normal(size=(N, K)).astype(np.float32) * 0.05
+    bias = rng.normal(size=N)
+    D = A.astype(np.float64) @ B.astype(np.float64).T
+    Z = D + bias
+    ref = np.tanh(Z) if act == 0 else (np.maximum(Z, 0) if act == 1 else Z)
+    assert np.max(np.abs(gemm(ctx, A, B, epi=1, act=act, bias=bias) - ref)) <= 1e-5
+    Y = ref.astype(np.float32)
+    d = (1 - Y.astype(np.float64) ** 2) if act == 0 else ((Y > 0) * 1.0 if act == 1 else 1.0)
+    assert np.max(np.abs(gemm(ctx, A, B, epi=2, act=act, Y=Y) - D * d)) <= 1e-5
+    assert np.max(np.abs(gemm(ctx, A, B, alpha=0.25) - 0.25 * D)) <= 1e-5
+
+
 def test_transpose(ctx):
     x = np.random.default_rng(0).normal(size=(1000, 77)).astype(np.float32)
     dx = ctx.upload(x)
