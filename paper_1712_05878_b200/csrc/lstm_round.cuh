@@ -107,6 +107,11 @@ struct ClusterRS {
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
     return w;
   }
+  // four consecutive tagged elements (32-B aligned): two 16-B loads
+  __device__ static void ld_tag4(const unsigned long long* p, unsigned long long (&w)[4]) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w[0]), "=l"(w[1]) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w[2]), "=l"(w[3]) : "l"(p + 2) : "memory");
+  }
 
   // smem: recv (2·CS·SL floats), vsub / vnew / wnew (SL each), badr (8·CS ints), 4 mbarriers
   static constexpr int smem_floats() { return 2 * CS * SL + 3 * SL + 8 * CS + 8; }
@@ -315,18 +320,27 @@ struct ClusterRS {
     // (d) gather slice j of the new weights, OR the flags, push to the cluster
     int sbad = 0;
     for (int k = 4 * threadIdx.x; k < SL; k += 4 * blockDim.x) {
-      unsigned long long v[4];
-      bool ok;
-      long long spin = 0;
-      do {
-        if (++spin > (1ll << 26)) __trap();
-        ok = true;
+      // two polls in flight (the second issued before the first is checked):
+      // a value that lands is seen ≈ half an L2 round trip sooner
+      unsigned long long v[4], u[4];
+      auto ready = [&](const unsigned long long (&x)[4]) {
+        bool ok = true;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          v[i] = ld_tag(tw + e0 + k + i);
-          ok &= ((unsigned)(v[i] >> 32) | 1u) == (tag | 1u);
+        for (int i = 0; i < 4; ++i) ok &= ((unsigned)(x[i] >> 32) | 1u) == (tag | 1u);
+        return ok;
+      };
+      ld_tag4(tw + e0 + k, v);
+      for (long long spin = 0;; ++spin) {
+        if (spin > (1ll << 26)) __trap();
+        ld_tag4(tw + e0 + k, u);
+        if (ready(v)) break;
+        ld_tag4(tw + e0 + k, v);
+        if (ready(u)) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = u[i];
+          break;
         }
-      } while (!ok);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) sbad |= (int)((v[i] >> 32) & 1u);
       const float4 w4 = make_float4(__uint_as_float((unsigned)v[0]), __uint_as_float((unsigned)v[1]),
