@@ -17,7 +17,11 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_build")
+# --checked (or GHC_CHECKED=1): the bounds-checked variant (-DGHC_CHECKED,
+# ghc_device.cuh GHC_CHECK) into _build_checked/; load it with
+# GHC_LIB_PATH=paper_1712_05878_b200/_build_checked/libghc.so
+CHECKED = "--checked" in sys.argv or os.environ.get("GHC_CHECKED") == "1"
+OUT_DIR = os.path.join(HERE, "_build_checked" if CHECKED else "_build")
 OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libghc.so")
 
@@ -32,7 +36,7 @@ NVCC_FLAGS = [
     "-ccbin", "/usr/bin/g++",
     # lstm_samples<…, BWD=false> returns before the backward loops (if constexpr)
     "-diag-suppress", "128",
-]
+] + (["-DGHC_CHECKED"] if CHECKED else [])
 
 
 def sources():

@@ -25,6 +25,8 @@
 
 #include <cstdint>
 
+#include "ghc_device.cuh"  // GHC_CHECK
+
 namespace ghc {
 
 enum GemmEpi : int {
@@ -745,6 +747,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     // accesses and one loop body (instead of 128 unrolled epilogues).
     constexpr int LD = NP + 1;
     float* tile = reinterpret_cast<float*>(gsm);
+#ifdef GHC_CHECKED
+    {
+      unsigned dyn;
+      asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+      GHC_CHECK(BM * LD * 4 <= dyn && S * STAGE <= dyn);
+    }
+#endif
     {
       const int r = q * 32 + lane;
 #pragma unroll

@@ -7,6 +7,32 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+
+// Checked build (build.py --checked → _build_checked/libghc.so, -DGHC_CHECKED):
+// the index arithmetic of every shared-memory region and tagged L2 row is
+// asserted at its use — an access past its own region (into a neighbouring
+// buffer of the same CTA, which the hardware cannot flag) traps with the
+// source line instead of corrupting state.  The sanitizer stand-in on a pool
+// where compute-sanitizer is closed; the product build
+// compiles the checks away.
+#ifdef GHC_CHECKED
+#define GHC_CHECK(c)                                                                             \
+  do {                                                                                           \
+    if (!(c)) {                                                                                  \
+      printf("GHC_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c,       \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define GHC_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
+// [p, p + n) lies inside [base, base + size)   (element pointers of one type)
+#define GHC_CHECK_RANGE(p, n, base, size) \
+  GHC_CHECK((p) >= (base) && (p) + (n) <= (base) + (size))
 
 namespace ghc {
 

@@ -136,6 +136,9 @@ struct ClusterRS {
     SS = (((SL + NCr - 1) / NCr) + 3) & ~3;
     s0 = e0 + cl * SS;
     s1 = min(min(e0 + SL, E), s0 + SS);
+    GHC_CHECK(crank < CS && cid < NC && vrank < max(1, a.VR) && cl < NCr && SL % 4 == 0);
+    GHC_CHECK(s1 <= s0 || (s0 >= e0 && s1 <= e0 + SL && s1 - s0 <= SL && s1 <= EP));
+    GHC_CHECK(a.GX <= 1 || rank < GX);
     epoch = __ldcg(a.bar);
     xepoch = GX > 1 ? __ldcg(a.gcnt[rank] + CS * kFlagStride) : 0u;
     accepted = rejected = acc_samples = 0;
@@ -187,6 +190,7 @@ struct ClusterRS {
   // GPUs), then poll this rank's copy of the GX rows and sum in rank order.
   __device__ float cross_rank_sum(const StepArgs& a, int par, int e, float mine, unsigned tag) const {
     const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(mine);
+    GHC_CHECK(GX <= kMaxRanks && rank < GX && e < EP);
     for (int q = 0; q < GX; ++q) {
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.gpart[q]) +
                                 ((long long)par * GX + rank) * EP + e;
@@ -244,6 +248,7 @@ struct ClusterRS {
       const int e = q * SL + k;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (e < E) {
+        GHC_CHECK_RANGE(wparts + (long long)(nw - 1) * pstride + e, 4, wparts, (long long)nw * pstride);
         v = reinterpret_cast<const float4*>(wparts + e)[0];
         for (int w = 1; w < nw; ++w) {
           const float4 u = reinterpret_cast<const float4*>(wparts + (long long)w * pstride + e)[0];
@@ -253,6 +258,7 @@ struct ClusterRS {
           v.w += u.w;
         }
       }
+      GHC_CHECK_RANGE(recv + (mb * CS + crank) * SL + k, 4, recv, 2 * CS * SL);
       st_async(mapa(recv + (mb * CS + crank) * SL + k, q), v, mapa(mbp + mb, q));
     }
     wait(mbp + mb, ph);
@@ -263,6 +269,7 @@ struct ClusterRS {
       float t = 0.0f;
 #pragma unroll
       for (int q = 0; q < CS; ++q) t += recv[(mb * CS + q) * SL + k];
+      GHC_CHECK(e0 + k < EP && cid < NC);
       st_tag(rows + (long long)cid * EP + e0 + k, t, tag);
     }
     if (pr && threadIdx.x == 0) pr[5] = globaltimer();
@@ -273,6 +280,7 @@ struct ClusterRS {
     unsigned long long* tw = a.tw + ((long long)vrank * 2 + par) * EP;
     const unsigned long long* myrows = rows + (long long)vrank * NCr * EP;
     for (int e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
+      GHC_CHECK(e < EP && e - s0 < SL && vrank * NCr + NCr <= NC);
       float t = 0.0f;
       for (int c0 = 0; c0 < NCr; c0 += kRowBatch) {
         unsigned long long v[kRowBatch];
@@ -320,6 +328,7 @@ struct ClusterRS {
     // (d) gather slice j of the new weights, OR the flags, push to the cluster
     int sbad = 0;
     for (int k = 4 * threadIdx.x; k < SL; k += 4 * blockDim.x) {
+      GHC_CHECK(e0 + k + 4 <= EP);
       // two polls in flight (the second issued before the first is checked):
       // a value that lands is seen ≈ half an L2 round trip sooner
       unsigned long long v[4], u[4];
@@ -410,7 +419,7 @@ struct RoundLayout {
   // weight buffers receive whole slices (st.async) → at least EP floats
   static constexpr int WBP = N::PPAD > EP ? N::PPAD : EP;
   static constexpr int RSF = ClusterRS<N::P, SL, EP, CS>::smem_floats();
-  static size_t smem_bytes(int nw) {
+  __host__ __device__ static size_t smem_bytes(int nw) {
     return sizeof(float) * (size_t)(2 * WBP + nw * SPW * N::WARP_FLOATS + nw * N::PPAD + 2 * SL +
                                     ((CS + 3) & ~3) + RSF);
   }
@@ -693,6 +702,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   float* wpart = smem + 2 * RL::WBP + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
   float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
   ClusterRS<N::P, SL, RL::EP, CS> rs;  // the round's exchange (one GPU or GX ranks)
+#ifdef GHC_CHECKED
+  {  // the host sized the launch's shared memory with the same layout
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    GHC_CHECK(RL::smem_bytes(NW) <= dyn);
+  }
+#endif
   rs.init(a, cluster, vsl + 2 * SL + ((CS + 3) & ~3));
 
   unsigned long long round0 = 0;

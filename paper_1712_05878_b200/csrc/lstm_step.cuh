@@ -391,6 +391,11 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     hs[sp] = ws + sp * N::WARP_FLOATS + N::S_H;
     cs[sp] = ws + sp * N::WARP_FLOATS + N::S_C;
     dzs[sp] = ws + sp * N::WARP_FLOATS + N::S_DZ;  // dz[t][4H]
+    // the slot's last region ends inside the slot; x rows come from a slot's
+    // double buffer (or the caller's staging row)
+    GHC_CHECK(N::S_DZ + T * 4 * H <= N::WARP_FLOATS && N::S_C + T * H * 8 <= N::S_DZ &&
+              N::S_H + T * H <= N::S_C && 2 * N::XWP <= N::S_L);
+    GHC_CHECK(xs[sp] != nullptr && (reinterpret_cast<uintptr_t>(xs[sp]) & 15u) == 0);
   }
   // x_t (DP floats, float4 loads) and h_t (H floats, float4 when H%4==0)
   auto load_x = [&](int sp, int t, float (&v)[DP]) {
