@@ -817,6 +817,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   };
 
   if (RES && blockIdx.x == 0 && threadIdx.x == 0) a.res->ctas = gridDim.x;
+  if constexpr (RES) __syncthreads();  // s_has_next initialised before any thread reads it
   unsigned long long pk[8];  // thread 0: the next command's slot, loaded during the last round
   unsigned long long* prl = nullptr;  // probe row of the last round run (resident: segment-boundary probes)
   for (;;) {  // segments
@@ -843,8 +844,10 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     cp_async_commit();
   }
   prefetched = false;
-  if (threadIdx.x == 0) s_has_next = s_early = 0;
+  // reset after the barrier: every thread has read `have` (s_has_next) for
+  // this segment — the peeked-command fast path has no barrier of its own
   __syncthreads();
+  if (threadIdx.x == 0) s_has_next = s_early = 0;
 
   for (int r = 0; r < srounds; ++r, ++rg) {
     int ntot = GX * a.n;  // samples of round r over all ranks (SPEC.md:358-366 weighted mean)
