@@ -153,3 +153,48 @@ def test_packed_rows_bit_identical(ctx, monkeypatch):
     mt = g.Master(atc, w0, 0.01, 0.9)
     with pytest.raises(g.ConfigError):
         mt.sync_rounds(dp, None, di, B, B, 1)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_resident_randomised_command_stream(ctx, seed):
+    """Stress of the command protocol (the peeked-command fast path, the early
+    and late next-batch fetch, the slot ring): random command lengths, queue
+    depths 1..6 and host-side pauses between submissions, batches alternating
+    between device and pinned host memory — always bit-identical to one
+    ordinary launch over the same rounds."""
+    rng = np.random.default_rng(seed)
+    B = 1000
+    lens = rng.integers(1, 5, size=40)
+    R = int(lens.sum())
+    arch, x, y, idx, dx, dy, di = _setup(ctx, R, B)
+    w0 = g.init_weights(arch, 7)
+    # packed rows (x | label | pad) for both paths; host copies of each round's batch
+    dp = g.pack_dataset(ctx, dx, dy)
+    ref = g.Master(arch, w0, 0.01, 0.9)
+    lref = ctx.array(R)
+    ref.sync_rounds(dp, None, di, B, B, R, loss_out=lref)
+    xp = g.pack_rows(x[idx], y[idx])  # round r's batch = rows r*B .. r*B+B-1
+    hx = ctx.host_array(xp.shape)
+    hx.np[:] = xp
+    m = g.Master(arch, w0, 0.01, 0.9)
+    loss = ctx.array(R)
+    res = g.Resident(m, B)
+    seqs, r0, k = [], 0, 0
+    while r0 < R:
+        n = int(lens[k])
+        if rng.random() < 0.5:  # device dataset + index stream
+            seqs.append(res.submit(dp, None, di, B, n, loss_out=loss, idx_offset=r0 * B, loss_offset=r0))
+        else:  # contiguous batches in pinned host memory
+            seqs.append(res.submit(hx.sub(r0 * B), None, None, B, n, loss_out=loss, loss_offset=r0))
+        r0 += n
+        k += 1
+        depth = int(rng.integers(1, 7))
+        while len(seqs) >= depth and seqs:
+            res.wait(seqs.pop(0))
+        if rng.random() < 0.2:
+            time.sleep(float(rng.uniform(0, 2e-4)))
+    for s in seqs:
+        res.wait(s)
+    res.stop()
+    assert np.array_equal(m.read()[0], ref.read()[0])
+    assert np.array_equal(loss.numpy(), lref.numpy())
