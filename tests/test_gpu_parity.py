@@ -109,6 +109,31 @@ def test_label_out_of_range(ctx):
         g.forward_backward(np.zeros(arch.n_params, np.float32), arch, x, y)
 
 
+def test_empty_batch_and_negative_label(ctx):
+    """nn.cpp:104 (n_samples >= 1) and nn.cpp:242/290 (labels in [0, K)) on
+    every device entry: the fused worker step, the master's sync rounds and
+    the resident service."""
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    x, y = dataset(BENCH_ARCH, 10)
+    w = np.zeros(arch.n_params, np.float32)
+    with pytest.raises(g.ShapeError):
+        g.forward_backward(w, arch, x[:0], y[:0])
+    yn = y.copy()
+    yn[0] = -1
+    with pytest.raises(g.ShapeError):
+        g.forward_backward(w, arch, x, yn)
+    m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+    dx, dy = ctx.upload(x), ctx.upload(y)
+    with pytest.raises(g.ShapeError):
+        m.sync_rounds(dx, dy, None, 10, 0, 1)
+    with pytest.raises(g.ShapeError):
+        g.Resident(m, 0)
+    # the label K-1 is valid, K is not (checked on the device, raised at the next sync point)
+    yk = y.copy()
+    yk[:] = 2
+    g.forward_backward(w, arch, x, yk)
+
+
 def test_invalid_arch_is_config_error(ctx):
     """ConfigError only where the reference rejects too (arch.cpp:26-73);
     shapes outside the fused table run on the generic path (test_gpu_generic)."""
