@@ -5,6 +5,7 @@
 // cooperative launches for the kernels that carry a grid barrier.  All math
 // runs in the sm_100a kernels of lstm_step.cuh / update_kernels.cuh; there is
 // no CPU compute path.
+#include <cstdio>
 #include <cstdlib>
 
 #include "ghc_internal.cuh"
@@ -343,6 +344,14 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
       if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(fn), &cfg) != cudaSuccess)
         ncl = 0;
       cudaGetLastError();
+      // GHC_MAX_CTAS=n: a persistent grid of at most n CTAs — for processes
+      // sharing one GPU (MPS), whose grids must be co-resident side by side
+      // (the occupancy query sees the whole device)
+      static const int cap = [] {
+        const char* e = std::getenv("GHC_MAX_CTAS");
+        return e ? std::atoi(e) : 0;
+      }();
+      if (cap > 0 && ncl > cap / cs) ncl = cap / cs;
       return ncl;
     };
     const int64_t bench_batch = 1000;  // per-worker batch of the bench config
@@ -373,6 +382,8 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
       const char* fcs = std::getenv("GHC_CS");
       const int force_cs = fcs ? std::atoi(fcs) : 0;
       int best_warps = 1 << 30;
+      int64_t fb_slots = 0;  // no size holds the bench batch in one pass (e.g. a
+      int fb_ci = -1, fb_ncl = 0, fb_warps = 0;  // GHC_MAX_CTAS cap): the most slots, smaller clusters on ties
       for (int ci : {1, 0, 2}) {
         const int cs = kClusterSizes[ci];
         if (force_cs ? cs != force_cs : cs == 2) continue;
@@ -389,6 +400,18 @@ ghc_status ghc_plan_create(ghc_ctx* c, const char* arch_text, ghc_plan** out) {
           p->max_clusters = ncl;
           p->round_warps = warps;
         }
+        if (slots * warps > fb_slots || (slots * warps == fb_slots && cs < kClusterSizes[fb_ci])) {
+          fb_slots = slots * warps;
+          fb_ci = ci;
+          fb_ncl = ncl;
+          fb_warps = warps;
+        }
+      }
+      if (best_warps == (1 << 30) && fb_ci >= 0) {
+        p->cluster_size = kClusterSizes[fb_ci];
+        p->cs_index = fb_ci;
+        p->max_clusters = fb_ncl;
+        p->round_warps = fb_warps;
       }
     }
     if (p->use_cluster && p->max_clusters > 0) {
