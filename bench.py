@@ -159,8 +159,11 @@ def under_profiler() -> bool:
 
 
 def dist_env():
+    # GHC_BENCH_DEVICE pins every rank to one device (validation of the N > 1
+    # path with all ranks sharing one GPU under MPS, tools/gpurun_r2_mps_bench.sh)
+    dev = os.environ.get("GHC_BENCH_DEVICE")
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
+            int(dev) if dev is not None else int(os.environ.get("LOCAL_RANK", 0)))
 
 
 # --------------------------------------------------------------------------
@@ -455,14 +458,15 @@ def run_ours_dist(args, rank, world, local):
     loss = ctx.array(total_rounds)
     state = {"m": m}
 
-    def rounds(r0, n, loss_offset):
+    def rounds(r0, n, loss_offset, lbuf=None):
         m = state["m"]
+        lbuf = loss if lbuf is None else lbuf
         if p2p:
-            ex.sync_rounds(m, dx, dy, di, B, 0, dc, B, n, loss_out=loss, idx_offset=r0 * B,
+            ex.sync_rounds(m, dx, dy, di, B, 0, dc, B, n, loss_out=lbuf, idx_offset=r0 * B,
                            counts_offset=r0 * world, loss_offset=loss_offset)
         else:
             gd.dist_sync_rounds(m, comm, exchange, dx, dy, di, B, counts[r0:r0 + n], n,
-                                loss, idx_offset=r0 * B)
+                                lbuf, idx_offset=r0 * B)
 
     rounds(0, args.warmup, 0)
     ctx.sync()
@@ -471,8 +475,9 @@ def run_ours_dist(args, rank, world, local):
         # busy pre-roll (untimed, same number of calls on every rank: the
         # fused exchange pairs the ranks' rounds) on a scratch master
         state["m"] = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
+        scratch_loss = ctx.array(total_rounds)  # the scratch master's losses stay out of the report
         for _ in range(args.preroll_calls):
-            rounds(0, min(total_rounds, 2000), 0)
+            rounds(0, min(total_rounds, 2000), 0, scratch_loss)
         ctx.sync()
         state["m"] = m
         launches0 = ctx.launches
