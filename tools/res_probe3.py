@@ -74,5 +74,9 @@ out = {"host_batches": HOST, "loss_to_host": LOSS, "depth": DEPTH, "wall_us_per_
                                      for nm, i in (("x_in", 8), ("fwd", 9), ("softmax", 10), ("bptt", 11),
                                                    ("dW", 12), ("samples", 2), ("push_wait", 4),
                                                    ("row_store", 5), ("subslice_sgd", 6), ("gather_push", 7),
-                                                   ("commit", 13))}}
+                                                   ("commit", 13))},
+       "phase_us_from_round_start_max_cta": {nm: float(np.median(np.max(pr[sl, :, i] - pr[sl, :, 0], axis=1))) / 1e3
+                                             for nm, i in (("x_in", 8), ("fwd", 9), ("samples", 2), ("push_wait", 4),
+                                                           ("subslice_sgd", 6), ("gather_push", 7), ("commit", 13))},
+       "round_start_spread_us": float(np.median(pr[sl, :, 0].max(axis=1) - pr[sl, :, 0].min(axis=1))) / 1e3}
 print(json.dumps(out, indent=1))
