@@ -770,10 +770,16 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   // y == nullptr: packed dataset rows (ghc_dataset_pack) — x padded to a
   // 32-byte multiple with the label inside the padding: one row = whole
   // sectors, no separate label sector (DRAM traffic ≈ the algorithmic bytes)
+  // this lane's row elements (lane, lane + 32) and their padded smem offsets:
+  // round-invariant, so the per-row copy is two cp.async with no index math
+  const int xo0 = lane < N::XW ? N::xoff(lane) : 0;
+  const int xo1 = lane + 32 < N::XW ? N::xoff(lane + 32) : 0;
   auto fetch_rows = [&](int sp, int row, int b, const float* X, const int32_t* Y) {
     const float* xrow = X + (long long)row * (Y ? N::XW : N::XWPK);
     float* dst = slot_x(sp, b);
-    for (int i = lane; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);
+    if (lane < N::XW) cp_async4(dst + xo0, xrow + lane);
+    if (lane + 32 < N::XW) cp_async4(dst + xo1, xrow + lane + 32);
+    for (int i = lane + 64; i < N::XW; i += 32) cp_async4(dst + N::xoff(i), xrow + i);  // rows > 64 floats
     if (lane == 0) cp_async4(slot_l(sp) + b, Y ? static_cast<const void*>(Y + row) : xrow + N::XW);
   };
   auto fetch_nocommit = [&](int sp, int row, int b) { fetch_rows(sp, row, b, sx, sy); };
