@@ -81,6 +81,11 @@ __device__ __forceinline__ void grid_barrier(MasterDev* ms) {
 // reciprocal (BSSY/BSYNC), which serialises the four gate activations; these
 // are 4-5 instructions with no control flow, abs error ≲ 3e-7 — well inside
 // the fp32 parity budget (the reference uses libm exp/tanh, nn.cpp:15-19).
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -674,7 +674,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
     float den = 0.0f, zy = 0.0f;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      e[sp][k] = expf(z[k] - zmax);
+      e[sp][k] = ex2_approx((z[k] - zmax) * 1.4426950408889634f);  // MUFU: ≤ 2 ulp, z − zmax ≤ 0
       den += e[sp][k];
       // z[label] as a branch-free select: `if (k == label) zy = z[k]` lets the
       // compiler fold the unrolled loop into z[label] — a dynamically
@@ -683,7 +683,7 @@ __device__ __forceinline__ void lstm_samples(const float* __restrict__ wsm, floa
                            __float_as_uint(zy));
     }
     inv_den[sp] = 1.0f / den;
-    loss[sp] = logf(den) - (zy - zmax);
+    loss[sp] = lg2_approx(den) * 0.6931471805599453f - (zy - zmax);  // den ∈ [1, K]
     if (probs_row[sp] != nullptr) {
 #pragma unroll
       for (int k = 0; k < K; ++k)
