@@ -15,7 +15,11 @@
 //   rows × 16 B; LBO = stride between the two 16-B K-chunks of one MMA,
 //   SBO = stride between 8-row groups — CUTLASS mma_sm100_desc.hpp).
 // * Epilogue: tcgen05.ld 32x32b.x32 → registers → fused bias / activation /
-//   activation-derivative / scale → st.global.
+//   activation-derivative / scale → st.global (the (epi, act) switch once per
+//   chunk: each variant a branch-free unrolled loop).
+// * Large M and N: tcgen05_gemm_pair_kernel (below) — a CTA pair
+//   (cta_group::2) per 256 × 256 tile, half the shared-memory operand bytes
+//   per output, accumulator segments drained to registers for accuracy.
 #pragma once
 
 #include <type_traits>
