@@ -235,3 +235,19 @@ def test_easgd_c3_b1000(ctx, oracle):
     close(out["w"], r.w)
     for k in range(W):
         close(out["worker_w"][k], r.extra["worker_w"][k])
+
+
+def test_hierarchical_c5_b1000(ctx, oracle):
+    """c5's topology at the benchmark batch: 2 sub-masters × 4 workers,
+    B = 1000 per worker, flush K = 2 into the pass-through top master."""
+    kw = dict(n_workers=8, batch_size=1000, epochs=1, groups=2, flush_k=2)
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    s = g.Session(arch, g.train_config(**kw), g.data_spec(16, 4000))
+    s.run()
+    out = s.read()
+    spec, x, y = oracle_data(oracle, 16, 4000)
+    r = oracle.run_hier(oracle.parse_arch(BENCH_ARCH), spec, x, y, oracle.train_cfg(**kw))
+    assert out["version"] == r.stats.updates and out["samples"] == r.stats.samples
+    close(out["w"], r.w)
+    for q in range(2):
+        close(out["group_w"][q], r.extra["group_w"][q])
