@@ -335,7 +335,7 @@ def run_ours(args):
 # + its indices, 1000 × (50 + 1 + 1) × 4 B = 208 KB; the packed 256-B rows are
 # two whole 128-B lines each (the unpacked 200-B rows + separate labels cost
 # 324.7 KB per round, profiles/r01_ncu_full_round_final_r1_raw.csv).
-TRAFFIC_PER_ROUND = (53.533184e6 + 0.484864e6) / 200
+TRAFFIC_PER_ROUND = (53.456896e6 + 0.518912e6) / 200
 TRAFFIC_SOURCE = ("ncu --set full, 200-round launch on packed rows (profiles/r02_ncu_round_raw.csv): "
                   "dram read+write / 200; traffic = per round × timed rounds")
 
