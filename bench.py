@@ -330,8 +330,8 @@ def run_ours(args):
 
 
 # ncu --set full of one 200-round launch of lstm_round_kernel<5,20,10,3,4> on the
-# packed dataset (profiles/r02_ncu_round_raw.csv): dram__bytes_read.sum 53.53 MB
-# + dram__bytes_write.sum 0.48 MB → per round.  Algorithmic: the gathered batch
+# packed dataset (profiles/r02_ncu_round_raw.csv): dram__bytes_read.sum 53.46 MB
+# + dram__bytes_write.sum 0.52 MB → per round.  Algorithmic: the gathered batch
 # + its indices, 1000 × (50 + 1 + 1) × 4 B = 208 KB; the packed 256-B rows are
 # two whole 128-B lines each (the unpacked 200-B rows + separate labels cost
 # 324.7 KB per round, profiles/r01_ncu_full_round_final_r1_raw.csv).
