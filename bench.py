@@ -581,6 +581,12 @@ def run_e2e(args, g, ctx, arch, x, y, idx):
         m = g.Master(arch, w0, 0.01, 0.9)
         m.sync_rounds(xs, ys, ix, stride, B, min(3, rounds), loss_out=loss_out)  # warm-up
         ctx.sync()
+        # busy pre-roll (untimed, same kernel and data): the host-side packing
+        # above leaves the GPU idle long enough to drop its clocks
+        t0 = time.time()
+        while time.time() - t0 < 0.25:
+            m.sync_rounds(xs, ys, ix, stride, B, rounds, loss_out=loss_out)
+            ctx.sync()
         m = g.Master(arch, w0, 0.01, 0.9)
         loss_out.np[:] = np.nan
         ctx.sync()
