@@ -864,7 +864,12 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     const float scale = sgd ? 1.0f / (float)ntot : a.grad_scale;
     unsigned long long* pr =
         a.probe ? a.probe + ((long long)(RES ? (long long)rg : r) * gridDim.x + blockIdx.x) * 16 : nullptr;
-    if (pr && threadIdx.x == 0) pr[0] = globaltimer();
+    if (pr && threadIdx.x == 0) {
+      pr[0] = globaltimer();
+      unsigned sm;
+      asm("mov.u32 %0, %%smid;" : "=r"(sm));
+      pr[1] = sm;  // which SM ran this CTA (diagnostics: per-SM skew)
+    }
 
     // ---- samples ----
     float lsum = 0.0f;

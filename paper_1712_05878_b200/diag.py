@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1000)
     ap.add_argument("--arch", default="lstm(5,20,10),softmax(20,3)")
     ap.add_argument("--barriers", action="store_true", help="grid-barrier micro-benchmark")
+    ap.add_argument("--dump", default=None, help="save the raw probe array [rounds][ctas][16] (.npy)")
     ap.add_argument("--p2p", type=int, default=1,
                     help="G > 1: fused cross-rank exchange with G virtual ranks (batch per rank)")
     args = ap.parse_args()
@@ -87,6 +88,8 @@ def main():
     pr = probe.numpy().reshape(R, ctas, 16).astype(np.int64)
     used = int((pr[0, :, 0] != 0).sum())
     pr = pr[:, :used, :]
+    if args.dump:
+        np.save(args.dump, pr)
     out = {"kernel": arch.kernel_name, "max_clusters": maxc, "cluster_size": cs, "warps": warps,
            "rounds": R,
            "ctas": used, "us_per_round": 1e3 * ms / R, "phases_ns": {}}
