@@ -105,6 +105,17 @@ def test_gemm_pair_epilogues(ctx, act):
     assert np.max(np.abs(gemm(ctx, A, B, alpha=0.25) - 0.25 * D)) <= 1e-5
 
 
+@pytest.mark.parametrize("rows,cols", [(1000, 4096), (4096, 20), (20, 4096), (257, 132), (1, 256), (300, 300)])
+def test_transpose_vec(ctx, rows, cols):
+    """The float4 register-block transpose (rows·cols ≥ 2^16 or aligned
+    shapes): ragged 64-tiles and partial 4×4 blocks at the edges."""
+    x = np.random.default_rng(rows + cols).normal(size=(rows, cols)).astype(np.float32)
+    dx = ctx.upload(x)
+    dt = ctx.array((cols, rows))
+    _lib.check(ctx.lib.ghc_transpose(ctx.h, dt.ptr, dx.ptr, rows, cols, cols, rows))
+    assert np.array_equal(dt.numpy(), x.T)
+
+
 def test_transpose(ctx):
     x = np.random.default_rng(0).normal(size=(1000, 77)).astype(np.float32)
     dx = ctx.upload(x)
