@@ -488,6 +488,11 @@ def run_ours_dist(args, rank, world, local):
         gate = not under_profiler()
         if gate:
             ctx.hold()  # queue the timed launches behind a gate (device time only)
+        if p2p:
+            # device-side barrier of the ranks right before the start event:
+            # the processes' gates open tens of µs apart after the host
+            # barrier, which the max over ranks would otherwise count
+            ex.device_barrier()
         ctx.timer_start()
         rounds(args.warmup, args.steps, args.warmup)
         if gate:
@@ -534,6 +539,7 @@ def run_e2e_dist(args, g, gd, tdist, ctx, arch, ex, x, y, plan, dc, rank, world)
     m = g.Master(arch, g.init_weights(arch, 7), 0.01, 0.9)
     ctx.sync()
     tdist.barrier()
+    ex.device_barrier()  # align the ranks' start events on the device (no host skew)
     ctx.timer_start()
     ex.sync_rounds(m, hx, hy, None, B, 0, dc, B, K, loss_out=hl)
     ms_local = ctx.timer_stop()

@@ -412,6 +412,13 @@ ghc_status ghc_p2p_diag_push(ghc_p2p* p, int32_t dst, uint32_t tag, int32_t n);
 ghc_status ghc_p2p_diag_check(ghc_p2p* p, int32_t src, uint32_t tag, int32_t n, int32_t* h_bad);
 /* Elements per receive row (the fused kernel's padded gradient row, EP). */
 int32_t ghc_p2p_row_elems(const ghc_p2p* p);
+/* Device-side barrier of the nranks ranks, queued on the context stream
+ * (system-scope flag stores into every peer's mapped line, then a poll of
+ * this rank's line): work queued after it starts on all ranks within about
+ * one NVLink round trip.  Every rank must call it equally often.  Virtual
+ * exchanges: no-op.  (No reference counterpart: measurement plumbing for
+ * timing the fused exchange across processes without host skew.) */
+ghc_status ghc_p2p_barrier(ghc_p2p* p);
 
 /* ------------------------------------------------------------------ */
 /* Data layer, host side, bit-identical to the oracle */

@@ -147,6 +147,7 @@ SIGNATURES = [
     ("ghc_p2p_diag_push", C.c_int, [_vp, _i32, C.c_uint32, _i32]),
     ("ghc_p2p_diag_check", C.c_int, [_vp, _i32, C.c_uint32, _i32, _vp]),
     ("ghc_p2p_row_elems", _i32, [_vp]),
+    ("ghc_p2p_barrier", C.c_int, [_vp]),
     ("ghc_p2p_sync_rounds", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp]),
     ("ghc_session_create", C.c_int, [_vp, _vp, _vp, _vp]),
     ("ghc_session_destroy", None, [_vp]),

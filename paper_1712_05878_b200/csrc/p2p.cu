@@ -29,13 +29,16 @@ struct ghc_p2p {
   void* opened[kMaxRanks] = {};        // IPC-opened peer allocations
   float* gpart[kMaxRanks] = {};
   unsigned* gcnt[kMaxRanks] = {};
+  unsigned barrier_epoch = 0;          // ghc_p2p_barrier calls so far (equal on all ranks)
 };
 
 namespace {
 
 // receive rows are epoch-tagged values (uint2 per element, see ClusterXchg)
 size_t gpart_bytes(int G, int ep) { return ((sizeof(uint2) * 2 * G * ep) + 255) & ~size_t(255); }
-size_t cnt_bytes(int cs) { return sizeof(unsigned) * kFlagStride * (cs + 1); }
+// counter lines: [cs] ClusterXchg lines, [cs] the exchange epoch, [cs + 1]
+// the start barrier (slot q = rank q's arrival epoch)
+size_t cnt_bytes(int cs) { return sizeof(unsigned) * kFlagStride * (cs + 2); }
 
 ghc_status p2p_new(ghc_plan* plan, int rank, int G, bool virt, ghc_p2p** out) {
   if (!out) return fail(GHC_ERR_CONFIG, "p2p: null out");
@@ -224,3 +227,46 @@ extern "C" ghc_status ghc_p2p_diag_check(ghc_p2p* p, int32_t src, uint32_t tag, 
 }
 
 extern "C" int32_t ghc_p2p_row_elems(const ghc_p2p* p) { return p ? p->ep : 0; }
+
+namespace {
+struct BarrierPeers {
+  unsigned* line[kMaxRanks];  // each rank's barrier line (peer-mapped)
+};
+// Lane q < G stores this rank's epoch into slot `rank` of rank q's line
+// (system scope: the line lives in another GPU's memory), then waits until
+// slot q of this rank's own line reaches the epoch.  Monotone epochs: a
+// rank that runs ahead into the next barrier only raises its slot further.
+__global__ void p2p_start_barrier_kernel(BarrierPeers peers, int rank, int G, unsigned epoch) {
+  const int q = threadIdx.x;
+  if (q < G) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(peers.line[q] + rank), "r"(epoch) : "memory");
+    for (long long spin = 0;; ++spin) {
+      unsigned v;
+      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(peers.line[rank] + q) : "memory");
+      if ((int)(v - epoch) >= 0) break;
+      if (spin > (1ll << 26)) __trap();  // a rank that never arrives: fail, do not hang
+    }
+  }
+}
+}  // namespace
+
+// Device-side barrier of the G ranks on the context stream: every rank's
+// stream passes it within about one NVLink round trip of the last arrival.
+// Queued right before a timed launch, it aligns the ranks' start on the
+// device (a host barrier leaves tens of µs of skew between the processes'
+// launches).  Virtual exchanges (one grid): no-op.
+extern "C" ghc_status ghc_p2p_barrier(ghc_p2p* p) {
+  if (!p) return fail(GHC_ERR_CONFIG, "p2p_barrier: null handle");
+  if (p->virt) return GHC_OK;
+  BarrierPeers peers{};
+  for (int q = 0; q < p->G; ++q) {
+    if (!p->gcnt[q]) return fail(GHC_ERR_TRANSPORT, "p2p_barrier: peers not imported");
+    peers.line[q] = p->gcnt[q] + (p->plan->cluster_size + 1) * kFlagStride;
+  }
+  ++p->barrier_epoch;
+  CU(cudaSetDevice(p->plan->ctx->device));
+  p2p_start_barrier_kernel<<<1, 32, 0, p->plan->ctx->stream>>>(peers, p->rank, p->G, p->barrier_epoch);
+  CU(cudaGetLastError());
+  p->plan->ctx->launches++;
+  return GHC_OK;
+}

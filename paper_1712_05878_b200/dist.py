@@ -205,6 +205,11 @@ class P2PExchange:
             n_max, rounds, loss_out.offset(loss_offset) if loss_out is not None else None),
             "p2p_sync_rounds")
 
+    def device_barrier(self):
+        """ghc_p2p_barrier: queue a device-side barrier of all ranks on the
+        context stream (aligns the ranks' next launch without host skew)."""
+        g.check(self.ctx.lib.ghc_p2p_barrier(self.h), "p2p_barrier")
+
     def close(self):
         if self.h is not None and self.ctx.h and not g._SHUTDOWN[0]:
             self.ctx.lib.ghc_p2p_destroy(self.h)

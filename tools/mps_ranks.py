@@ -48,6 +48,7 @@ for split in ((R,) if os.environ.get("MPS_R") else (R, 7)):
     loss = ctx.array(R)
     for r0 in range(0, R, split):
         n = min(split, R - r0)
+        ex.device_barrier()  # ghc_p2p_barrier across the processes (start alignment)
         ex.sync_rounds(m, dx, dy, di, B, 0, dc, B, n, loss_out=loss, idx_offset=r0 * B,
                        counts_offset=r0 * world, loss_offset=r0)
     ctx.sync()
