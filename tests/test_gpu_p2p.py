@@ -75,6 +75,7 @@ def test_p2p_split_launches_same_bits(ctx):
         ex = gd.P2PExchange(arch, 0, W, virtual=True)
         for r0 in range(0, R, split):
             n = min(split, R - r0)
+            ex.device_barrier()  # ghc_p2p_barrier: a no-op for virtual ranks
             ex.sync_rounds(m, dx, dy, di, B, R * B, dc, B, n, idx_offset=r0 * B,
                            counts_offset=r0 * W)
         outs.append(m.read()[0])
