@@ -488,11 +488,13 @@ def run_ours_dist(args, rank, world, local):
         gate = not under_profiler()
         if gate:
             ctx.hold()  # queue the timed launches behind a gate (device time only)
+        # device-side barrier of the ranks right before the start event: the
+        # processes' gates open tens of µs apart after the host barrier,
+        # which the max over ranks would otherwise count
         if p2p:
-            # device-side barrier of the ranks right before the start event:
-            # the processes' gates open tens of µs apart after the host
-            # barrier, which the max over ranks would otherwise count
             ex.device_barrier()
+        else:
+            comm.device_barrier()
         ctx.timer_start()
         rounds(args.warmup, args.steps, args.warmup)
         if gate:

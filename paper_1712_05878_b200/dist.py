@@ -106,6 +106,16 @@ class Comm:
         g.check(ctx.lib.ghc_comm_init(ctx.h, buf, rank, world, C.byref(h)), "ncclCommInitRank")
         self.h = h
 
+    def device_barrier(self):
+        """A barrier on the context stream: a 1-element reduce to rank 0 and
+        a broadcast back (NCCL), so work queued after it starts on all ranks
+        together — the start alignment of a timed multi-rank region."""
+        if getattr(self, "_one", None) is None:
+            self._one = self.ctx.array(1)
+            self._one.zero()
+        g.check(self.ctx.lib.ghc_comm_reduce_sum(self.h, self._one.ptr, self._one.ptr, 1, 0), "reduce_sum")
+        g.check(self.ctx.lib.ghc_comm_broadcast(self.h, self._one.ptr, 1, 0), "broadcast")
+
     def split(self, color: int, key: int) -> "Comm | None":
         h = C.c_void_p()
         g.check(self.ctx.lib.ghc_comm_split(self.h, color, key, C.byref(h)), "ncclCommSplit")

@@ -107,6 +107,7 @@ def test_dist_sync_rounds_world1(ctx, oracle, mode):
     loss = ctx.array(R)
     counts = plan.counts.reshape(R, 1)
     dx, dy, di = ctx.upload(x), ctx.upload(y), ctx.upload(plan.idx_local)
+    comm.device_barrier()  # the bench's start alignment (reduce + broadcast of one float)
     gd.dist_sync_rounds(m, comm, mode, dx, dy, di, B, counts[:5], 5, loss)  # two calls: the
     gd.dist_sync_rounds(m, comm, mode, dx, dy, di, B, counts[5:], R - 5, ctx.array(R),
                         idx_offset=5 * B)  # cached buffer index must stay right
