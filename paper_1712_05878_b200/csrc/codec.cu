@@ -5,13 +5,16 @@
 // the frame of a 16.9 M-parameter gradient is 67.5 MB (f32) — an HBM-bound
 // byte-shuffling job, done here where the parameters already live:
 //
-//   pack:   one thread per ALIGNED 16-byte chunk of the output frame; value
+//   pack:   per tensor, blocks of 1024 ALIGNED 16-byte output chunks; value
 //           bytes start at arbitrary byte offsets (15-byte header, 1-byte
-//           ranks), so each chunk is assembled from ≤ 5 source words with
-//           funnel shifts and written with one 16-byte store (coalesced);
-//           the few chunks that touch header bytes take a bytewise path.
-//   unpack: one thread per value, two/three aligned 32-bit loads + funnel
-//           shift; the header is parsed and validated on the host first with
+//           ranks), so the block stages the value words in shared memory
+//           (coalesced loads) and each chunk is assembled from ≤ 5 staged
+//           words with funnel shifts and written with one 16-byte store
+//           (coalesced); the few chunks that touch header bytes or region
+//           boundaries take a bytewise path.
+//   unpack: per tensor, blocks of 16 KB of value bytes staged as aligned
+//           words (coalesced loads), one funnel shift per value, coalesced
+//           stores; the header is parsed and validated on the host first with
 //           the reference's DecodeStatus taxonomy.
 //
 // Layout (little-endian): "GHUB" | u16 format 1 | u8 type (0x02 WEIGHTS,
@@ -24,6 +27,9 @@ namespace {
 
 constexpr int kMaxT = 16;       // parameter tensors of an arch (5 for the bench net)
 constexpr int kHdrMax = 256;    // header bytes of a frame (fixed part + tensor headers)
+constexpr int kMaxEdge = 3 * kMaxT + kHdrMax / 16 + 4;  // edge chunks: ≤ 2 per boundary + header + tail
+constexpr int kPackChunks = 1024;   // output chunks (16 B) per pack block: 16 KB
+constexpr int kUnpackBytes = 16384; // frame bytes per unpack block
 
 struct FrameMap {
   long long total;              // frame bytes
@@ -36,7 +42,20 @@ struct FrameMap {
   long long hdr_dst[kMaxT + 1]; // frame offset of header piece i
   int hdr_off[kMaxT + 2];       // piece i = hdr[hdr_off[i] .. hdr_off[i+1])
   unsigned char hdr[kHdrMax];
+  int nedge;                    // 16-B output chunks not inside one tensor's values
+  long long edge[kMaxEdge];     // (header pieces, region boundaries, frame tail)
+  int blk0[kMaxT + 1];          // launch: tensor t owns blocks [blk0[t], blk0[t+1]) (flat grid)
 };
+
+// Flat grid: block → (tensor, block within the tensor).  No empty blocks
+// (a grid of (blocks of the largest tensor) × tensors launched ~36 k idle
+// blocks for the wide net, ≈ 30 µs of block scheduling).
+__device__ __forceinline__ int block_tensor(const FrameMap& m, int& bx) {
+  int t = 0;
+  while (t < m.nt && static_cast<int>(blockIdx.x) >= m.blk0[t + 1]) ++t;
+  bx = static_cast<int>(blockIdx.x) - m.blk0[t];
+  return t;
+}
 
 void put_le(unsigned char* p, uint64_t v, int n) {
   for (int i = 0; i < n; ++i) p[i] = static_cast<unsigned char>(v >> (8 * i));
@@ -99,6 +118,18 @@ ghc_status build_map(const ghc_plan* p, int kind, int f64, uint64_t version, uin
   m.hdr_len = hl;
   m.total = pos;
   put_le(h + 7, static_cast<uint64_t>(pos - 15), 8);
+  // chunks the interior pass of the pack kernel does not write: every chunk
+  // that is not wholly inside one tensor's value bytes
+  const long long nch = (pos + 15) / 16;
+  long long c = 0;
+  for (int t = 0; t <= m.nt; ++t) {
+    const long long stop = t < m.nt ? (m.dst[t] + 15) / 16 : nch;  // first interior chunk of t
+    for (; c < stop; ++c) {
+      if (m.nedge >= kMaxEdge) return fail(GHC_ERR_CONFIG, "frame: too many edge chunks");
+      m.edge[m.nedge++] = c;
+    }
+    if (t < m.nt) c = std::max(c, (m.dst[t] + m.n[t] * m.es) / 16);  // past t's interior chunks
+  }
   return GHC_OK;
 }
 
@@ -126,97 +157,185 @@ __device__ __forceinline__ unsigned frame_byte(const FrameMap& m, const float* _
   return 0;
 }
 
-// 32-bit word j of the value stream of tensor t (f64: low/high halves)
-__device__ __forceinline__ unsigned value_word(const FrameMap& m, const float* __restrict__ w, int t,
-                                               long long j) {
-  if (m.es == 4) return __float_as_uint(__ldg(w + m.src[t] + j));
-  const double d = static_cast<double>(__ldg(w + m.src[t] + (j >> 1)));
-  const long long bits = __double_as_longlong(d);
-  return (j & 1) ? static_cast<unsigned>(bits >> 32) : static_cast<unsigned>(bits);
-}
-
-__global__ void pack_frame_kernel(const FrameMap m, const float* __restrict__ w,
-                                  unsigned char* __restrict__ out) {
-  const long long nchunk = (m.total + 15) / 16;
-  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < nchunk;
-       c += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long c0 = c * 16;
-    int seg = -1;
-    for (int t = 0; t < m.nt; ++t)
-      if (c0 >= m.dst[t] && c0 + 16 <= m.dst[t] + m.n[t] * m.es) seg = t;
-    if (seg >= 0) {  // whole chunk inside one tensor's values: funnel-shifted words
-      const long long b = c0 - m.dst[seg];
-      const long long j0 = b >> 2;
-      const int r = static_cast<int>(b & 3);
-      const long long nw = m.n[seg] * (m.es / 4);
-      unsigned wd[5];
-      const long long a = j0 & ~3LL;  // f32: two aligned 16-B loads cover words j0..j0+4
-      if (m.es == 4 && ((m.src[seg] + a) & 3) == 0 && a + 8 <= nw) {
-        const uint4* q = reinterpret_cast<const uint4*>(w + m.src[seg] + a);
-        const uint4 q0 = __ldg(q), q1 = __ldg(q + 1);
-        const unsigned v8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        switch (static_cast<int>(j0 - a)) {  // static register indices per case
-          case 0: wd[0] = v8[0]; wd[1] = v8[1]; wd[2] = v8[2]; wd[3] = v8[3]; wd[4] = v8[4]; break;
-          case 1: wd[0] = v8[1]; wd[1] = v8[2]; wd[2] = v8[3]; wd[3] = v8[4]; wd[4] = v8[5]; break;
-          case 2: wd[0] = v8[2]; wd[1] = v8[3]; wd[2] = v8[4]; wd[3] = v8[5]; wd[4] = v8[6]; break;
-          default: wd[0] = v8[3]; wd[1] = v8[4]; wd[2] = v8[5]; wd[3] = v8[6]; wd[4] = v8[7]; break;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 5; ++k) wd[k] = (k < 4 || r) && j0 + k < nw ? value_word(m, w, seg, j0 + k) : 0u;
-      }
-      uint4 o;
-      o.x = r ? __funnelshift_r(wd[0], wd[1], 8 * r) : wd[0];
-      o.y = r ? __funnelshift_r(wd[1], wd[2], 8 * r) : wd[1];
-      o.z = r ? __funnelshift_r(wd[2], wd[3], 8 * r) : wd[2];
-      o.w = r ? __funnelshift_r(wd[3], wd[4], 8 * r) : wd[3];
-      reinterpret_cast<uint4*>(out + c0)[0] = o;
-    } else {  // header bytes / segment edges / frame tail: bytewise
+// Pack.  Blocks of tensor t (block_tensor): the 16-B output chunks wholly
+// inside t's value bytes, kPackChunks per block: the block stages the value words it
+// needs in shared memory (coalesced loads of the f32 parameters; f64 frames:
+// the widened doubles' halves), then each thread assembles consecutive
+// chunks from five staged words (funnel shift by the region's byte
+// misalignment) and stores them as coalesced 16-B stores.  The last block:
+// the edge chunks (headers, region boundaries, tail), bytewise.
+__global__ void __launch_bounds__(256) pack_frame_kernel(const FrameMap m, const float* __restrict__ w,
+                                                          unsigned char* __restrict__ out) {
+  // f32: 4·kPackChunks + 5 staged words (+ ≤ 3 of alignment); f64: the
+  // 2·kPackChunks + 3 floats are staged above the words they widen into
+  constexpr int kF64Stage = 4 * kPackChunks + 8;  // ≥ 2·nf: widened words never overwrite staged floats
+  __shared__ __align__(16) unsigned sw[kF64Stage + 2 * kPackChunks + 16];
+  int bx;
+  const int t = block_tensor(m, bx);
+  if (t == m.nt) {  // the last block: edge chunks
+    for (int e = threadIdx.x; e < m.nedge; e += blockDim.x) {
+      const long long c0 = m.edge[e] * 16;
       for (int i = 0; i < 16 && c0 + i < m.total; ++i)
         out[c0 + i] = static_cast<unsigned char>(frame_byte(m, w, c0 + i));
     }
+    return;
+  }
+  const long long L = m.dst[t], H = L + m.n[t] * m.es;
+  const long long cfirst = (L + 15) / 16, cend = H / 16;  // interior chunks [cfirst, cend)
+  const long long c0 = cfirst + static_cast<long long>(bx) * kPackChunks;
+  if (c0 >= cend) return;
+  const int nc = static_cast<int>(min(static_cast<long long>(kPackChunks), cend - c0));
+  const long long nwords = m.n[t] * (m.es / 4);
+  const int r = static_cast<int>((16 * c0 - L) & 3);   // byte misalignment (same for every chunk)
+  long long j_lo = (16 * c0 - L) >> 2;                  // first value word of chunk c0
+  if (m.es == 8) j_lo &= ~1LL;                          // whole doubles
+  const long long j_hi = min(nwords, ((16 * (c0 + nc) - L) >> 2) + 1);  // one past the last word needed
+  const int nw = static_cast<int>(j_hi - j_lo);
+  // staged floats: [g0, g0 + nf) of the parameter array, loaded as aligned
+  // float4s from A = g0 & ~3 (all of a thread's loads in flight before its
+  // shared-memory stores); word j of the value stream is sw[(j - j_lo) + d]
+  // (f32) or a half of the double widened from staged float (j - j_lo) / 2
+  const long long pend = m.src[m.nt - 1] + m.n[m.nt - 1];  // end of the parameter array
+  const long long g0 = m.src[t] + (m.es == 4 ? j_lo : (j_lo >> 1));
+  const int nf = m.es == 4 ? nw : (nw + 1) / 2;
+  const long long A = g0 & ~3LL;
+  const int d = static_cast<int>(g0 - A);
+  const int nv = (d + nf + 3) / 4;
+  float* sf = reinterpret_cast<float*>(sw);  // f64: floats first, widened below
+  for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * blockDim.x) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      const long long e = A + 4LL * i;
+      if (i < nv && e + 4 <= pend) {
+        v[u] = __ldg(reinterpret_cast<const float4*>(w + e));
+      } else {
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < nv) {
+          if (e < pend) v[u].x = __ldg(w + e);
+          if (e + 1 < pend) v[u].y = __ldg(w + e + 1);
+          if (e + 2 < pend) v[u].z = __ldg(w + e + 2);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < nv) {
+        if (m.es == 4) {
+          reinterpret_cast<float4*>(sf)[i] = v[u];
+        } else {  // f64: staged above the ≤ 2·nf words they widen into
+          reinterpret_cast<float4*>(sf + kF64Stage)[i] = v[u];
+        }
+      }
+    }
+  }
+  if (m.es == 8) {  // floats staged at sf[kF64Stage + d + k] → double k = words 2k, 2k+1
+    __syncthreads();
+    for (int k = threadIdx.x; k < nf; k += blockDim.x) {
+      const long long bits = __double_as_longlong(static_cast<double>(sf[kF64Stage + d + k]));
+      sw[2 * k] = static_cast<unsigned>(bits);
+      sw[2 * k + 1] = static_cast<unsigned>(bits >> 32);
+    }
+  }
+  const int wo = m.es == 4 ? d : 0;  // word j ↔ sw[j - j_lo + wo]
+  __syncthreads();
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+    const long long c = c0 + q;
+    const int a = static_cast<int>(((16 * c - L) >> 2) - j_lo) + wo;
+    // two aligned LDS.128 (consecutive lanes, consecutive 16 B: no bank
+    // conflicts; five scalar loads at a 4-word lane stride were 4-way)
+    const uint4* sw4 = reinterpret_cast<const uint4*>(sw) + (a >> 2);
+    const uint4 u0 = sw4[0], u1 = sw4[1];
+    unsigned wd[5];
+    switch (a & 3) {  // static register indices per case
+      case 0: wd[0] = u0.x; wd[1] = u0.y; wd[2] = u0.z; wd[3] = u0.w; wd[4] = u1.x; break;
+      case 1: wd[0] = u0.y; wd[1] = u0.z; wd[2] = u0.w; wd[3] = u1.x; wd[4] = u1.y; break;
+      case 2: wd[0] = u0.z; wd[1] = u0.w; wd[2] = u1.x; wd[3] = u1.y; wd[4] = u1.z; break;
+      default: wd[0] = u0.w; wd[1] = u1.x; wd[2] = u1.y; wd[3] = u1.z; wd[4] = u1.w; break;
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) wd[k] = a + k < nw + wo ? wd[k] : 0u;
+    uint4 o;
+    o.x = r ? __funnelshift_r(wd[0], wd[1], 8 * r) : wd[0];
+    o.y = r ? __funnelshift_r(wd[1], wd[2], 8 * r) : wd[1];
+    o.z = r ? __funnelshift_r(wd[2], wd[3], 8 * r) : wd[2];
+    o.w = r ? __funnelshift_r(wd[3], wd[4], 8 * r) : wd[3];
+    reinterpret_cast<uint4*>(out + 16 * c)[0] = o;
   }
 }
 
-__global__ void unpack_frame_kernel(const FrameMap m, const unsigned char* __restrict__ in,
-                                    long long len, float* __restrict__ w) {
-  long long total = 0;
-  for (int t = 0; t < m.nt; ++t) total += m.n[t];
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int t = 0;
-    long long k = i;
-    while (k >= m.n[t]) k -= m.n[t++];
-    const long long b = m.dst[t] + k * m.es;
-    const long long a0 = b & ~3LL;
-    const int r = static_cast<int>(b & 3);
-    const int words = m.es / 4 + (r ? 1 : 0);
-    unsigned wd[3];
-    if (a0 + 4 * words <= len) {
+// Unpack.  Blocks of tensor t (block_tensor), each a span of
+// kUnpackBytes / es values: the block stages the frame words covering their bytes in shared
+// memory (coalesced 4-B loads), then each thread funnel-shifts a value out of
+// its staged words and stores it (coalesced).  Never reads past `len`.
+__global__ void __launch_bounds__(256) unpack_frame_kernel(const FrameMap m, const unsigned char* __restrict__ in,
+                                                            long long len, float* __restrict__ w) {
+  __shared__ __align__(16) unsigned sw[kUnpackBytes / 4 + 16];
+  int bx;
+  const int t = block_tensor(m, bx);
+  if (t >= m.nt) return;
+  const int per = kUnpackBytes / m.es;
+  const long long k0 = static_cast<long long>(bx) * per;
+  if (k0 >= m.n[t]) return;
+  const int nk = static_cast<int>(min(static_cast<long long>(per), m.n[t] - k0));
+  const long long b0 = m.dst[t] + k0 * m.es;              // first byte of the block's values
+  const long long w_lo = b0 >> 2;
+  const long long w_hi = (b0 + static_cast<long long>(nk) * m.es + 3) / 4 + 1;  // + the funnel's extra word
+  const int nw = static_cast<int>(w_hi - w_lo);
+  // aligned 16-B loads from word A = w_lo & ~3 (16-B aligned frames; else
+  // 4-B loads), all of a thread's loads in flight before its smem stores;
+  // word wi ↔ sw[wi - w_lo + d]
+  const bool vec = (reinterpret_cast<uintptr_t>(in) & 15u) == 0;
+  const long long A = vec ? (w_lo & ~3LL) : w_lo;
+  const int d = static_cast<int>(w_lo - A);
+  const int nv = vec ? (d + nw + 3) / 4 : nw;
+  auto word = [&](long long wi) {
+    if (4 * wi + 4 <= len) return __ldg(reinterpret_cast<const unsigned*>(in) + wi);
+    unsigned v = 0;  // the frame's last word: bytes before `len` only
+    for (int y = 0; y < 4; ++y)
+      if (4 * wi + y < len) v |= static_cast<unsigned>(in[4 * wi + y]) << (8 * y);
+    return v;
+  };
+  for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * blockDim.x) {
+    uint4 v[4];
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-        wd[q] = q < words ? __ldg(reinterpret_cast<const unsigned*>(in + a0) + q) : 0u;
-    } else {  // last value of the frame: never read past its end
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        unsigned v = 0;
-        for (int y = 0; y < 4; ++y) {
-          const long long p = a0 + 4 * q + y;
-          if (p < len) v |= static_cast<unsigned>(in[p]) << (8 * y);
-        }
-        wd[q] = v;
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= nv) continue;
+      if (!vec) {
+        v[u].x = word(A + i);
+      } else if (16 * (A / 4 + i) + 16 <= len) {
+        v[u] = __ldg(reinterpret_cast<const uint4*>(in) + A / 4 + i);
+      } else {
+        v[u] = make_uint4(word(A + 4 * i), word(A + 4 * i + 1), word(A + 4 * i + 2), word(A + 4 * i + 3));
       }
     }
-    const unsigned lo = r ? __funnelshift_r(wd[0], wd[1], 8 * r) : wd[0];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= nv) continue;
+      if (vec) reinterpret_cast<uint4*>(sw)[i] = v[u];
+      else sw[i] = v[u].x;
+    }
+  }
+  __syncthreads();
+  float* dst = w + m.src[t] + k0;
+  for (int q = threadIdx.x; q < nk; q += blockDim.x) {
+    const long long b = b0 + static_cast<long long>(q) * m.es;
+    const int a = static_cast<int>((b >> 2) - w_lo) + d;
+    const int r = static_cast<int>(b & 3);
+    const unsigned lo = r ? __funnelshift_r(sw[a], sw[a + 1], 8 * r) : sw[a];
     float v;
     if (m.es == 4) {
       v = __uint_as_float(lo);
     } else {
-      const unsigned hi = r ? __funnelshift_r(wd[1], wd[2], 8 * r) : wd[1];
+      const unsigned hi = r ? __funnelshift_r(sw[a + 1], sw[a + 2], 8 * r) : sw[a + 1];
       v = __double2float_rn(__longlong_as_double(
           static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo)));
     }
-    w[m.src[t] + k] = v;
+    dst[q] = v;
   }
 }
 
@@ -227,10 +346,25 @@ const char* decode_name(int s) {
   return s >= 0 && s <= 6 ? names[s] : "?";
 }
 
-int grid_for(ghc_ctx* c, long long work) {
-  const long long g = (work + 255) / 256;
-  const long long cap = 8LL * c->num_sms;
-  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+// The header bytes decode expects, gathered on the device in ONE launch and
+// brought to the host in ONE copy: the first 64 bytes (fixed header + first
+// tensor header) and every later tensor header at its position in a WEIGHTS /
+// GRADIENT frame of this architecture, f32 and f64 — instead of one
+// synchronous copy per header field (≈ 20 round trips per decode).
+constexpr int kMaxPieces = 4 * kMaxT + 1;
+constexpr int kHdrScratch = 64 + 4 * kMaxT * 16;  // piece bytes: first 64 + ≤ 9 per tensor header
+struct Pieces {
+  int n;
+  long long off[kMaxPieces];
+  int len[kMaxPieces];
+  int out[kMaxPieces];
+};
+__global__ void gather_pieces_kernel(const unsigned char* __restrict__ in, long long len, const Pieces p,
+                                     unsigned char* __restrict__ out) {
+  const int i = blockIdx.x;
+  if (i >= p.n) return;
+  for (int b = threadIdx.x; b < p.len[i]; b += blockDim.x)
+    out[p.out[i] + b] = p.off[i] + b < len ? in[p.off[i] + b] : 0;
 }
 
 }  // namespace
@@ -252,7 +386,13 @@ ghc_status ghc_encode_frame(ghc_plan* p, int32_t kind, int32_t wire_f64, const f
   if (reinterpret_cast<uintptr_t>(d_out) & 15) return fail(GHC_ERR_CONFIG, "encode: output must be 16-byte aligned");
   if (kind != 0 && !d_w) return fail(GHC_ERR_CONFIG, "encode: null parameters");
   ghc_ctx* c = p->ctx;
-  pack_frame_kernel<<<grid_for(c, (m.total + 15) / 16), 256, 0, c->stream>>>(m, d_w, d_out);
+  long long nb = 0;  // flat grid: each tensor's interior chunk blocks, then one edge block
+  for (int t = 0; t < m.nt; ++t) {
+    m.blk0[t] = static_cast<int>(nb);
+    nb += std::max(0LL, ((m.dst[t] + m.n[t] * m.es) / 16 - (m.dst[t] + 15) / 16 + kPackChunks - 1) / kPackChunks);
+  }
+  m.blk0[m.nt] = static_cast<int>(nb);
+  pack_frame_kernel<<<static_cast<unsigned>(nb + 1), 256, 0, c->stream>>>(m, d_w, d_out);
   c->launches++;
   CU(cudaGetLastError());
   return GHC_OK;
@@ -267,8 +407,44 @@ ghc_status ghc_decode_frame(ghc_plan* p, const uint8_t* d_frame, int64_t len, in
     return fail(GHC_ERR_PROTOCOL, std::string("decode: ") + decode_name(s));
   };
   if (decode_status) *decode_status = 0;
-  // header bytes → host (at most kHdrMax + the value regions we skip)
+  // header bytes → host: the expected header pieces in one gather + copy;
+  // a read outside them (a frame of another layout) falls back to its own copy
+  Pieces pc{};
+  auto add = [&](long long off, int n) {
+    if (pc.n >= kMaxPieces || n <= 0 || off >= len) return;
+    pc.off[pc.n] = off;
+    pc.len[pc.n] = n;
+    pc.out[pc.n] = pc.n ? pc.out[pc.n - 1] + pc.len[pc.n - 1] : 0;
+    ++pc.n;
+  };
+  add(0, 64);
+  for (int kind_ : {1, 2})
+    for (int f64_ : {0, 1}) {
+      FrameMap mm;
+      if (build_map(p, kind_, f64_, 0, 1, mm) != GHC_OK) continue;
+      for (int t = 1; t < mm.nt; ++t) add(mm.hdr_dst[t], mm.hdr_off[t + 1] - mm.hdr_off[t]);
+    }
+  std::vector<unsigned char> cache;
+  if (pc.n > 0) {
+    const int total = pc.n ? pc.out[pc.n - 1] + pc.len[pc.n - 1] : 0;
+    cache.resize(static_cast<size_t>(total));
+    // a context-owned scratch (a stream-ordered allocation per call costs
+    // a pool remap after every synchronisation: ≈ 0.3 ms per decode)
+    if (total > kHdrScratch) return fail(GHC_ERR_CONFIG, "decode: header pieces exceed the scratch");
+    if (!c->hdr_scratch) CU(cudaMalloc(reinterpret_cast<void**>(&c->hdr_scratch), kHdrScratch));
+    gather_pieces_kernel<<<pc.n, 64, 0, c->stream>>>(d_frame, len, pc, c->hdr_scratch);
+    c->launches++;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(cache.data(), c->hdr_scratch, static_cast<size_t>(total), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
   auto fetch = [&](int64_t off, int64_t n, unsigned char* dst) -> ghc_status {
+    for (int i = 0; i < pc.n; ++i)
+      if (off >= pc.off[i] && off + n <= pc.off[i] + pc.len[i] && off + n <= len) {
+        std::memcpy(dst, cache.data() + pc.out[i] + (off - pc.off[i]), static_cast<size_t>(n));
+        return GHC_OK;
+      }
     CU(cudaMemcpyAsync(dst, d_frame + off, static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     return GHC_OK;
@@ -352,8 +528,14 @@ ghc_status ghc_decode_frame(ghc_plan* p, const uint8_t* d_frame, int64_t len, in
   if (version) *version = ver;
   if (sample_count) *sample_count = cnt;
   if (d_w) {
-    unpack_frame_kernel<<<grid_for(c, want.src[want.nt - 1] + want.n[want.nt - 1]), 256, 0,
-                          c->stream>>>(m, d_frame, len, d_w);
+    if (reinterpret_cast<uintptr_t>(d_frame) & 3) return fail(GHC_ERR_CONFIG, "decode: frame must be 4-byte aligned");
+    long long nb = 0;  // flat grid: kUnpackBytes of values per block
+    for (int t = 0; t < m.nt; ++t) {
+      m.blk0[t] = static_cast<int>(nb);
+      nb += (m.n[t] * es + kUnpackBytes - 1) / kUnpackBytes;
+    }
+    m.blk0[m.nt] = static_cast<int>(nb);
+    unpack_frame_kernel<<<static_cast<unsigned>(std::max(1LL, nb)), 256, 0, c->stream>>>(m, d_frame, len, d_w);
     c->launches++;
     CU(cudaGetLastError());
   }

@@ -103,6 +103,7 @@ void ghc_ctx_destroy(ghc_ctx* c) {
   cudaStreamDestroy(c->stream);
   cudaFree(c->splitk_ws);
   cudaFree(c->scratch_ms);
+  cudaFree(c->hdr_scratch);
   if (c->gate_h) cudaFreeHost(c->gate_h);
   delete c;
 }

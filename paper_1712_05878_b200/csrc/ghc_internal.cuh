@@ -64,6 +64,7 @@ struct ghc_ctx {
   float* splitk_ws = nullptr;  // split-K GEMM partials (dense.cu), grown on demand
   size_t splitk_bytes = 0;
   MasterDev* scratch_ms = nullptr;  // barrier state of the context-level cooperative kernels
+  unsigned char* hdr_scratch = nullptr;  // decode: gathered frame-header bytes (codec.cu), kHdrScratch
   int* gate_h = nullptr;            // ghc_stream_hold: pinned flag (host view)
   int* gate_d = nullptr;            //                  (device view)
 };
