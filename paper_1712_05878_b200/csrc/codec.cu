@@ -50,10 +50,10 @@ struct FrameMap {
 // Flat grid: block → (tensor, block within the tensor).  No empty blocks
 // (a grid of (blocks of the largest tensor) × tensors launched ~36 k idle
 // blocks for the wide net, ≈ 30 µs of block scheduling).
-__device__ __forceinline__ int block_tensor(const FrameMap& m, int& bx) {
+__device__ __forceinline__ int block_tensor(const FrameMap& m, int b, int& bx) {
   int t = 0;
-  while (t < m.nt && static_cast<int>(blockIdx.x) >= m.blk0[t + 1]) ++t;
-  bx = static_cast<int>(blockIdx.x) - m.blk0[t];
+  while (t < m.nt && b >= m.blk0[t + 1]) ++t;
+  bx = b - m.blk0[t];
   return t;
 }
 
@@ -162,24 +162,25 @@ __device__ __forceinline__ unsigned frame_byte(const FrameMap& m, const float* _
 // needs in shared memory (coalesced loads of the f32 parameters; f64 frames:
 // the widened doubles' halves), then each thread assembles consecutive
 // chunks from five staged words (funnel shift by the region's byte
-// misalignment) and stores them as coalesced 16-B stores.  The last block:
-// the edge chunks (headers, region boundaries, tail), bytewise.
+// misalignment) and stores them as coalesced 16-B stores.  Block 0: the
+// edge chunks (headers, region boundaries, tail), bytewise.
 __global__ void __launch_bounds__(256) pack_frame_kernel(const FrameMap m, const float* __restrict__ w,
                                                           unsigned char* __restrict__ out) {
   // f32: 4·kPackChunks + 5 staged words (+ ≤ 3 of alignment); f64: the
   // 2·kPackChunks + 3 floats are staged above the words they widen into
   constexpr int kF64Stage = 4 * kPackChunks + 8;  // ≥ 2·nf: widened words never overwrite staged floats
   __shared__ __align__(16) unsigned sw[kF64Stage + 2 * kPackChunks + 16];
-  int bx;
-  const int t = block_tensor(m, bx);
-  if (t == m.nt) {  // the last block: edge chunks
-    for (int e = threadIdx.x; e < m.nedge; e += blockDim.x) {
-      const long long c0 = m.edge[e] * 16;
-      for (int i = 0; i < 16 && c0 + i < m.total; ++i)
-        out[c0 + i] = static_cast<unsigned char>(frame_byte(m, w, c0 + i));
+  if (blockIdx.x == 0) {  // block 0: the edge chunks, one byte per thread (its
+    // loads overlap the bulk instead of trailing it as the last block)
+    for (int e = threadIdx.x; e < 16 * m.nedge; e += blockDim.x) {
+      const long long b = m.edge[e >> 4] * 16 + (e & 15);
+      if (b < m.total) out[b] = static_cast<unsigned char>(frame_byte(m, w, b));
     }
     return;
   }
+  int bx;
+  const int t = block_tensor(m, static_cast<int>(blockIdx.x) - 1, bx);
+  if (t >= m.nt) return;
   const long long L = m.dst[t], H = L + m.n[t] * m.es;
   const long long cfirst = (L + 15) / 16, cend = H / 16;  // interior chunks [cfirst, cend)
   const long long c0 = cfirst + static_cast<long long>(bx) * kPackChunks;
@@ -241,9 +242,10 @@ __global__ void __launch_bounds__(256) pack_frame_kernel(const FrameMap m, const
   }
   const int wo = m.es == 4 ? d : 0;  // word j ↔ sw[j - j_lo + wo]
   __syncthreads();
+  const int a0 = static_cast<int>(((16 * c0 - L) >> 2) - j_lo) + wo;  // staged word of chunk c0's first byte
   for (int q = threadIdx.x; q < nc; q += blockDim.x) {
     const long long c = c0 + q;
-    const int a = static_cast<int>(((16 * c - L) >> 2) - j_lo) + wo;
+    const int a = a0 + 4 * q;
     // two aligned LDS.128 (consecutive lanes, consecutive 16 B: no bank
     // conflicts; five scalar loads at a 4-word lane stride were 4-way)
     const uint4* sw4 = reinterpret_cast<const uint4*>(sw) + (a >> 2);
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(256) unpack_frame_kernel(const FrameMap m, con
                                                             long long len, float* __restrict__ w) {
   __shared__ __align__(16) unsigned sw[kUnpackBytes / 4 + 16];
   int bx;
-  const int t = block_tensor(m, bx);
+  const int t = block_tensor(m, static_cast<int>(blockIdx.x), bx);
   if (t >= m.nt) return;
   const int per = kUnpackBytes / m.es;
   const long long k0 = static_cast<long long>(bx) * per;
@@ -322,10 +324,66 @@ __global__ void __launch_bounds__(256) unpack_frame_kernel(const FrameMap m, con
   }
   __syncthreads();
   float* dst = w + m.src[t] + k0;
-  for (int q = threadIdx.x; q < nk; q += blockDim.x) {
+  const int r = static_cast<int>(b0 & 3);  // the same byte misalignment for every value
+  const int ab = static_cast<int>((b0 >> 2) - w_lo) + d;  // staged word of the first value
+  int q0 = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    // four values per thread: their (es/4)·4 + 1 words from aligned LDS.128s
+    // (consecutive lanes, consecutive 16 B) and one 16-B store
+    const int nq = nk / 4;
+    const uint4* sw4 = reinterpret_cast<const uint4*>(sw);
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      const int a = ab + (m.es / 4) * 4 * q;  // ≡ ab (mod 4)
+      unsigned wv[12];
+      const uint4 u0 = sw4[a >> 2], u1 = sw4[(a >> 2) + 1];
+      wv[0] = u0.x; wv[1] = u0.y; wv[2] = u0.z; wv[3] = u0.w;
+      wv[4] = u1.x; wv[5] = u1.y; wv[6] = u1.z; wv[7] = u1.w;
+      if (m.es == 8) {
+        const uint4 u2 = sw4[(a >> 2) + 2];
+        wv[8] = u2.x; wv[9] = u2.y; wv[10] = u2.z; wv[11] = u2.w;
+      } else {
+        wv[8] = wv[9] = wv[10] = wv[11] = 0u;
+      }
+      unsigned x[9];  // words a .. a+8 (shift by a & 3, static register indices)
+      switch (a & 3) {
+        case 0:
+#pragma unroll
+          for (int i = 0; i < 9; ++i) x[i] = wv[i];
+          break;
+        case 1:
+#pragma unroll
+          for (int i = 0; i < 9; ++i) x[i] = wv[i + 1];
+          break;
+        case 2:
+#pragma unroll
+          for (int i = 0; i < 9; ++i) x[i] = wv[i + 2];
+          break;
+        default:
+#pragma unroll
+          for (int i = 0; i < 9; ++i) x[i] = wv[i + 3];
+          break;
+      }
+      float4 o;
+      float* ov = &o.x;
+      if (m.es == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ov[i] = __uint_as_float(r ? __funnelshift_r(x[i], x[i + 1], 8 * r) : x[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const unsigned lo = r ? __funnelshift_r(x[2 * i], x[2 * i + 1], 8 * r) : x[2 * i];
+          const unsigned hi = r ? __funnelshift_r(x[2 * i + 1], x[2 * i + 2], 8 * r) : x[2 * i + 1];
+          ov[i] = __double2float_rn(__longlong_as_double(
+              static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo)));
+        }
+      }
+      reinterpret_cast<float4*>(dst)[q] = o;
+    }
+    q0 = 4 * nq;
+  }
+  for (int q = q0 + threadIdx.x; q < nk; q += blockDim.x) {  // the rest, one value per thread
     const long long b = b0 + static_cast<long long>(q) * m.es;
     const int a = static_cast<int>((b >> 2) - w_lo) + d;
-    const int r = static_cast<int>(b & 3);
     const unsigned lo = r ? __funnelshift_r(sw[a], sw[a + 1], 8 * r) : sw[a];
     float v;
     if (m.es == 4) {
