@@ -78,3 +78,24 @@ def test_malformed_frames(ctx, oracle):
                                             np.zeros(g.arch_info("lstm(3,4,5),softmax(4,3)")[0])))
     with pytest.raises(g.ConfigError):
         g.encode_frame(arch, 2, w, sample_count=0)
+
+
+@pytest.mark.parametrize("shift", [4, 8, 12])
+@pytest.mark.parametrize("f64", [False, True])
+def test_decode_frame_at_unaligned_offsets(ctx, shift, f64):
+    """A frame that starts 4/8/12 bytes into a device buffer (not 16-B
+    aligned): the unpack kernel's 4-byte staging path, same values."""
+    import ctypes as C
+    arch = g.Architecture(ctx, "lstm(5,20,10),dense(20,64,relu),softmax(64,3)")
+    w = g.init_weights(arch, 5).astype(np.float32)
+    fr = g.encode_frame(arch, 2, w, version=9, sample_count=3, wire_f64=f64)
+    buf = np.zeros(len(fr) + 16, np.uint8)
+    buf[shift:shift + len(fr)] = np.frombuffer(fr, np.uint8)
+    d = ctx.upload(buf)
+    w2 = ctx.array(arch.n_params)
+    kind, ff, st = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    ver, cnt = C.c_uint64(0), C.c_uint64(0)
+    g.gradhub.check(ctx.lib.ghc_decode_frame(arch.h, C.c_void_p(d.ptr.value + shift), len(fr), C.byref(kind),
+                                             w2.ptr, C.byref(ver), C.byref(cnt), C.byref(ff), C.byref(st)))
+    assert (kind.value, ver.value, cnt.value, bool(ff.value)) == (2, 9, 3, f64)
+    assert np.array_equal(w2.numpy(), w)
