@@ -194,39 +194,78 @@ __global__ void __launch_bounds__(256) head_block_kernel(
   }
 }
 
-// Stage 1 of the column reduction for wide rows (cols % 4 == 0, 16-B rows):
-// thread = 4 columns × one 16-row chunk, all 16 float4 loads in flight
-// (16 MB of the 4096-wide layer ≈ all in flight at once); partials
-// [chunk][k][cols] in fixed row order, stage 2 = colsum_final_kernel.
-__global__ void __launch_bounds__(256) colsum4_partial_kernel(float* __restrict__ part,
-                                                              const float* __restrict__ X, int ldx,
-                                                              const float* __restrict__ coef, int kc,
-                                                              int n, int cols) {
-  constexpr int R = 16;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;  // column quad
-  const int ch = blockIdx.y;
-  const int k0 = 4 * blockIdx.z;
-  if (4 * q >= cols) return;
-  const int s0 = ch * R;
+// One-launch column reduction for wide rows (cols % 4 == 0, 16-B rows):
+// block = 4 column quads (16 columns) × 64 row lanes; row lane ry sums rows
+// ry, ry + 64, … (eight float4 loads in flight per thread; up to 4
+// coefficient columns k0..k0+3 from one read of X), then the 64 row-lane
+// sums per column are added by a fixed pairwise tree in shared memory —
+// deterministic; one launch instead of the two-stage partial + final pair (two launches of
+// ≈ 8 µs each per call in the wide round).
+__global__ void __launch_bounds__(256) colsum4_kernel(float* __restrict__ out, int ldo,
+                                                      const float* __restrict__ X, int ldx,
+                                                      const float* __restrict__ coef, int kc, int n,
+                                                      int cols) {
+  constexpr int QX = 4, RY = 64, U = 8;
+  __shared__ float4 red[4][RY][QX + 1];
+  const int qx = threadIdx.x & (QX - 1), ry = threadIdx.x / QX;
+  const int q = blockIdx.x * QX + qx;  // column quad
+  const int k0 = 4 * blockIdx.y;
   const int nk = coef ? min(4, kc - k0) : 1;
-  float4 v[R];
+  float4 acc[4];
 #pragma unroll
-  for (int i = 0; i < R; ++i)
-    v[i] = s0 + i < n ? __ldg(reinterpret_cast<const float4*>(X + (long long)(s0 + i) * ldx) + q)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (4 * q < cols) {
+    for (int s0 = ry; s0 < n; s0 += RY * U) {
+      float4 v[U];
+      float cf[U][4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (k >= nk) break;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < U; ++u) {
+        const int s = s0 + RY * u;
+        v[u] = s < n ? __ldg(reinterpret_cast<const float4*>(X + (long long)s * ldx) + q)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const float cf = coef ? (s0 + i < n ? __ldg(coef + (long long)(s0 + i) * kc + k0 + k) : 0.f) : 1.f;
-      acc.x = fmaf(cf, v[i].x, acc.x);
-      acc.y = fmaf(cf, v[i].y, acc.y);
-      acc.z = fmaf(cf, v[i].z, acc.z);
-      acc.w = fmaf(cf, v[i].w, acc.w);
+        for (int k = 0; k < 4; ++k)
+          cf[u][k] = coef ? (s < n && k < nk ? __ldg(coef + (long long)s * kc + k0 + k) : 0.f) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k >= nk) break;
+          acc[k].x = fmaf(cf[u][k], v[u].x, acc[k].x);
+          acc[k].y = fmaf(cf[u][k], v[u].y, acc[k].y);
+          acc[k].z = fmaf(cf[u][k], v[u].z, acc[k].z);
+          acc[k].w = fmaf(cf[u][k], v[u].w, acc[k].w);
+        }
     }
-    reinterpret_cast<float4*>(part + ((long long)ch * kc + k0 + k) * cols)[q] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < nk) red[k][ry][qx] = acc[k];
+#pragma unroll
+  for (int h = RY / 2; h > 0; h >>= 1) {  // fixed pairwise tree over the row lanes
+    __syncthreads();
+    if (ry < h) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k >= nk) break;
+        const float4 a = red[k][ry][qx], b = red[k][ry + h][qx];
+        red[k][ry][qx] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < QX * nk) {
+    const int k = threadIdx.x / QX, qq = threadIdx.x % QX;
+    const int c = 4 * (blockIdx.x * QX + qq);
+    if (c < cols) {
+      const float4 o = red[k][0][qq];
+      float* dst = out + (long long)(k0 + k) * ldo + c;
+      dst[0] = o.x;
+      dst[1] = o.y;
+      dst[2] = o.z;
+      dst[3] = o.w;
+    }
   }
 }
 
@@ -267,30 +306,6 @@ __global__ void colsum_final_kernel(float* __restrict__ out, int ldo, const floa
 #pragma unroll 8
   for (int ch = 0; ch < nchunks; ++ch) t += part[((long long)ch * kc + k) * cols + c];
   out[(long long)k * ldo + c] = t;
-}
-
-// Stage 2 for many chunks: block = 32 columns × 8 chunk groups; chunks ty,
-// ty+8, … in order, then the 8 groups in order (deterministic).
-__global__ void __launch_bounds__(256) colsum_final2_kernel(float* __restrict__ out, int ldo,
-                                                            const float* __restrict__ part, int kc,
-                                                            int cols, int nchunks) {
-  __shared__ float red[8][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + tx;
-  const int k = blockIdx.y;
-  float t = 0.f;
-  if (c < cols) {
-#pragma unroll 8
-    for (int ch = ty; ch < nchunks; ch += 8) t += part[((long long)ch * kc + k) * cols + c];
-  }
-  red[ty][tx] = t;
-  __syncthreads();
-  if (ty == 0 && c < cols) {
-    float o = 0.f;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) o += red[r][tx];
-    out[(long long)k * ldo + c] = o;
-  }
 }
 
 __global__ void sum_kernel(float* out, const float* v, int n) {
@@ -336,13 +351,9 @@ ghc_status colsum(ghc_ctx* c, LayeredWorkspace& ws, float* out, int ldo, const f
                   const float* coef, int kc, int n, int cols) {
   if (cols >= 256 && cols % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15u) == 0) {
     const int kcc = coef ? kc : 1;
-    const int nch = (n + 15) / 16;
-    if (ghc_status s = ws.part.ensure(static_cast<size_t>(nch) * kcc * cols)) return s;
-    colsum4_partial_kernel<<<dim3((cols / 4 + 255) / 256, nch, (kcc + 3) / 4), 256, 0, c->stream>>>(
-        ws.part.p, X, ldx, coef, kcc, n, cols);
-    colsum_final2_kernel<<<dim3((cols + 31) / 32, kcc), 256, 0, c->stream>>>(out, ldo, ws.part.p, kcc,
-                                                                             cols, nch);
-    c->launches += 2;
+    colsum4_kernel<<<dim3((cols / 4 + 3) / 4, (kcc + 3) / 4), 256, 0, c->stream>>>(out, ldo, X, ldx, coef,
+                                                                                  kcc, n, cols);
+    c->launches++;
     CU(cudaGetLastError());
     return GHC_OK;
   }
