@@ -461,7 +461,8 @@ ghc_status ghc_encode_frame(ghc_plan* plan, int32_t kind, int32_t wire_f64, cons
  * *decode_status = the reference's DecodeStatus 1..6; tensors not matching
  * the arch → GHC_ERR_SHAPE) and unpacks the values into d_w[P] (f64 frames
  * rounded to f32).  *kind: 1 WEIGHTS, 2 GRADIENT, 0 SHUTDOWN, -type for the
- * other message types. */
+ * other message types.  d_frame must be 4-byte aligned (16-byte aligned
+ * frames take the vector path). */
 ghc_status ghc_decode_frame(ghc_plan* plan, const uint8_t* d_frame, int64_t len, int32_t* kind,
                             float* d_w, uint64_t* version, uint64_t* sample_count,
                             int32_t* wire_f64, int32_t* decode_status);
