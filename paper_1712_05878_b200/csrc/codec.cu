@@ -11,11 +11,12 @@
 //           (coalesced loads) and each chunk is assembled from ≤ 5 staged
 //           words with funnel shifts and written with one 16-byte store
 //           (coalesced); the few chunks that touch header bytes or region
-//           boundaries take a bytewise path.
+//           boundaries take a bytewise path in block 0.
 //   unpack: per tensor, blocks of 16 KB of value bytes staged as aligned
-//           words (coalesced loads), one funnel shift per value, coalesced
-//           stores; the header is parsed and validated on the host first with
-//           the reference's DecodeStatus taxonomy.
+//           words (uint4 loads), four values per thread, one 16-byte store;
+//           the header pieces are gathered in one launch + one copy and
+//           validated on the host with the reference's DecodeStatus taxonomy.
+// Flat grids (every block has work).  Measured: DESIGN.md §8 f4.
 //
 // Layout (little-endian): "GHUB" | u16 format 1 | u8 type (0x02 WEIGHTS,
 // 0x03 GRADIENT, | 0x40 for f64 values, 0x06 SHUTDOWN) | u64 payload length |
