@@ -174,6 +174,20 @@ ghc_status ghc_worker_grad(ghc_plan* plan, const float* d_w, const float* d_x,
                            const int32_t* d_y, const int32_t* d_idx, int64_t n,
                            float grad_scale, float* d_grad, float* d_loss_sum);
 
+/* n_workers (≤ 8) independent worker gradients in ONE launch: worker k at
+ * weights d_w + k·w_stride over rows h_idx[k][0 .. h_n[k]) (h_idx: host
+ * array of device pointers; an entry may be NULL → rows 0 .. h_n[k]-1),
+ * scaled by 1/h_n[k], into d_grad + k·g_stride; its loss sum into
+ * d_loss[k] (nullable).  The grid is split into n_workers virtual ranks of
+ * the fused round kernel with no cross-rank sum (the session's sync EASGD
+ * round, whose workers' gradients are independent within a round); shapes
+ * without that kernel variant fall back to n_workers ghc_worker_grad calls.
+ * Same semantics as ghc_worker_grad per worker (nn.cpp:250-399); the
+ * reduction order differs (fewer clusters per worker), deterministic. */
+ghc_status ghc_worker_grads(ghc_plan* plan, int32_t n_workers, const float* d_w, int64_t w_stride,
+                            const float* d_x, const int32_t* d_y, const int32_t* const* h_idx,
+                            const int32_t* h_n, float* d_grad, int64_t g_stride, float* d_loss);
+
 /* Forward only: class probabilities d_probs[n×K] (nullable) and loss sum. */
 ghc_status ghc_forward(ghc_plan* plan, const float* d_w, const float* d_x,
                        const int32_t* d_y, const int32_t* d_idx, int64_t n,

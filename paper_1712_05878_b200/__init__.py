@@ -9,7 +9,8 @@ from .gradhub import (Architecture, arch_info, CacheMismatchError, ConfigError, 
                       OptimState, ProtocolError, ShapeError, TransportError, batches, data_spec,
                       easgd_center_step, easgd_worker_step, elastic_pull, epoch_indices, forward,
                       forward_backward, generate, init_weights, sgd_step, shard_files,
-                      worker_grad_device, Session, train_config, DOWNPOUR, EASGD, SYNC,
+                      worker_grad_device, worker_grads_device, Session, train_config, DOWNPOUR,
+                      EASGD, SYNC,
                       REPLAY, validate, HostArray, encode_frame, decode_frame,
                       FRAME_SHUTDOWN, FRAME_WEIGHTS, FRAME_GRADIENT, Resident, pack_rows,
                       pack_dataset)

@@ -101,6 +101,7 @@ SIGNATURES = [
     ("ghc_init_weights_text", C.c_int, [_cp, _u64, _vp]),
     ("ghc_init_weights", C.c_int, [_vp, _u64, _vp]),
     ("ghc_worker_grad", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _vp, _vp]),
+    ("ghc_worker_grads", C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     ("ghc_forward", C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     ("ghc_forward_cache", C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     ("ghc_gemm_nt", C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,

@@ -545,6 +545,45 @@ ghc_status ghc_worker_grad(ghc_plan* p, const float* d_w, const float* d_x, cons
   return launch_step(p, a, n);
 }
 
+ghc_status ghc_worker_grads(ghc_plan* p, int32_t W, const float* d_w, int64_t w_stride, const float* d_x,
+                            const int32_t* d_y, const int32_t* const* h_idx, const int32_t* h_n,
+                            float* d_grad, int64_t g_stride, float* d_loss) {
+  if (W < 1 || W > kMaxRanks) return fail(GHC_ERR_CONFIG, "worker_grads: n_workers must be in [1, 8]");
+  if (!p || !d_w || !d_x || !h_idx || !h_n || !d_grad) return fail(GHC_ERR_CONFIG, "worker_grads: null argument");
+  int64_t n_max = 0;
+  for (int k = 0; k < W; ++k) {
+    if (h_n[k] < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");  // nn.cpp:104
+    n_max = std::max<int64_t>(n_max, h_n[k]);
+  }
+  const bool fused = !p->layered && p->lstm && p->use_cluster && !p->use_tc && p->max_clusters / W >= 1 &&
+                     p->lstm->fn_multi[p->cs_index] != nullptr;
+  if (!fused || W == 1) {
+    for (int k = 0; k < W; ++k)
+      if (ghc_status s = ghc_worker_grad(p, d_w + k * w_stride, d_x, d_y, h_idx[k], h_n[k],
+                                         1.0f / static_cast<float>(h_n[k]), d_grad + k * g_stride,
+                                         d_loss ? d_loss + k : nullptr))
+        return s;
+    return GHC_OK;
+  }
+  StepArgs a{};
+  a.x = d_x;
+  a.y = d_y;
+  a.n = static_cast<int>(n_max);
+  a.rounds = 1;
+  a.w_in = d_w;
+  a.ms = p->ms;
+  a.g_out = d_grad;
+  a.loss_out = d_loss;
+  a.mode = MODE_GRAD;
+  a.w_vstride = w_stride;
+  a.g_vstride = g_stride;
+  for (int k = 0; k < W; ++k) {
+    a.idx_v[k] = h_idx[k];
+    a.n_v[k] = static_cast<int>(h_n[k]);
+  }
+  return launch_step(p, a, n_max, W, nullptr, true);
+}
+
 ghc_status ghc_forward(ghc_plan* p, const float* d_w, const float* d_x, const int32_t* d_y,
                        const int32_t* d_idx, int64_t n, float* d_probs, float* d_loss_sum) {
   if (n < 1) return fail(GHC_ERR_SHAPE, "batch: n_samples must be >= 1");

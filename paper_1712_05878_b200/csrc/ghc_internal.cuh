@@ -41,6 +41,7 @@ struct LstmEntry {
   void (*fn_round[3])(StepArgs);   // SIMT round kernel (lstm_round.cuh)
   void (*fn_res[3])(StepArgs);     // its resident-service variant (null for trunks)
   void (*fn_tc[3])(StepArgs);      // tensor-core cluster variant (lstm_tc.cuh); null: n/a
+  void (*fn_multi[3])(StepArgs);   // per-worker gradients in one launch (MULTI; null: n/a)
   int P, ppad, ep[3];
   size_t (*smem)(int);
   size_t (*smem_round[3])(int);
@@ -156,7 +157,7 @@ inline void step_geometry(const ghc_plan* p, int64_t n, int& ctas, int& warps) {
 // vr > 1: vr virtual ranks share the grid (cross-rank exchange, SIMT kernel),
 // each with max_clusters / vr clusters and n_max samples per round.
 inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 1,
-                              cudaStream_t stream = nullptr) {
+                              cudaStream_t stream = nullptr, bool multi = false) {
   if (!p->lstm) return fail(GHC_ERR_CONFIG, "plan has no fused worker kernel");
   if (a.res && !(p->use_cluster && p->max_clusters > 0 && !p->use_tc))
     return fail(GHC_ERR_CONFIG, "resident rounds need the SIMT cluster round kernel");
@@ -216,10 +217,11 @@ inline ghc_status launch_step(ghc_plan* p, StepArgs& a, int64_t n_max, int vr = 
       return e && e[0] == '1';
     }();
     cfg.numAttrs = no_coop ? 1 : 2;
-    void (*fn)(StepArgs) = tc ? p->lstm->fn_tc[p->cs_index]
-                              : (a.res ? p->lstm->fn_res[p->cs_index] : p->lstm->fn_round[p->cs_index]);
+    void (*fn)(StepArgs) = multi ? p->lstm->fn_multi[p->cs_index]
+                           : tc  ? p->lstm->fn_tc[p->cs_index]
+                                 : (a.res ? p->lstm->fn_res[p->cs_index] : p->lstm->fn_round[p->cs_index]);
     if (!fn) return fail(GHC_ERR_CONFIG, "no kernel variant for this launch");
-    if (a.res) {  // same shared-memory opt-in as the ordinary variant
+    if (a.res || multi) {  // same shared-memory opt-in as the ordinary variant
       CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(cfg.dynamicSmemBytes)));
     }

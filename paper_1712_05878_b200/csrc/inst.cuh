@@ -13,6 +13,13 @@ constexpr void (*tc_fn())(StepArgs) {
   else return nullptr;
 }
 
+// the per-worker-gradient variant (MULTI: session sync EASGD; head shapes, clusters of 4)
+template <int D, int H, int T, int K, bool HEAD>
+constexpr void (*multi_fn())(StepArgs) {
+  if constexpr (HEAD) return &lstm_round_kernel<D, H, T, K, 4, false, true>;
+  else return nullptr;
+}
+
 // the resident-service variant of the round kernel (head shapes only)
 template <int D, int H, int T, int K, int CS, bool HEAD>
 constexpr void (*res_fn())(StepArgs) {
@@ -38,6 +45,7 @@ LstmEntry make_entry(const char* name) {
                     &lstm_round_kernel<D, H, T, K, 2>},
                    {res_fn<D, H, T, K, 4, TC>(), res_fn<D, H, T, K, 8, TC>(), res_fn<D, H, T, K, 2, TC>()},
                    {tc_fn<D, H, T, K, 4, TC>(), tc_fn<D, H, T, K, 8, TC>(), nullptr},
+                   {multi_fn<D, H, T, K, TC>(), nullptr, nullptr},
                    N::P,
                    N::PPAD,
                    {R4::EP, R8::EP, R2::EP},

@@ -54,7 +54,7 @@ constexpr int kSamplesPerWarp = GHC_SPW;
 // tag sees the value: no fences, no flag barriers.  Rows are double-buffered
 // by epoch parity; a cluster reaches round r+2's stores only after every
 // cluster consumed round r (its round r+1 rows depend on them).
-template <int P, int SL, int EP, int CS>
+template <int P, int SL, int EP, int CS, bool MULTI = false>
 struct ClusterRS {
   static constexpr int E = P + 1;
   static constexpr int kRowBatch = 32;  // tagged cluster rows polled per batch (all of them for ≤ 32 clusters)
@@ -301,9 +301,14 @@ struct ClusterRS {
       }
       if (GX > 1) t = cross_rank_sum(a, xepoch & 1, e, t, xepoch);
       if (e == P) {
-        if (loss_out) loss_out[r] = t;
+        if constexpr (MULTI) {
+          if (loss_out) loss_out[vrank] = t;  // worker vrank's loss sum
+        } else {
+          if (loss_out) loss_out[r] = t;
+        }
       } else if (a.mode == MODE_GRAD) {
-        a.g_out[e] = t;
+        if constexpr (MULTI) a.g_out[vrank * a.g_vstride + e] = t;  // worker vrank's gradient
+        else a.g_out[e] = t;
       } else if (sgd) {
         // sgd_step (optim.cpp:59-60): v = mu*v - lr*g; w += v.  Each element
         // carries its own non-finite bit in its tag (2·epoch + bit); step (d)
@@ -683,7 +688,7 @@ struct ClusterXchg {
 
 // RES: the resident round service variant (commands from a.res); a separate
 // instantiation so the ordinary launch carries none of its state (registers).
-template <int D, int H, int T, int K, int CS, bool RES = false>
+template <int D, int H, int T, int K, int CS, bool RES = false, bool MULTI = false>
 __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   using N = LstmNet<D, H, T, K>;
   using RL = RoundLayout<D, H, T, K, CS>;
@@ -701,7 +706,7 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   float* ws = smem + 2 * RL::WBP + warp * SPW * N::WARP_FLOATS;  // SPW sample slots
   float* wpart = smem + 2 * RL::WBP + NW * SPW * N::WARP_FLOATS;  // [NW][PPAD]; [0] = CTA partial
   float* vsl = wpart + NW * N::PPAD;                           // [SL] velocity slice
-  ClusterRS<N::P, SL, RL::EP, CS> rs;  // the round's exchange (one GPU or GX ranks)
+  ClusterRS<N::P, SL, RL::EP, CS, MULTI> rs;  // the round's exchange (one GPU or GX ranks)
 #ifdef GHC_CHECKED
   {  // the host sized the launch's shared memory with the same layout
     unsigned dyn;
@@ -720,7 +725,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   }
   float* gw = sgd ? (cur ? a.w1 : a.w0) : nullptr;  // master weights in HBM
   float* gv = sgd ? (cur ? a.v1 : a.v0) : nullptr;
-  rs.load_state(sgd ? gw : a.w_in, gv, wbuf0);
+  if constexpr (MULTI) rs.load_state(a.w_in + rs.vrank * a.w_vstride, gv, wbuf0);  // worker vrank's weights
+  else rs.load_state(sgd ? gw : a.w_in, gv, wbuf0);
   cluster.sync();  // peers' mbarriers initialised before any st.async
   float* wa = wbuf0;  // weights the samples use
   float* wb = wbuf1;  // peers deposit the next weights here
@@ -734,10 +740,13 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
   const int Gr = G / max(1, a.VR);
   const int lb = blockIdx.x % Gr;
   const int GX = max(1, a.GX);
-  auto n_of = [&](int r, int q) { return a.counts ? __ldg(a.counts + (long long)r * GX + q) : a.n; };
+  auto n_of = [&](int r, int q) {
+    if constexpr (MULTI) return a.n_v[q];  // worker q's batch (one round)
+    return a.counts ? __ldg(a.counts + (long long)r * GX + q) : a.n;
+  };
   // Without per-round counts every round has the same sample range and scale:
   // computed once (the integer division by the CTA count is a serial chain).
-  const bool fixed_n = a.counts == nullptr;
+  const bool fixed_n = !MULTI && a.counts == nullptr;
   const int fs_spc = (a.n + Gr - 1) / Gr;
   const int fs_s0 = lb * fs_spc, fs_s1 = min(a.n, fs_s0 + fs_spc);
   auto first_sample = [&](int r, int& s, int& s1) {
@@ -839,7 +848,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
     srounds = cmd.rounds;
     sloss = cmd.loss_out;
   }
-  idxv = sidx ? sidx + (long long)rs.vrank * a.idx_vstride : nullptr;
+  if constexpr (MULTI) idxv = a.idx_v[rs.vrank];
+  else idxv = sidx ? sidx + (long long)rs.vrank * a.idx_vstride : nullptr;
   if (a.pipelined && srounds > 0 && !prefetched) {
     int s, s1;
     first_sample(0, s, s1);
@@ -861,7 +871,8 @@ __global__ void __launch_bounds__(256, 1) lstm_round_kernel(StepArgs a) {
       ntot = 0;
       for (int q = 0; q < GX; ++q) ntot += n_of(r, q);
     }
-    const float scale = sgd ? 1.0f / (float)ntot : a.grad_scale;
+    float scale = sgd ? 1.0f / (float)ntot : a.grad_scale;
+    if constexpr (MULTI) scale = 1.0f / (float)n_of(r, rs.rank);  // worker mean
     unsigned long long* pr =
         a.probe ? a.probe + ((long long)(RES ? (long long)rg : r) * gridDim.x + blockIdx.x) * 16 : nullptr;
     if (pr && threadIdx.x == 0) {

@@ -269,6 +269,14 @@ struct StepArgs {
   unsigned long long* tw;      // single-GPU exchange: tagged new weights [2][EP]
   unsigned* gcnt[kMaxRanks];   // per rank: line [CS*kFlagStride] keeps the exchange epoch
   ResidentCtl* res;            // non-null: resident round service (commands in res)
+  // ---- independent per-worker gradients in one launch (MULTI kernels) ----
+  // virtual rank v computes worker v's gradient at weights w_in + v·w_vstride
+  // over its own batch (rows idx_v[v][0 .. n_v[v])), scaled by 1/n_v[v], into
+  // g_out + v·g_vstride, its loss sum into loss_out[v]; no cross-rank sum.
+  const int32_t* idx_v[kMaxRanks];
+  int n_v[kMaxRanks];
+  long long w_vstride;
+  long long g_vstride;
 };
 
 // Grid barrier for the persistent round loop (gather → broadcast):

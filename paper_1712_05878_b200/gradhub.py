@@ -266,6 +266,21 @@ def worker_grad_device(arch: Architecture, w: DeviceArray, x: DeviceArray, y: De
                                        grad.ptr, loss_sum.ptr), "worker_grad")
 
 
+def worker_grads_device(arch: Architecture, w: DeviceArray, x: DeviceArray, y: DeviceArray | None,
+                        idx: list, n: list, grad: DeviceArray, loss: DeviceArray | None = None):
+    """ghc_worker_grads: len(n) independent worker gradients in one launch;
+    worker k at w[k] (rows of w = P each), rows idx[k] (a DeviceArray or None)
+    of x, scaled by 1/n[k], into grad[k]; loss sums into loss[k]."""
+    W = len(n)
+    P = arch.n_params
+    ptrs = (C.c_void_p * W)(*[i.ptr.value if i is not None else None for i in idx])
+    ns = (C.c_int32 * W)(*[int(v) for v in n])
+    check(arch.ctx.lib.ghc_worker_grads(arch.h, W, w.ptr, w.shape[1] if len(w.shape) > 1 else P, x.ptr,
+                                        y.ptr if y is not None else None, ptrs, ns, grad.ptr,
+                                        grad.shape[1] if len(grad.shape) > 1 else P,
+                                        loss.ptr if loss is not None else None), "worker_grads")
+
+
 def forward_backward(w: np.ndarray, arch: Architecture, x: np.ndarray, y: np.ndarray):
     """forward (nn.cpp:100) + loss (nn.cpp:234) + backward (nn.cpp:250) with
     host arrays: returns (mean gradient f32[P], loss).  Copy-in/copy-out."""

@@ -384,3 +384,30 @@ def test_master_streams_host_batches(ctx, B):
     assert ver1 == ver2 == R
     assert np.array_equal(w1, w2) and np.array_equal(v1, v2) and np.array_equal(w1, w3)
     assert np.array_equal(l1.numpy(), hl.np)
+
+
+@pytest.mark.parametrize("W,ns", [(8, [1000] * 8), (8, [1000, 999, 37, 1, 500, 1000, 64, 200]), (3, [250, 17, 1000])])
+def test_worker_grads_one_launch(ctx, W, ns):
+    """ghc_worker_grads (W workers' gradients in one launch, per-worker
+    weights and batches) vs W ghc_worker_grad calls: same values to fp32
+    rounding (the per-worker reduction order differs), loss sums likewise;
+    repeat → same bits."""
+    arch = g.Architecture(ctx, BENCH_ARCH)
+    P = arch.n_params
+    x, y = g.generate(g.data_spec(8, 1000))
+    rng = np.random.default_rng(W + sum(ns))
+    ws = np.stack([g.init_weights(arch, 7 + k) for k in range(W)]).astype(np.float32)
+    idxs = [rng.integers(0, len(y), size=n).astype(np.int32) for n in ns]
+    dx, dy, dw = ctx.upload(x), ctx.upload(y), ctx.upload(ws)
+    di = [ctx.upload(i) for i in idxs]
+    grad, loss = ctx.array((W, P)), ctx.array(W)
+    g.worker_grads_device(arch, dw, dx, dy, di, ns, grad, loss)
+    G, L = grad.numpy(), loss.numpy()
+    for k in range(W):
+        gk, lk = ctx.array(P), ctx.array(1)
+        g.worker_grad_device(arch, ctx.upload(ws[k]), dx, dy, ns[k], gk, lk, idx=di[k])
+        ref = gk.numpy()
+        assert np.linalg.norm(G[k] - ref) / np.linalg.norm(ref) <= 1e-6, k
+        assert abs(L[k] - lk.numpy()[0]) <= 1e-5 * abs(lk.numpy()[0]), k
+    g.worker_grads_device(arch, dw, dx, dy, di, ns, grad, loss)
+    assert np.array_equal(grad.numpy(), G)
