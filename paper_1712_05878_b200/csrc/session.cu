@@ -59,6 +59,44 @@ __global__ void __launch_bounds__(256) easgd_exchange_kernel(float* __restrict__
   finish_rejecting(ms, rej, nullptr, (exchange && !rej) ? cver : nullptr, nullptr);
 }
 
+// One sync EASGD round's exchanges (workers 0..R-1 in rank order) in ONE
+// single-CTA launch for small P (the bench net: 2,143 parameters — the R
+// cooperative easgd_exchange_kernel launches were ~10 µs of launch each):
+// the same per-element arithmetic in the same order, the center's updates
+// ordered by a CTA barrier between workers; a non-finite gradient stops the
+// round at that worker (err bit 2), as the per-worker kernels do.
+__global__ void __launch_bounds__(1024) easgd_round_kernel(float* __restrict__ ww, long long w_stride,
+                                                           float* __restrict__ c, const float* __restrict__ g0,
+                                                           long long g_stride, long long P, float lr,
+                                                           float alpha, unsigned exch_mask, int R, int* err,
+                                                           unsigned long long* cver) {
+  if (__ldcg(err) & 2) return;
+  for (int k = 0; k < R; ++k) {
+    const float* g = g0 + k * g_stride;
+    float* w = ww + k * w_stride;
+    int bad = 0;
+    for (long long i = threadIdx.x; i < P; i += blockDim.x) bad |= is_finite_f(__ldcg(g + i)) ? 0 : 1;
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) atomicOr(err, 2);  // GHC_ERR_NONFINITE: the worker aborts (optim.cpp:90-92)
+      return;
+    }
+    const bool exchange = (exch_mask >> k) & 1u;
+    for (long long i = threadIdx.x; i < P; i += blockDim.x) {
+      float w1 = w[i];
+      w1 -= lr * __ldcg(g + i);
+      if (exchange) {
+        float cv = c[i];
+        cv += alpha * (w1 - cv);
+        c[i] = cv;
+        w1 -= alpha * (w1 - cv);
+      }
+      w[i] = w1;
+    }
+    __syncthreads();  // this worker's center update before the next worker's
+    if (exchange && threadIdx.x == 0) ++*cver;
+  }
+}
+
 // out = a - b (hierarchical pseudo-gradient: snapshot - current)
 __global__ void sub_kernel(float* __restrict__ out, const float* __restrict__ a,
                            const float* __restrict__ b, long long P) {
@@ -108,6 +146,8 @@ struct ghc_session {
   float* worker_w = nullptr;                 // [W][P] worker copies (async / EASGD)
   float* center = nullptr;                   // EASGD center
   float* scratch_g = nullptr;                // [P+1] one worker gradient (+ loss)
+  float* multi_g = nullptr;                  // [W][Pp] one round's worker gradients (sync EASGD)
+  float* multi_l = nullptr;                  // [W] their loss sums
   float* snap = nullptr;                     // [G][P] flush snapshots
   float* pseudo = nullptr;                   // [G][P]
   float* comb = nullptr;                     // [P]
@@ -313,8 +353,14 @@ ghc_status run_sync(ghc_session* s, float* h_loss) {
   return st;
 }
 
+// sync_rounds: `order` is the sync EASGD round-robin (each round every active
+// worker once, in rank order).  A worker's gradient then depends only on its
+// own weights, fixed since its previous step, so a round's gradients are
+// computed up front in ONE launch (ghc_worker_grads) when the round's
+// workers are 0..R-1 (contiguous weight rows); the exchanges stay serial in
+// rank order.
 ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, float* h_loss,
-                      int64_t* h_stale) {
+                      int64_t* h_stale, bool sync_rounds = false) {
   ghc_ctx* c = s->plan->ctx;
   const int64_t P = s->P;
   std::vector<float*> loss_dst;
@@ -329,16 +375,95 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
     CU(cudaMalloc(&d_stale, sizeof(long long) * (n_order > 0 ? n_order : 1)));
     CU(cudaMemcpy(&samples0, s->d_samples, sizeof(samples0), cudaMemcpyDeviceToHost));
   }
+  const int64_t Pp = (P + 4) & ~3LL;  // multi_g row stride (16-B rows)
+  int64_t round_end = 0, round_begin = 0;
+  bool round_multi = false;
+  std::vector<int32_t> round_n;
   for (int64_t step = 0; step < n_order; ++step) {
     const int k = order[step];
     if (k < 0 || k >= s->W) return fail(GHC_ERR_PROTOCOL, "replay order names an unknown worker");
     float* wk = s->worker_w + static_cast<int64_t>(k) * P;
+    if (sync_rounds && !downpour && step == round_end) {
+      // the next round: the run of strictly increasing worker ids from here
+      round_begin = step;
+      round_end = step;
+      while (round_end < n_order && (round_end == step || order[round_end] > order[round_end - 1])) ++round_end;
+      const int R = static_cast<int>(round_end - round_begin);
+      round_multi = R > 1 && R <= kMaxRanks;
+      for (int i = 0; i < R && round_multi; ++i) round_multi = order[round_begin + i] == i;  // workers 0..R-1
+      if (round_multi) {
+        std::vector<const int32_t*> idx(static_cast<size_t>(R));
+        round_n.assign(static_cast<size_t>(R), 0);
+        for (int i = 0; i < R; ++i) {
+          auto& cur = s->cursor[static_cast<size_t>(i)];
+          const auto& bl = s->batches[static_cast<size_t>(i)];
+          if (cur >= bl.size()) return fail(GHC_ERR_PROTOCOL, "replay order uses a worker that already sent DONE");
+          const Batch b = bl[cur++];
+          idx[static_cast<size_t>(i)] = s->streams + s->stream_off[static_cast<size_t>(i)] + b.off;
+          round_n[static_cast<size_t>(i)] = b.n;
+        }
+        if (!s->multi_g) {
+          CU(cudaMalloc(&s->multi_g, sizeof(float) * static_cast<size_t>(kMaxRanks * Pp)));
+          CU(cudaMalloc(&s->multi_l, sizeof(float) * kMaxRanks));
+        }
+        if (ghc_status st = ghc_worker_grads(s->plan, R, s->worker_w, P, s->X, s->Y, idx.data(),
+                                             round_n.data(), s->multi_g, Pp, s->multi_l))
+          return st;
+      }
+    }
+    if (round_multi && step == round_begin && P <= (1LL << 16)) {
+      // the whole round's host bookkeeping, then ONE exchange launch — unless
+      // a validation falls inside the round (it must see the center between
+      // two workers' exchanges): then the per-worker path below
+      const int R = static_cast<int>(round_end - round_begin);
+      unsigned mask = 0;
+      int64_t v = version;
+      bool val_inside = false;
+      for (int i = 0; i < R; ++i) {
+        const uint64_t bi = s->bidx[static_cast<size_t>(i)];
+        if ((bi % static_cast<uint64_t>(s->cfg.tau)) == 0) {
+          mask |= 1u << i;
+          ++v;
+          if (s->v_every > 0 && v % s->v_every == 0) val_inside = true;
+        }
+      }
+      if (!val_inside) {
+        for (int i = 0; i < R; ++i) {
+          const int64_t st_i = round_begin + i;
+          const int32_t ni = round_n[static_cast<size_t>(i)];
+          counts.push_back(ni);
+          CU(cudaMemcpyAsync(d_loss + st_i, s->multi_l + i, sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+          s->samples += ni;
+          s->bidx[static_cast<size_t>(i)]++;
+          const bool exch = (mask >> i) & 1u;
+          if (h_stale && st_i < s->trace_cap) h_stale[st_i] = exch ? version - s->basis[static_cast<size_t>(i)] : 0;
+          if (exch) {
+            ++version;
+            s->basis[static_cast<size_t>(i)] = version;
+          }
+        }
+        easgd_round_kernel<<<1, 1024, 0, c->stream>>>(s->worker_w, P, s->center, s->multi_g, Pp, P, s->cfg.lr,
+                                                      s->cfg.alpha, mask, R, s->err, s->cver);
+        CU(cudaGetLastError());
+        c->launches++;
+        step = round_end - 1;
+        continue;
+      }
+    }
     int32_t n = 0;
-    if (ghc_status st = worker_step(s, k, wk, n)) return st;
-    if (n == 0) return fail(GHC_ERR_PROTOCOL, "replay order uses a worker that already sent DONE");
+    const float* g_step = s->scratch_g;
+    if (round_multi) {
+      const int i = static_cast<int>(step - round_begin);
+      n = round_n[static_cast<size_t>(i)];
+      g_step = s->multi_g + i * Pp;
+      CU(cudaMemcpyAsync(d_loss + step, s->multi_l + i, sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      if (ghc_status st = worker_step(s, k, wk, n)) return st;
+      if (n == 0) return fail(GHC_ERR_PROTOCOL, "replay order uses a worker that already sent DONE");
+      CU(cudaMemcpyAsync(d_loss + step, s->scratch_g + P, sizeof(float), cudaMemcpyDeviceToDevice,
+                         c->stream));
+    }
     counts.push_back(n);
-    CU(cudaMemcpyAsync(d_loss + step, s->scratch_g + P, sizeof(float), cudaMemcpyDeviceToDevice,
-                       c->stream));
     if (downpour) {
       // sgd_step at the master, reply to the sender only;
       // staleness / basis / samples follow the device's accepted count
@@ -365,7 +490,7 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
       if (h_stale && step < s->trace_cap)
         h_stale[step] = exch ? version - s->basis[static_cast<size_t>(k)] : 0;
       float* cc = s->center;
-      const float* g = s->scratch_g;
+      const float* g = g_step;
       long long PP = P;
       float lr = s->cfg.lr, alpha = s->cfg.alpha;
       MasterDev* ms = s->ms;
@@ -615,6 +740,8 @@ void ghc_session_destroy(ghc_session* s) {
   cudaFree(s->worker_w);
   cudaFree(s->center);
   cudaFree(s->scratch_g);
+  cudaFree(s->multi_g);
+  cudaFree(s->multi_l);
   cudaFree(s->snap);
   cudaFree(s->pseudo);
   cudaFree(s->comb);
@@ -633,6 +760,7 @@ ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_ord
   s->trace_cap = trace_cap < 0 ? 0 : trace_cap;
   ghc_status st;
   std::vector<int32_t> rr;
+  bool sync_order = false;  // rr: the sync EASGD round-robin (run_replay batches each round's gradients)
   if (s->cfg.groups > 0) {
     st = run_hier(s, h_loss);
   } else if (s->cfg.mode == GHC_MODE_SYNC && s->cfg.algo == GHC_ALGO_DOWNPOUR) {
@@ -655,8 +783,9 @@ ghc_status ghc_session_run(ghc_session* s, const int32_t* h_order, int64_t n_ord
       }
       h_order = rr.data();
       n_order = static_cast<int64_t>(rr.size());
+      sync_order = true;
     }
-    st = run_replay(s, h_order, n_order, h_loss, h_staleness);
+    st = run_replay(s, h_order, n_order, h_loss, h_staleness, sync_order);
   }
   if (st != GHC_OK) return st;
   int err = 0;
