@@ -59,6 +59,65 @@ __global__ void __launch_bounds__(256) easgd_exchange_kernel(float* __restrict__
   finish_rejecting(ms, rej, nullptr, (exchange && !rej) ? cver : nullptr, nullptr);
 }
 
+// One replayed async Downpour step's master side in ONE single-CTA launch for
+// small P (replay_pre + sgd_db + db_fixup + replay_post + the reply copy were
+// five stream operations of a few µs each): staleness against the sender's
+// basis, the whole-update reject on a non-finite gradient (optim.cpp:49-53),
+// sgd_step (optim.cpp:59-60: v = μv − ηg, w += v — the arithmetic of
+// sgd_pass) into the other double buffer (a reject copies the old state
+// there, as db_fixup does; the buffers flip either way, det mode), the
+// version / rejected / status counters, the sender's new basis and samples,
+// and the reply: the new weights into the sender's copy wk.
+__global__ void __launch_bounds__(1024) replay_apply_kernel(float* const* __restrict__ wb,
+                                                            float* const* __restrict__ vb,
+                                                            const float* __restrict__ g, long long P,
+                                                            float lr, float mu, MasterDev* ms,
+                                                            unsigned long long* basis, int k,
+                                                            long long* stale_out, unsigned long long* samples,
+                                                            int n, float* __restrict__ wk) {
+  __shared__ int s_cur;
+  if (threadIdx.x == 0) {
+    s_cur = ms->cur;
+    *stale_out = (long long)(ms->version - basis[k]);
+  }
+  __syncthreads();
+  const int cur = s_cur;
+  const float* w = wb[cur];
+  const float* v = vb[cur];
+  float* w2 = wb[cur ^ 1];
+  float* v2 = vb[cur ^ 1];
+  int bad = 0;
+  for (long long i = threadIdx.x; i < P; i += blockDim.x) bad |= isfinite(g[i]) ? 0 : 1;
+  bad = __syncthreads_or(bad);
+  for (long long i = threadIdx.x; i < P; i += blockDim.x) {
+    if (bad) {
+      const float wi = w[i];
+      w2[i] = wi;
+      v2[i] = v[i];
+      wk[i] = wi;
+    } else {
+      const float vn = fmaf(mu, v[i], -lr * g[i]);
+      const float wn = w[i] + vn;
+      v2[i] = vn;
+      w2[i] = wn;
+      wk[i] = wn;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ms->cur = cur ^ 1;
+    if (bad) {
+      ms->rejected += 1ull;
+      ms->status = 2;  // GHC_ERR_NONFINITE
+    } else {
+      ms->version += 1ull;
+      ms->status = 0;
+      *samples += (unsigned long long)n;
+    }
+    basis[k] = ms->version;
+  }
+}
+
 // One sync EASGD round's exchanges (workers 0..R-1 in rank order) in ONE
 // single-CTA launch for small P (the bench net: 2,143 parameters — the R
 // cooperative easgd_exchange_kernel launches were ~10 µs of launch each):
@@ -467,14 +526,27 @@ ghc_status run_replay(ghc_session* s, const int32_t* order, int64_t n_order, flo
     if (downpour) {
       // sgd_step at the master, reply to the sender only;
       // staleness / basis / samples follow the device's accepted count
-      replay_pre_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, d_stale + step);
-      if (ghc_status st = apply_master(s, s->master, s->scratch_g, s->cfg.lr, s->cfg.mu))
-        return st;
-      replay_post_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, s->d_samples, n);
-      c->launches += 2;
-      CU(cudaGetLastError());
-      CU(cudaMemcpyAsync(wk, master_w(s->master), sizeof(float) * P, cudaMemcpyDeviceToDevice,
-                         c->stream));
+      if (P <= (1LL << 16)) {
+        ghc_master* m = s->master;
+        int cur = 0;
+        if (ghc_status st = ghc_master_current(m, &cur)) return st;
+        replay_apply_kernel<<<1, 1024, 0, c->stream>>>(m->bufs, m->bufs + 2, s->scratch_g, P, s->cfg.lr,
+                                                       s->cfg.mu, m->ms, s->d_basis, k, d_stale + step,
+                                                       s->d_samples, n, wk);
+        CU(cudaGetLastError());
+        c->launches++;
+        m->host_cur = cur ^ 1;  // the buffers flip on every step (det mode)
+        m->host_cur_known = true;
+      } else {
+        replay_pre_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, d_stale + step);
+        if (ghc_status st = apply_master(s, s->master, s->scratch_g, s->cfg.lr, s->cfg.mu))
+          return st;
+        replay_post_kernel<<<1, 1, 0, c->stream>>>(s->master->ms, s->d_basis, k, s->d_samples, n);
+        c->launches += 2;
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(wk, master_w(s->master), sizeof(float) * P, cudaMemcpyDeviceToDevice,
+                           c->stream));
+      }
       if (s->v_every > 0) {  // the cadence needs the accepted count (serial)
         uint64_t ver = 0;
         CU(cudaMemcpyAsync(&ver, &s->master->ms->version, sizeof(ver), cudaMemcpyDeviceToHost,
